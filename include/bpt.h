@@ -1,0 +1,195 @@
+/*
+ * bpt.h -- C-ABI of the B200-native fused breadth-first probabilistic traversal (BPT)
+ * library: IMM reverse-reachable (RRR) set sampling with up to 64 fused colours per
+ * traversal group, plus greedy max-k-cover seed selection.
+ *
+ * Paper: "Fused Breadth-First Probabilistic Traversals on Distributed GPU Systems"
+ * (arXiv 2311.10201). Citations P:n are lines of its PAPER.md; C-k are the readings
+ * listed in DESIGN.md ("Readings of the paper").
+ *
+ * Conventions (apply to every call):
+ *   - Every call returns bpt_status; BPT_OK = 0. On error the outputs are untouched and
+ *     bpt_last_error() returns a thread-local, human-readable message.
+ *   - Pointer arguments are plain pointers to HOST or DEVICE memory; the library
+ *     detects which (cudaPointerGetAttributes). Input arrays are caller-owned and
+ *     copied: the library never retains a caller pointer after the call returns.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *     Calls are synchronous with respect to the host on return (results are ready).
+ *   - Handles own their device memory until the matching *_free (NULL-safe).
+ *   - Sample ids s are GLOBAL: s in [0, theta). Traversal group = C consecutive samples
+ *     (s = g*C + c, colour c = bit c mod 64 of the 64-sample block s/64, reading C-9).
+ *   - No CPU fallback: if no CUDA device is usable every call fails with BPT_ECUDA.
+ */
+#ifndef BPT_H
+#define BPT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BPT_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define BPT_API __attribute__((visibility("default")))
+#else
+#define BPT_API
+#endif
+
+typedef enum {
+    BPT_OK = 0,
+    BPT_EINVAL = -1,   /* invalid argument (message names it) */
+    BPT_ENOMEM = -2,   /* device allocation failed, or a caller buffer is too small */
+    BPT_ECUDA = -3,    /* CUDA runtime error (message carries cudaGetErrorString) */
+    BPT_ENCCL = -4,    /* NCCL error (message carries ncclGetErrorString) */
+    BPT_ESTATE = -5    /* call out of order / handle mismatch */
+} bpt_status;
+
+/* Diffusion models: independent cascade, linear threshold (reading C-6). */
+typedef enum { BPT_IC = 0, BPT_LT = 1 } bpt_model;
+
+typedef struct bpt_comm bpt_comm;
+typedef struct bpt_graph bpt_graph;
+typedef struct bpt_samples bpt_samples;
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+BPT_API const char* bpt_last_error(void);
+BPT_API int bpt_abi_version(void);
+
+/* ---------------------------------------------------------------------------------
+ * Communicator (one process per GPU). world == 1 needs no NCCL id.
+ * bpt_comm_unique_id writes a 128-byte ncclUniqueId (call on rank 0, broadcast it
+ * with any transport, e.g. torch.distributed). cuda_device is the device ordinal this
+ * rank uses; every later call on handles derived from this comm runs on that device.
+ * Errors: EINVAL (world < 1, rank outside [0, world), uid NULL with world > 1),
+ * ENCCL, ECUDA.
+ * ------------------------------------------------------------------------------- */
+BPT_API bpt_status bpt_comm_unique_id(void* uid_out /* 128 bytes, host */);
+BPT_API bpt_status bpt_comm_init(const void* nccl_uid, int world, int rank, int cuda_device, bpt_comm** out);
+BPT_API void bpt_comm_free(bpt_comm* comm);
+
+/* ---------------------------------------------------------------------------------
+ * bpt_graph_load -- A0 + A1: validate a FORWARD CSR with per-edge weights, copy it to
+ * the device and build the reverse CSR the BPTs traverse (Def. 2: a BPT
+ * from v over the transpose visits exactly the u with a path u ~> v).
+ *   row_ptr[n+1] u64: forward rows; col[m] u32: destinations; edge (u, col[e]) for
+ *     e in [row_ptr[u], row_ptr[u+1]). Duplicates and self-loops are accepted (each
+ *     parallel edge is its own coin, reading C-15).
+ *   Weights: exactly one of w_f32[m] (probability in [0,1]; converted to Q1.31 as
+ *     floor(p * 2^31), reading C-5) or w_q31[m] (thresholds in [0, 2^31], p = thr/2^31).
+ *   model: BPT_IC keeps per-edge thresholds; BPT_LT requires, for every vertex v, the
+ *     sum of the thresholds of v's in-edges to be <= 2^31 (reading C-6) and stores
+ *     the per-row inclusive prefix instead.
+ *   Canonical reverse order (reading C-4): rows by destination; within a row, entries
+ *     in forward position order. The edge id used by the coins is the position in
+ *     this reverse CSR.
+ *   comm may be NULL (single GPU: current device).
+ * Errors: EINVAL if n == 0, m >= 2^32, row_ptr[0] != 0, row_ptr not non-decreasing,
+ *   row_ptr[n] != m, any col >= n, any weight outside its range (NaN included), both
+ *   or neither weight arrays given, or an LT row sum > 2^31 (message names the vertex);
+ *   ENOMEM; ECUDA.
+ * ------------------------------------------------------------------------------- */
+BPT_API bpt_status bpt_graph_load(bpt_comm* comm, const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                          uint64_t m, const float* w_f32, const uint32_t* w_q31, bpt_model model,
+                          void* stream, bpt_graph** out);
+/* Export the reverse CSR (tests): roff[n+1], src[m], val[m] (IC: threshold; LT: cumulative
+ * threshold). Any pointer may be NULL. Host or device buffers. */
+BPT_API bpt_status bpt_graph_reverse(const bpt_graph* g, uint32_t* roff, uint32_t* src, uint32_t* val);
+BPT_API bpt_status bpt_graph_dims(const bpt_graph* g, uint32_t* n, uint64_t* m, int* model);
+BPT_API void bpt_graph_free(bpt_graph* g);
+
+/* ---------------------------------------------------------------------------------
+ * bpt_sample -- A2..A5: sample theta RRR sets with `colors` BPTs fused per traversal
+ * group (Listing 1), level-synchronous (reading C-7).
+ *   Start vertex of sample s: reading C-3 ("selected uniformly at random from V").
+ *   IC coin of sample s on reverse edge e: Philox2x32-10 keyed by (seed, s, e), edge live
+ *     iff (r >> 1) < thr(e) (readings C-1, C-2). LT: one draw per (s, v) picks <= 1
+ *     in-edge (reading C-6).
+ *   Result: RRR sets stored in fused form (per 64-sample block, a u64 colour mask per
+ *     vertex = Listing 1's visited[]), plus per-sample sizes and digests
+ *     (DESIGN.md "Digest"). RRR sets are identical for any colors, batch size and number
+ *     of ranks (readings C-9, C-14).
+ *   colors must divide 64 (1, 2, 4, 8, 16, 32, 64). theta in [1, 2^32).
+ *   Multi-rank: every rank calls with identical arguments; rank r samples the 64-sample
+ *     blocks [floor(r*nb/W), floor((r+1)*nb/W)), nb = ceil(theta/64). No communication.
+ * Errors: EINVAL (theta, colors, model != graph model), ENOMEM (store does not fit),
+ *   ECUDA.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t batch_groups;   /* 64-sample blocks traversed concurrently; 0 = automatic */
+    uint32_t poll_levels;    /* levels launched between host polls; 0 = automatic */
+    uint32_t flags;          /* BPT_FLAG_* */
+    uint32_t reserved;
+} bpt_sample_opts;
+#define BPT_FLAG_PROFILE 1u  /* time every expansion launch with CUDA events */
+
+BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
+                      void* stream, bpt_samples** out);
+BPT_API bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
+                         const bpt_sample_opts* opts, void* stream, bpt_samples** out);
+
+typedef struct {
+    uint64_t theta, seed, s0, s1;          /* this rank owns global samples [s0, s1) */
+    uint32_t colors, model, world, rank;
+    uint32_t n, batch_groups, batches, levels_max;  /* levels_max: deepest batch */
+    uint64_t e_phys;        /* IC: reverse-edge records read by the fused expansion;
+                               LT: (vertex, colour) expansions = sum |RR_s| */
+    uint64_t e_logical;     /* IC: sum_s sum_{v in RR_s} indeg(v) (unfused reads); LT: sum |RR_s| */
+    uint64_t members;       /* sum_s |RR_s| over this rank's samples */
+    uint64_t levels_total;  /* sum over batches of levels traversed */
+    uint64_t frontier_entries; /* (vertex, slice) frontier entries expanded */
+    uint64_t coins;         /* coin evaluations (schedule-dependent, informational) */
+    uint64_t atomics;       /* atomicOr merges issued (schedule-dependent) */
+    uint64_t store_bytes;   /* bytes of the fused RRR store on this rank */
+    uint64_t kernel_launches;
+    uint64_t expand_launches;
+    double ms_total;        /* host wall time of bpt_sample */
+    double ms_expand;       /* sum of CUDA-event times of expansion launches (BPT_FLAG_PROFILE) */
+    double expand_bytes;    /* algorithmic bytes moved by expansion launches */
+} bpt_samples_info;
+
+BPT_API bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* out);
+
+/* Per level of every batch: {batch, level, raw_entries, kept_entries, edges_or_tasks, vc_pairs}
+ * as 6 u64 per row, host buffer. *rows = number of rows available (written if rows_out != NULL). */
+BPT_API bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_rows, uint64_t* rows_out);
+
+/* ---------------------------------------------------------------------------------
+ * A5/A6: per-sample results for global sample ids [first, first+count), which must lie
+ * in this rank's range (else EINVAL).
+ *   sizes[count] u32 = |RR_s|; digests[count] u64 = sum over v in RR_s of
+ *   splitmix64(v) mod 2^64.
+ *   bpt_rrr_extract: Listing 1 lines 18-21 -- RRR lists, sorted ascending,
+ *   start included (reading C-10). offsets[count+1] u64 (offsets[0] = 0), members
+ *   u32[capacity]. If capacity < offsets[count] -> ENOMEM (message gives the size) and
+ *   nothing is written.
+ * ------------------------------------------------------------------------------- */
+BPT_API bpt_status bpt_rrr_sizes(const bpt_samples* s, uint64_t first, uint64_t count, uint32_t* sizes);
+BPT_API bpt_status bpt_rrr_digests(const bpt_samples* s, uint64_t first, uint64_t count, uint64_t* digests);
+BPT_API bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count, uint64_t* offsets,
+                           uint32_t* members, uint64_t capacity);
+
+/* ---------------------------------------------------------------------------------
+ * bpt_select_seeds -- A7/A8: greedy max-k-cover over all theta RRR sets:
+ * each round picks the vertex covering the most uncovered sets, smallest id on ties,
+ * smallest unselected id once everything is covered (reading C-11).
+ *   seeds[k] u32, gains[k] u64 (sets newly covered per round), *sigma_hat =
+ *   n * sum(gains) / theta (f64, reading C-12). Any output may be NULL. Host or device.
+ *   Collective across the comm (same result on every rank). Does not modify the store:
+ *   may be called again with another k.
+ * Errors: EINVAL (k == 0 or k > n), ENCCL, ECUDA.
+ * ------------------------------------------------------------------------------- */
+BPT_API bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* seeds, uint64_t* gains,
+                            double* sigma_hat);
+
+BPT_API void bpt_samples_free(bpt_samples* s);
+
+/* Library-wide count of kernels launched by this process (evidence for gpu_launches). */
+BPT_API uint64_t bpt_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPT_H */

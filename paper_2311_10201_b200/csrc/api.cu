@@ -1,0 +1,589 @@
+// api.cu -- the C-ABI of include/bpt.h and the host orchestration of the hot path:
+// argument checks, host/device pointer handling, sample-range sharding, batch planning,
+// the device-resident level loop with pipelined polling, and statistics.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+
+#include "internal.cuh"
+
+namespace bpt {
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_last_error;
+uint64_t g_launches = 0;
+
+void fail(bpt_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) fail(BPT_ENOMEM, std::string("device allocation failed: ") + what);
+    fail(BPT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevBuf::alloc(size_t b) {
+    reset();
+    if (b == 0) b = 8;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation)
+            fail(BPT_ENOMEM, "cudaMalloc of " + std::to_string(b) + " bytes failed (out of device memory)");
+        fail(BPT_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    bytes = b;
+}
+void DevBuf::reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+int num_sms() {
+    int dev = 0, sms = 0;
+    BPT_CUDA(cudaGetDevice(&dev));
+    BPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+
+// launchers defined in other translation units
+uint32_t expand_tile();
+void launch_compact(const BatchArgs& a, int level, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st);
+void launch_expand(const BatchArgs& a, int level, const uint32_t* tstart, cudaStream_t st);
+void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
+                   cudaStream_t st);
+void comm_unique_id(void* out);
+void comm_init(Comm* c, const void* uid);
+void comm_destroy(Comm* c);
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// device view of a caller array: the pointer itself if on the device, else a copy
+struct DevIn {
+    DevBuf buf;
+    const void* p = nullptr;
+    DevIn(const void* src, size_t bytes, cudaStream_t st) {
+        if (!src) return;
+        if (is_device_ptr(src)) { p = src; return; }
+        buf.alloc(bytes);
+        BPT_CUDA(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, st));
+        p = buf.p;
+    }
+};
+
+void copy_out(void* dst, const void* dsrc, size_t bytes, cudaStream_t st) {
+    if (!dst || !bytes) return;
+    BPT_CUDA(cudaMemcpyAsync(dst, dsrc, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+}
+
+void use_device(int dev) {
+    int cur = -1;
+    BPT_CUDA(cudaGetDevice(&cur));
+    if (cur != dev) BPT_CUDA(cudaSetDevice(dev));
+}
+
+template <class F>
+bpt_status guarded(F&& f) {
+    try {
+        f();
+        return BPT_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return BPT_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BPT_ECUDA;
+    }
+}
+
+constexpr int kMaxLevels = 8192;
+
+struct PinnedRing {  // pinned host staging for level records
+    LevelRec* p = nullptr;
+    size_t cap = 0;
+    ~PinnedRing() { if (p) cudaFreeHost(p); }
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        size_t c = std::max(n, cap * 2);
+        BPT_CUDA(cudaMallocHost(&p, c * sizeof(LevelRec)));
+        cap = c;
+    }
+};
+
+struct EventPair { cudaEvent_t a, b; };
+
+}  // namespace
+
+// ------------------------------------------------------------------ sampling driver
+static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st) {
+    const Graph& g = *S.g;
+    const uint32_t n = g.n;
+    const uint32_t C = S.colors;
+    const uint64_t slices = 64 / C;
+    const auto t_begin = std::chrono::steady_clock::now();
+    const uint64_t launches0 = g_launches;
+
+    // ---- store + per-sample outputs
+    S.count0.alloc((size_t)S.n_pad * 4);
+    BPT_CUDA(cudaMemsetAsync(S.count0.p, 0, (size_t)S.n_pad * 4, st));
+    if (S.blocks == 0) {  // this rank owns no samples; it still joins the selection collectives
+        BPT_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    S.store.alloc((size_t)S.blocks * n * 8);
+    BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
+    const uint64_t nlocal = S.s1 - S.s0;
+    S.sizes.alloc(nlocal * 4);
+    S.digests.alloc(nlocal * 8);
+    BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
+    BPT_CUDA(cudaMemsetAsync(S.digests.p, 0, nlocal * 8, st));
+
+    // ---- batch plan
+    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 8 : 512);
+    uint64_t slots = umin64(umax64(want, 1), S.blocks);
+    const uint32_t tile = expand_tile();
+    auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
+        raw_cap = umin64(sl * slices * n, (1ull << 28) - 1);
+        q_cap = raw_cap;
+        const uint64_t work = S.model == BPT_IC ? umin64(sl * slices * g.m, kEdgeMask)
+                                                : umin64(sl * 64 * n, kEdgeMask);
+        ts_cap = work / tile + 2;
+        return sl * (uint64_t)n * 8 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 4;
+    };
+    size_t free_b = 0, total_b = 0;
+    BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t raw_cap = 0, q_cap = 0, ts_cap = 0;
+    while (slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
+    plan_bytes(slots, raw_cap, q_cap, ts_cap);
+
+    DevBuf N((size_t)slots * n * 8), raw(raw_cap * 8), q(q_cap * 16), qoff(q_cap * 8), tstart(ts_cap * 4),
+        lv((size_t)kMaxLevels * sizeof(LevelRec)), elog(8);
+    BPT_CUDA(cudaMemsetAsync(N.p, 0, N.bytes, st));
+    BPT_CUDA(cudaMemsetAsync(elog.p, 0, 8, st));
+
+    BatchArgs a{};
+    a.roff = g.roff.as<uint32_t>();
+    a.rec = g.rec.as<uint2>();
+    a.n = n;
+    a.model = S.model;
+    a.colors = C;
+    a.store = S.store.as<uint64_t>();
+    a.N = N.as<uint64_t>();
+    a.raw = raw.as<unsigned long long>();
+    a.raw_cap = raw_cap;
+    a.q = q.as<uint4>();
+    a.qoff = qoff.as<uint64_t>();
+    a.q_cap = q_cap;
+    a.lv = lv.as<LevelRec>();
+    a.theta = S.theta;
+    a.k_ic = stream_key(S.seed, kTagIC);
+    a.k_lt = stream_key(S.seed, kTagLT);
+    a.k_start = stream_key(S.seed, kTagStart);
+
+    const uint32_t K = opt.poll_levels ? opt.poll_levels : (S.model == BPT_IC ? 3 : 16);
+    const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
+    std::vector<EventPair> evs;
+    size_t ev_used = 0;
+    auto next_events = [&]() -> EventPair& {
+        if (ev_used == evs.size()) {
+            EventPair e{};
+            BPT_CUDA(cudaEventCreate(&e.a));
+            BPT_CUDA(cudaEventCreate(&e.b));
+            evs.push_back(e);
+        }
+        return evs[ev_used++];
+    };
+    cudaEvent_t poll_ev[2];
+    BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
+    BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
+    LevelRec* poll_host = nullptr;
+    BPT_CUDA(cudaMallocHost(&poll_host, 2 * sizeof(LevelRec)));
+    PinnedRing ring;
+    const uint64_t nbatches = (S.blocks + slots - 1) / slots;
+    ring.ensure(nbatches * 48);
+    std::vector<std::pair<size_t, int>> batch_rows;  // (ring offset, levels launched)
+    size_t ring_used = 0;
+
+    struct Cleanup {
+        std::vector<EventPair>* evs; cudaEvent_t* pe; LevelRec* ph;
+        ~Cleanup() {
+            for (auto& e : *evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+            cudaEventDestroy(pe[0]); cudaEventDestroy(pe[1]);
+            cudaFreeHost(ph);
+        }
+    } cleanup{&evs, poll_ev, poll_host};
+
+    uint64_t levels_max = 0;
+    for (uint64_t b0 = 0; b0 < S.blocks; b0 += slots) {
+        const uint32_t bs = (uint32_t)umin64(slots, S.blocks - b0);
+        a.blk0 = b0;
+        a.gblk0 = S.gb0 + b0;
+        a.slots = bs;
+        BPT_CUDA(cudaMemsetAsync(lv.p, 0, lv.bytes, st));
+        launch_init(a, st);
+        int L = 0, cur = 0;
+        bool have_prev = false, done = false;
+        while (!done) {
+            if (L + (int)K + 1 >= kMaxLevels) fail(BPT_ENOMEM, "level loop exceeded " + std::to_string(kMaxLevels) + " levels");
+            for (uint32_t i = 0; i < K; ++i, ++L) {
+                launch_compact(a, L, tstart.as<uint32_t>(), ts_cap, st);
+                if (profile) {
+                    EventPair& e = next_events();
+                    BPT_CUDA(cudaEventRecord(e.a, st));
+                    launch_expand(a, L, tstart.as<uint32_t>(), st);
+                    BPT_CUDA(cudaEventRecord(e.b, st));
+                } else {
+                    launch_expand(a, L, tstart.as<uint32_t>(), st);
+                }
+            }
+            BPT_CUDA(cudaMemcpyAsync(&poll_host[cur], &a.lv[L - 1], sizeof(LevelRec), cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaEventRecord(poll_ev[cur], st));
+            if (have_prev) {
+                const int prev = cur ^ 1;
+                BPT_CUDA(cudaEventSynchronize(poll_ev[prev]));
+                if (poll_host[prev].overflow)
+                    fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
+                if ((poll_host[prev].packed >> kPackShift) == 0) done = true;
+            }
+            have_prev = true;
+            cur ^= 1;
+        }
+        // statistics of this batch (levels [0, L)) -> pinned ring
+        if (ring_used + L > ring.cap) {
+            BPT_CUDA(cudaStreamSynchronize(st));
+            PinnedRing bigger;
+            bigger.ensure(std::max(ring.cap * 2, ring_used + L));
+            memcpy(bigger.p, ring.p, ring_used * sizeof(LevelRec));
+            std::swap(ring.p, bigger.p);
+            std::swap(ring.cap, bigger.cap);
+        }
+        BPT_CUDA(cudaMemcpyAsync(ring.p + ring_used, a.lv, (size_t)L * sizeof(LevelRec), cudaMemcpyDeviceToHost, st));
+        batch_rows.emplace_back(ring_used, L);
+        ring_used += L;
+        launch_finalize(S, b0, bs, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>());
+        launch_count_accumulate(S, b0, bs, st);
+    }
+    unsigned long long h_elog = 0;
+    BPT_CUDA(cudaMemcpyAsync(&h_elog, elog.p, 8, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+
+    // ---- statistics
+    bpt_samples_info& I = S.info;
+    I.e_phys = I.members = I.levels_total = I.frontier_entries = I.coins = I.atomics = 0;
+    double bytes = 0;
+    S.level_rows.clear();
+    for (size_t bi = 0; bi < batch_rows.size(); ++bi) {
+        const LevelRec* R = ring.p + batch_rows[bi].first;
+        const int L = batch_rows[bi].second;
+        int last_nonempty = -1;
+        for (int l = 0; l < L; ++l) {
+            if (R[l].overflow) fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
+            const uint64_t kept = R[l].packed >> kPackShift, work = R[l].packed & kEdgeMask;
+            if (R[l].raw) last_nonempty = l;
+            I.frontier_entries += kept;
+            I.members += R[l].vc;
+            I.coins += R[l].coins;
+            I.atomics += R[l].atomics;
+            I.e_phys += S.model == BPT_IC ? work : 0;
+            const uint64_t raw_next = l + 1 < L ? R[l + 1].raw : 0;
+            bytes += S.model == BPT_IC ? 16.0 * work + 8.0 * R[l].atomics + 24.0 * kept + 8.0 * raw_next
+                                       : 24.0 * work + 8.0 * R[l].atomics + 24.0 * kept + 8.0 * raw_next;
+            if (R[l].raw) {
+                const uint64_t row[6] = {bi, (uint64_t)l, R[l].raw, kept, work, R[l].vc};
+                S.level_rows.insert(S.level_rows.end(), row, row + 6);
+            }
+        }
+        const uint64_t levels = (uint64_t)(last_nonempty + 1);
+        I.levels_total += levels;
+        levels_max = std::max(levels_max, levels);
+    }
+    if (S.model == BPT_LT) I.e_phys = I.members;
+    I.e_logical = S.model == BPT_IC ? h_elog : I.members;
+    I.levels_max = (uint32_t)levels_max;
+    I.batch_groups = (uint32_t)slots;
+    I.batches = (uint32_t)nbatches;
+    I.store_bytes = S.store.bytes;
+    I.expand_bytes = bytes;
+    I.ms_expand = 0;
+    I.expand_launches = 0;
+    if (profile) {
+        for (size_t i = 0; i < ev_used; ++i) {
+            float ms = 0;
+            BPT_CUDA(cudaEventElapsedTime(&ms, evs[i].a, evs[i].b));
+            I.ms_expand += ms;
+        }
+        I.expand_launches = ev_used;
+    }
+    I.kernel_launches = g_launches - launches0;
+    I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+}
+
+}  // namespace bpt
+
+// ==================================================================== C-ABI
+using namespace bpt;
+
+struct bpt_comm { Comm c; };
+struct bpt_graph { Graph g; };
+struct bpt_samples { Samples s; };
+
+extern "C" {
+
+const char* bpt_last_error(void) { return g_last_error.c_str(); }
+int bpt_abi_version(void) { return BPT_ABI_VERSION; }
+uint64_t bpt_kernel_launch_count(void) { return g_launches; }
+
+bpt_status bpt_comm_unique_id(void* uid_out) {
+    return guarded([&] {
+        if (!uid_out) fail(BPT_EINVAL, "uid_out is NULL");
+        comm_unique_id(uid_out);
+    });
+}
+
+bpt_status bpt_comm_init(const void* nccl_uid, int world, int rank, int cuda_device, bpt_comm** out) {
+    return guarded([&] {
+        if (!out) fail(BPT_EINVAL, "out is NULL");
+        if (world < 1 || rank < 0 || rank >= world) fail(BPT_EINVAL, "need 0 <= rank < world, world >= 1");
+        if (world > 1 && !nccl_uid) fail(BPT_EINVAL, "world > 1 needs an NCCL unique id");
+        int ndev = 0;
+        BPT_CUDA(cudaGetDeviceCount(&ndev));
+        if (cuda_device < 0 || cuda_device >= ndev) fail(BPT_EINVAL, "cuda_device out of range");
+        BPT_CUDA(cudaSetDevice(cuda_device));
+        auto c = std::make_unique<bpt_comm>();
+        c->c.world = world;
+        c->c.rank = rank;
+        c->c.device = cuda_device;
+        if (world > 1) comm_init(&c->c, nccl_uid);
+        *out = c.release();
+    });
+}
+
+void bpt_comm_free(bpt_comm* comm) {
+    if (!comm) return;
+    comm_destroy(&comm->c);
+    delete comm;
+}
+
+bpt_status bpt_graph_load(bpt_comm* comm, const uint64_t* row_ptr, const uint32_t* col, uint32_t n, uint64_t m,
+                          const float* w_f32, const uint32_t* w_q31, bpt_model model, void* stream, bpt_graph** out) {
+    return guarded([&] {
+        if (!out) fail(BPT_EINVAL, "out is NULL");
+        if (n == 0) fail(BPT_EINVAL, "n must be > 0");
+        if (m >= (1ull << 32)) fail(BPT_EINVAL, "m must be < 2^32");
+        if (!row_ptr || (m && !col)) fail(BPT_EINVAL, "row_ptr / col is NULL");
+        if ((w_f32 == nullptr) == (w_q31 == nullptr)) fail(BPT_EINVAL, "give exactly one of w_f32, w_q31");
+        if (model != BPT_IC && model != BPT_LT) fail(BPT_EINVAL, "model must be BPT_IC or BPT_LT");
+        int dev = 0;
+        if (comm) { use_device(comm->c.device); dev = comm->c.device; }
+        else BPT_CUDA(cudaGetDevice(&dev));
+        cudaStream_t st = (cudaStream_t)stream;
+        auto G = std::make_unique<bpt_graph>();
+        G->g.comm = comm ? &comm->c : nullptr;
+        G->g.device = dev;
+        G->g.n = n;
+        G->g.m = m;
+        G->g.model = model;
+        DevIn drp(row_ptr, ((size_t)n + 1) * 8, st);
+        DevIn dcol(col, m * 4, st);
+        DevIn dwf(w_f32, m * 4, st);
+        DevIn dwq(w_q31, m * 4, st);
+        build_reverse_csr(G->g, (const uint64_t*)drp.p, (const uint32_t*)dcol.p, (const float*)dwf.p,
+                          (const uint32_t*)dwq.p, st);
+        *out = G.release();
+    });
+}
+
+bpt_status bpt_graph_reverse(const bpt_graph* g, uint32_t* roff, uint32_t* src, uint32_t* val) {
+    return guarded([&] {
+        if (!g) fail(BPT_EINVAL, "graph is NULL");
+        use_device(g->g.device);
+        const Graph& G = g->g;
+        copy_out(roff, G.roff.p, ((size_t)G.n + 1) * 4, 0);
+        if (src || val) {
+            std::vector<uint2> h(G.m);
+            if (G.m) BPT_CUDA(cudaMemcpy(h.data(), G.rec.p, G.m * 8, cudaMemcpyDeviceToHost));
+            std::vector<uint32_t> a(G.m), b(G.m);
+            for (uint64_t i = 0; i < G.m; ++i) { a[i] = h[i].x; b[i] = h[i].y; }
+            if (src) BPT_CUDA(cudaMemcpy(src, a.data(), G.m * 4, cudaMemcpyDefault));
+            if (val) BPT_CUDA(cudaMemcpy(val, b.data(), G.m * 4, cudaMemcpyDefault));
+        }
+        BPT_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+bpt_status bpt_graph_dims(const bpt_graph* g, uint32_t* n, uint64_t* m, int* model) {
+    return guarded([&] {
+        if (!g) fail(BPT_EINVAL, "graph is NULL");
+        if (n) *n = g->g.n;
+        if (m) *m = g->g.m;
+        if (model) *model = g->g.model;
+    });
+}
+
+void bpt_graph_free(bpt_graph* g) {
+    if (!g) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g->g.device) cudaSetDevice(g->g.device);
+    delete g;
+}
+
+bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
+                         const bpt_sample_opts* opts, void* stream, bpt_samples** out) {
+    return guarded([&] {
+        if (!g || !out) fail(BPT_EINVAL, "graph / out is NULL");
+        if ((int)model != g->g.model) fail(BPT_EINVAL, "model does not match the loaded graph");
+        if (theta == 0 || theta >= (1ull << 32)) fail(BPT_EINVAL, "theta must be in [1, 2^32)");
+        if (colors < 1 || colors > 64 || (64 % colors) != 0) fail(BPT_EINVAL, "colors must divide 64 (1,2,4,...,64)");
+        use_device(g->g.device);
+        bpt_sample_opts o{};
+        if (opts) o = *opts;
+        auto S = std::make_unique<bpt_samples>();
+        Samples& s = S->s;
+        s.g = &g->g;
+        s.model = model;
+        s.theta = theta;
+        s.seed = seed;
+        s.colors = colors;
+        const Comm* c = g->g.comm;
+        const uint64_t W = c ? c->world : 1, r = c ? c->rank : 0;
+        const uint64_t nb = (theta + 63) / 64;
+        const uint64_t b0 = r * nb / W, b1 = (r + 1) * nb / W;  // 64-sample blocks of this rank
+        s.gb0 = b0;
+        s.blocks = b1 - b0;
+        s.s0 = umin64(64 * b0, theta);
+        s.s1 = umin64(64 * b1, theta);
+        const uint64_t pad = 64 * W;
+        s.n_pad = (uint32_t)(((uint64_t)g->g.n + pad - 1) / pad * pad);
+        bpt_samples_info& I = s.info;
+        memset(&I, 0, sizeof(I));
+        I.theta = theta; I.seed = seed; I.s0 = s.s0; I.s1 = s.s1;
+        I.colors = colors; I.model = model; I.world = (uint32_t)W; I.rank = (uint32_t)r; I.n = g->g.n;
+        run_sampling(s, o, (cudaStream_t)stream);
+        *out = S.release();
+    });
+}
+
+bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
+                      void* stream, bpt_samples** out) {
+    return bpt_sample_ex(g, model, theta, colors, seed, nullptr, stream, out);
+}
+
+bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* out) {
+    return guarded([&] {
+        if (!s || !out) fail(BPT_EINVAL, "NULL argument");
+        *out = s->s.info;
+    });
+}
+
+bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_rows, uint64_t* rows_out) {
+    return guarded([&] {
+        if (!s) fail(BPT_EINVAL, "samples is NULL");
+        const uint64_t rows = s->s.level_rows.size() / 6;
+        if (rows_out) *rows_out = rows;
+        if (out) memcpy(out, s->s.level_rows.data(), std::min(rows, cap_rows) * 6 * 8);
+    });
+}
+
+static void check_range(const Samples& S, uint64_t first, uint64_t count) {
+    if (count == 0) fail(BPT_EINVAL, "count must be > 0");
+    if (first < S.s0 || first + count > S.s1 || first + count < first)
+        fail(BPT_EINVAL, "samples [" + std::to_string(first) + ", " + std::to_string(first + count) +
+                             ") are not inside this rank's range [" + std::to_string(S.s0) + ", " +
+                             std::to_string(S.s1) + ")");
+}
+
+bpt_status bpt_rrr_sizes(const bpt_samples* s, uint64_t first, uint64_t count, uint32_t* sizes) {
+    return guarded([&] {
+        if (!s || !sizes) fail(BPT_EINVAL, "NULL argument");
+        check_range(s->s, first, count);
+        use_device(s->s.g->device);
+        copy_out(sizes, s->s.sizes.as<uint32_t>() + (first - s->s.s0), count * 4, 0);
+        BPT_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+bpt_status bpt_rrr_digests(const bpt_samples* s, uint64_t first, uint64_t count, uint64_t* digests) {
+    return guarded([&] {
+        if (!s || !digests) fail(BPT_EINVAL, "NULL argument");
+        check_range(s->s, first, count);
+        use_device(s->s.g->device);
+        copy_out(digests, s->s.digests.as<uint64_t>() + (first - s->s.s0), count * 8, 0);
+        BPT_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count, uint64_t* offsets,
+                           uint32_t* members, uint64_t capacity) {
+    return guarded([&] {
+        if (!s || !offsets) fail(BPT_EINVAL, "NULL argument");
+        const Samples& S = s->s;
+        check_range(S, first, count);
+        use_device(S.g->device);
+        std::vector<uint32_t> sz(count);
+        BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.as<uint32_t>() + (first - S.s0), count * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> off(count + 1, 0);
+        for (uint64_t i = 0; i < count; ++i) off[i + 1] = off[i] + sz[i];
+        const uint64_t total = off[count];
+        if (capacity < total)
+            fail(BPT_ENOMEM, "members capacity " + std::to_string(capacity) + " < required " + std::to_string(total));
+        if (total && !members) fail(BPT_EINVAL, "members is NULL");
+        if (total) {
+            DevBuf tmp;
+            uint32_t* dm = members;
+            if (!is_device_ptr(members)) { tmp.alloc(total * 4); dm = tmp.as<uint32_t>(); }
+            extract_range(S, first, count, off.data(), dm, 0);
+            if (dm != members) BPT_CUDA(cudaMemcpyAsync(members, dm, total * 4, cudaMemcpyDeviceToHost, 0));
+            BPT_CUDA(cudaStreamSynchronize(0));
+        }
+        BPT_CUDA(cudaMemcpy(offsets, off.data(), (count + 1) * 8, cudaMemcpyDefault));
+    });
+}
+
+bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* seeds, uint64_t* gains, double* sigma_hat) {
+    return guarded([&] {
+        if (!s) fail(BPT_EINVAL, "samples is NULL");
+        const Samples& S = s->s;
+        if (k == 0 || k > S.g->n) fail(BPT_EINVAL, "k must be in [1, n]");
+        use_device(S.g->device);
+        std::vector<uint32_t> hs(k);
+        std::vector<uint64_t> hg(k);
+        select_seeds(S, k, hs.data(), hg.data(), 0);
+        uint64_t covered = 0;
+        for (uint32_t i = 0; i < k; ++i) covered += hg[i];
+        const double sig = (double)S.g->n * (double)covered / (double)S.theta;  // reading C-12
+        if (seeds) BPT_CUDA(cudaMemcpy(seeds, hs.data(), k * 4, cudaMemcpyDefault));
+        if (gains) BPT_CUDA(cudaMemcpy(gains, hg.data(), k * 8, cudaMemcpyDefault));
+        if (sigma_hat) {
+            if (is_device_ptr(sigma_hat)) BPT_CUDA(cudaMemcpy(sigma_hat, &sig, 8, cudaMemcpyHostToDevice));
+            else *sigma_hat = sig;
+        }
+    });
+}
+
+void bpt_samples_free(bpt_samples* s) {
+    if (!s) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != s->s.g->device) cudaSetDevice(s->s.g->device);
+    delete s;
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+// internal.cuh -- shared declarations of the libbpt CUDA implementation (sm_100a).
+// Not part of the ABI; the ABI is include/bpt.h.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/bpt.h"
+
+namespace bpt {
+
+// ------------------------------------------------------------------ error plumbing
+struct Error {
+    bpt_status code;
+    std::string msg;
+};
+[[noreturn]] void fail(bpt_status code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define BPT_CUDA(x) ::bpt::check_cuda((x), #x)
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+extern uint64_t g_launches;  // kernels launched by this process (host counter)
+inline void count_launch(uint64_t k = 1) { g_launches += k; }
+
+// ------------------------------------------------------------------ Philox2x32-10
+// Reading C-1: Philox2x32-10 of Salmon et al. (SC'11) with the Random123
+// constants. Written here from the definition; the CPU oracle has its own copy.
+constexpr uint32_t kPhiloxM = 0xD256D193u;
+constexpr uint32_t kPhiloxW = 0x9E3779B9u;
+constexpr uint32_t kTagIC = 0x49430001u, kTagLT = 0x4C540001u, kTagStart = 0x53540001u;
+
+__host__ __device__ __forceinline__ uint2 philox2x32_10(uint32_t x0, uint32_t x1, uint32_t key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p = (uint64_t)kPhiloxM * (uint64_t)x0;
+        uint32_t hi = (uint32_t)(p >> 32), lo = (uint32_t)p;
+        x0 = hi ^ key ^ x1;
+        x1 = lo;
+        key += kPhiloxW;
+    }
+    return make_uint2(x0, x1);
+}
+
+// k_tag = Philox(ctr = {lo32(seed), hi32(seed)}, key = tag)[0]
+inline uint32_t stream_key(uint64_t seed, uint32_t tag) {
+    return philox2x32_10((uint32_t)seed, (uint32_t)(seed >> 32), tag).x;
+}
+
+// ------------------------------------------------------------------ handles
+struct Comm {
+    int world = 1, rank = 0, device = 0;
+    void* nccl = nullptr;  // ncclComm_t
+};
+
+struct DevBuf {  // RAII device allocation
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t b) { alloc(b); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept { reset(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; return *this; }
+    ~DevBuf() { reset(); }
+    void alloc(size_t b);
+    void reset();
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Graph {
+    Comm* comm = nullptr;
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t m = 0;
+    int model = 0;
+    DevBuf roff;   // u32[n+1]
+    DevBuf rec;    // uint2[m] {src, thr (IC) | cum (LT)}
+};
+
+// Per-level device record of one batch (zeroed at batch start).
+struct LevelRec {
+    unsigned long long packed;   // kept entries << 36 | edges (or LT tasks) -- set by compaction
+    unsigned long long vc;       // sum popc(mask) over raw entries (vertex-colour pairs)
+    unsigned long long coins;    // coin evaluations by the expansion of this level
+    unsigned long long atomics;  // atomicOr merges issued by the expansion of this level
+    unsigned int raw;            // raw (discovered) entries appended for THIS level
+    unsigned int overflow;       // set if a queue overflowed
+    unsigned long long pad;
+};
+static_assert(sizeof(LevelRec) == 48, "LevelRec layout");
+constexpr int kPackShift = 36;
+constexpr unsigned long long kEdgeMask = (1ull << kPackShift) - 1;
+
+struct Samples {
+    const Graph* g = nullptr;
+    int model = 0;
+    uint64_t theta = 0, seed = 0, s0 = 0, s1 = 0;
+    uint32_t colors = 64;
+    uint64_t blocks = 0;        // local 64-sample blocks
+    uint64_t gb0 = 0;           // first global block
+    DevBuf store;               // u64[blocks][n] visited masks (fused RRR store)
+    DevBuf sizes;               // u32[s1 - s0]
+    DevBuf digests;             // u64[s1 - s0]
+    DevBuf count0;              // u32[n_pad]  occurrences: sum_s 1[v in RR_s] (local)
+    uint32_t n_pad = 0;
+    bpt_samples_info info{};
+    std::vector<uint64_t> level_rows;  // 6 per row
+};
+
+// ------------------------------------------------------------------ launchers
+// k_build.cu
+void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_col, const float* d_wf,
+                       const uint32_t* d_wq, cudaStream_t st);
+// k_sample.cu
+struct BatchArgs {
+    const uint32_t* roff;
+    const uint2* rec;
+    uint32_t n;
+    int model;
+    uint32_t colors;
+    uint64_t* store;          // V base of the local store
+    uint64_t* N;              // next-frontier accumulators [slots][n]
+    unsigned long long* raw;  // raw queue entries
+    uint64_t raw_cap;
+    uint4* q;                 // compacted entries {v, slot, mask lo, mask hi}
+    uint64_t* qoff;           // exclusive prefix of per-entry work
+    uint64_t q_cap;
+    LevelRec* lv;             // level records
+    uint64_t blk0;            // first local block of the batch
+    uint64_t gblk0;           // first global block of the batch (sample base = 64 * (gblk0 + slot))
+    uint32_t slots;           // blocks in this batch
+    uint64_t theta;           // global sample count (bits of samples >= theta stay 0)
+    uint32_t k_ic, k_lt, k_start;
+};
+void launch_init(const BatchArgs& a, cudaStream_t st);
+// k_store.cu
+void launch_finalize(const Samples& S, uint64_t blk0, uint32_t slots, const uint32_t* roff, cudaStream_t st,
+                     unsigned long long* d_elog);
+void launch_count_accumulate(const Samples& S, uint64_t blk0, uint32_t slots, cudaStream_t st);
+// k_select.cu
+void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace bpt

@@ -1,0 +1,124 @@
+// k_select.cu -- A7 greedy max-k-cover seed selection over the fused RRR store.
+//
+// State (device): count[v] = uncovered samples of THIS rank containing v; cov[g] = covered
+// samples of local 64-sample block g; selected[v].
+// Round r:  (1) key[v] = selected ? 0 : count[v] << 32 | ~v   (max gain, smallest id,
+//               reading C-11); multi-rank: count is ReduceScatter'ed first and the
+//               per-rank maxima are AllReduce(max)'ed -- the only collectives.
+//           (2) new_g = V_g[v*] & ~cov_g ; cov_g |= new_g ; list the blocks with new_g != 0
+//           (3) count[v] -= sum over listed g of popcount(V_g[v] & new_g)
+// Each sample leaves `count` exactly once, so the decrements over all rounds cost at most one
+// pass over the store plus the few blocks touched by later rounds.
+#include "internal.cuh"
+
+namespace bpt {
+
+void comm_reduce_scatter_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint64_t recv_count, cudaStream_t st);
+void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st);
+
+namespace {
+
+constexpr int kSelThreads = 512;
+
+__global__ void __launch_bounds__(kSelThreads) k_argmax(const uint32_t* __restrict__ count, uint64_t len, uint64_t vbase,
+                                                        uint32_t n, const uint8_t* __restrict__ selected,
+                                                        unsigned long long* __restrict__ key_out,
+                                                        uint32_t* __restrict__ nlist) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nlist = 0;
+    unsigned long long best = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = vbase + i;
+        if (v >= n || selected[v]) continue;
+        const unsigned long long k = ((unsigned long long)count[i] << 32) | (unsigned long long)(~(uint32_t)v);
+        best = k > best ? k : best;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, best, d);
+        best = o > best ? o : best;
+    }
+    __shared__ unsigned long long wb[kSelThreads / 32];
+    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kSelThreads / 32; ++w) best = wb[w] > best ? wb[w] : best;
+        if (best) atomicMax(key_out, best);
+    }
+}
+
+__global__ void k_cover(const uint64_t* __restrict__ store, uint32_t n, uint64_t blocks,
+                        const unsigned long long* __restrict__ key, uint64_t* __restrict__ cov,
+                        uint8_t* __restrict__ selected, uint32_t* __restrict__ nlist, uint32_t* __restrict__ list,
+                        uint64_t* __restrict__ newm) {
+    const uint32_t vstar = ~(uint32_t)(*key);
+    if (blockIdx.x == 0 && threadIdx.x == 0) selected[vstar] = 1;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < blocks; g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t nw = store[(size_t)g * n + vstar] & ~cov[g];
+        if (nw) {
+            cov[g] |= nw;
+            const uint32_t i = atomicAdd(nlist, 1u);
+            list[i] = (uint32_t)g;
+            newm[i] = nw;
+        }
+    }
+}
+
+__global__ void k_decrement(const uint64_t* __restrict__ store, uint32_t n, const uint32_t* __restrict__ nlist,
+                            const uint32_t* __restrict__ list, const uint64_t* __restrict__ newm,
+                            uint32_t* __restrict__ count) {
+    const uint32_t L = *nlist;
+    if (L == 0) return;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t d = 0;
+        for (uint32_t i = 0; i < L; ++i) d += __popcll(store[(size_t)list[i] * n + v] & newm[i]);
+        if (d) count[v] -= d;
+    }
+}
+
+}  // namespace
+
+void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st) {
+    const uint32_t n = S.g->n;
+    Comm* comm = S.g->comm;
+    const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+    const uint64_t blocks = S.blocks;
+    DevBuf count((uint64_t)S.n_pad * 4), shard(world > 1 ? (uint64_t)S.n_pad / world * 4 : 4), sel(n),
+        cov(blocks * 8 + 8), list(blocks * 4 + 4), newm(blocks * 8 + 8), nlist(4), keys((uint64_t)k * 8);
+    BPT_CUDA(cudaMemcpyAsync(count.p, S.count0.p, (uint64_t)S.n_pad * 4, cudaMemcpyDeviceToDevice, st));
+    BPT_CUDA(cudaMemsetAsync(sel.p, 0, n, st));
+    BPT_CUDA(cudaMemsetAsync(cov.p, 0, blocks * 8 + 8, st));
+    BPT_CUDA(cudaMemsetAsync(keys.p, 0, (uint64_t)k * 8, st));
+    const unsigned vgrid = (unsigned)umin64(((uint64_t)n + kSelThreads - 1) / kSelThreads, (uint64_t)num_sms() * 4);
+    const unsigned ggrid = (unsigned)umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4);
+    const unsigned dgrid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
+    const uint64_t shard_len = (uint64_t)S.n_pad / world;
+    for (uint32_t r = 0; r < k; ++r) {
+        unsigned long long* key = keys.as<unsigned long long>() + r;
+        if (world > 1) {
+            comm_reduce_scatter_u32(comm, count.as<uint32_t>(), shard.as<uint32_t>(), shard_len, st);
+            k_argmax<<<vgrid, kSelThreads, 0, st>>>(shard.as<uint32_t>(), shard_len, (uint64_t)rank * shard_len, n,
+                                                    sel.as<uint8_t>(), key, nlist.as<uint32_t>());
+            count_launch();
+            comm_allreduce_max_u64(comm, key, 1, st);
+        } else {
+            k_argmax<<<vgrid, kSelThreads, 0, st>>>(count.as<uint32_t>(), n, 0, n, sel.as<uint8_t>(), key,
+                                                    nlist.as<uint32_t>());
+            count_launch();
+        }
+        k_cover<<<ggrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blocks, key, cov.as<uint64_t>(), sel.as<uint8_t>(),
+                                       nlist.as<uint32_t>(), list.as<uint32_t>(), newm.as<uint64_t>());
+        k_decrement<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
+                                           newm.as<uint64_t>(), count.as<uint32_t>());
+        count_launch(2);
+        BPT_CUDA(cudaGetLastError());
+    }
+    std::vector<unsigned long long> hk(k);
+    BPT_CUDA(cudaMemcpyAsync(hk.data(), keys.p, (uint64_t)k * 8, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t r = 0; r < k; ++r) {
+        h_seeds[r] = ~(uint32_t)hk[r];
+        h_gains[r] = hk[r] >> 32;
+    }
+}
+
+}  // namespace bpt

@@ -1,0 +1,206 @@
+// k_store.cu -- A5 RRR store finalisation (sizes, digests, E_logical, occurrence counts)
+// and A6 RRR extraction (Listing 1 lines 18-21: "for vertex v, for colour c,
+// if visited[v].c: RRRset(c).add(v)") as an ordered, atomic-free mask -> list transpose.
+#include "internal.cuh"
+
+namespace bpt {
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t count, void* temp, cudaStream_t st);
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp, cudaStream_t st);
+size_t scan_temp_bytes(uint64_t count);
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// SplitMix64 output function of v + gamma (digest definition)
+__device__ __forceinline__ uint64_t digest_mix(uint64_t v) {
+    uint64_t z = v + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+constexpr int kFinThreads = 256;
+
+// grid (ranges, slots). Block (r, slot) scans vertices [r*chunk, (r+1)*chunk) of block
+// blk0+slot; thread (sub, c) accumulates colour c over a quarter of the non-zero masks.
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const uint64_t* __restrict__ store, uint32_t n, uint64_t blk0,
+                                                          uint64_t chunk, const uint32_t* __restrict__ roff,
+                                                          uint64_t nlocal, uint32_t* __restrict__ sizes,
+                                                          unsigned long long* __restrict__ digests,
+                                                          unsigned long long* __restrict__ elog_total) {
+    __shared__ unsigned long long s_mask[kFinThreads];
+    __shared__ unsigned long long s_mix[kFinThreads];
+    __shared__ uint32_t s_deg[kFinThreads];
+    __shared__ uint32_t s_wcnt[kFinThreads / 32];
+    __shared__ uint32_t s_size[4][64];
+    __shared__ unsigned long long s_dig[4][64];
+    __shared__ unsigned long long s_el[4][64];
+    const uint64_t blk = blk0 + blockIdx.y;
+    const uint64_t* V = store + (size_t)blk * n;
+    const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
+    const uint64_t v_end = umin64(v_begin + chunk, n);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int sub = threadIdx.x >> 6, c = threadIdx.x & 63;
+    uint32_t size = 0;
+    unsigned long long dig = 0, el = 0;
+    for (uint64_t base = v_begin; base < v_end; base += kFinThreads) {
+        const uint64_t v = base + threadIdx.x;
+        const uint64_t m = v < v_end ? V[v] : 0ull;
+        const uint32_t bal = __ballot_sync(kFull, m != 0);
+        __syncthreads();
+        if (lane == 0) s_wcnt[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+        for (int w = 0; w < kFinThreads / 32; ++w) { if (w < wid) off += s_wcnt[w]; tot += s_wcnt[w]; }
+        if (m) {
+            const uint32_t pos = off + __popc(bal & ((1u << lane) - 1u));
+            s_mask[pos] = m;
+            s_mix[pos] = digest_mix(v);
+            s_deg[pos] = roff[v + 1] - roff[v];
+        }
+        __syncthreads();
+        for (uint32_t i = sub; i < tot; i += 4) {
+            const uint32_t b = (uint32_t)(s_mask[i] >> c) & 1u;
+            size += b;
+            dig += b ? s_mix[i] : 0ull;
+            el += b ? s_deg[i] : 0u;
+        }
+    }
+    s_size[sub][c] = size;
+    s_dig[sub][c] = dig;
+    s_el[sub][c] = el;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        uint32_t S = 0;
+        unsigned long long D = 0, E = 0;
+        for (int q = 0; q < 4; ++q) { S += s_size[q][c]; D += s_dig[q][c]; E += s_el[q][c]; }
+        const uint64_t li = 64ull * blk + c;  // local sample index
+        if (li < nlocal) {
+            if (S) atomicAdd(&sizes[li], S);
+            if (D) atomicAdd(&digests[li], D);
+        }
+        s_el[0][c] = E;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long E = 0;
+        for (int q = 0; q < 64; ++q) E += s_el[0][q];
+        if (E) atomicAdd(elog_total, E);
+    }
+}
+
+// count0[v] += sum over the batch's blocks of popcount(V_g[v])  (occurrences, A7 round 0)
+__global__ void k_count_acc(const uint64_t* __restrict__ store, uint32_t n, uint64_t blk0, uint32_t slots,
+                            uint32_t* __restrict__ count0) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = 0;
+        for (uint32_t s = 0; s < slots; ++s) c += __popcll(store[(size_t)(blk0 + s) * n + v]);
+        if (c) count0[v] += c;
+    }
+}
+
+// ---------------------------------------------------------------------------- extraction
+// One warp owns a tile of kExRounds*32 consecutive vertices of block `blk`.
+constexpr int kExRounds = 32;
+constexpr uint32_t kExTile = 32 * kExRounds;
+
+// pass 1: per-(colour, tile) member counts, colour-major; colours outside [c_lo, c_hi) = 0
+__global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint32_t c_lo, uint32_t c_hi,
+                                uint32_t ntiles, uint32_t* __restrict__ tcnt) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    if (tile >= ntiles) return;
+    uint32_t cnt_lo = 0, cnt_hi = 0;  // lane l counts colours l and l + 32
+    for (int r = 0; r < kExRounds; ++r) {
+        const uint64_t v = tile * kExTile + (uint64_t)r * 32 + lane;
+        const uint64_t m = v < n ? V[v] : 0ull;
+        if (!__any_sync(kFull, m != 0)) continue;
+        for (uint32_t c = c_lo; c < c_hi; ++c) {
+            const uint32_t b = __ballot_sync(kFull, (m >> c) & 1ull);
+            if (lane == (int)(c & 31)) { if (c < 32) cnt_lo += __popc(b); else cnt_hi += __popc(b); }
+        }
+    }
+    if (lane >= (int)c_lo && lane < (int)c_hi) tcnt[(uint64_t)lane * ntiles + tile] = cnt_lo;
+    else tcnt[(uint64_t)lane * ntiles + tile] = 0;
+    const uint32_t c2 = lane + 32;
+    tcnt[(uint64_t)c2 * ntiles + tile] = (c2 >= c_lo && c2 < c_hi) ? cnt_hi : 0;
+}
+
+// pass 2: ordered scatter; tpos = exclusive colour-major scan of tcnt (position inside the
+// group's output slab, colours in ascending order, vertices ascending within a colour)
+__global__ void k_extract_write(const uint64_t* __restrict__ V, uint32_t n, uint32_t c_lo, uint32_t c_hi,
+                                uint32_t ntiles, const uint32_t* __restrict__ tpos, uint64_t out_base,
+                                uint32_t* __restrict__ members) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    if (tile >= ntiles) return;
+    uint32_t pos_lo = tpos[(uint64_t)lane * ntiles + tile];
+    uint32_t pos_hi = tpos[(uint64_t)(lane + 32) * ntiles + tile];
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int r = 0; r < kExRounds; ++r) {
+        const uint64_t v = tile * kExTile + (uint64_t)r * 32 + lane;
+        const uint64_t m = v < n ? V[v] : 0ull;
+        if (!__any_sync(kFull, m != 0)) continue;
+        for (uint32_t c = c_lo; c < c_hi; ++c) {
+            const bool has = (m >> c) & 1ull;
+            const uint32_t b = __ballot_sync(kFull, has);
+            if (!b) continue;
+            const uint32_t src_lane = c & 31;
+            const uint32_t p = __shfl_sync(kFull, c < 32 ? pos_lo : pos_hi, src_lane);
+            if (has) members[out_base + p + __popc(b & lt)] = (uint32_t)v;
+            if (lane == (int)src_lane) { if (c < 32) pos_lo += __popc(b); else pos_hi += __popc(b); }
+        }
+    }
+}
+
+}  // namespace
+
+void launch_finalize(const Samples& S, uint64_t blk0, uint32_t slots, const uint32_t* roff, cudaStream_t st,
+                     unsigned long long* d_elog) {
+    const uint32_t n = S.g->n;
+    uint64_t ranges = (uint64_t)num_sms() * 4 / (slots ? slots : 1);
+    if (ranges < 1) ranges = 1;
+    uint64_t chunk = (n + ranges - 1) / ranges;
+    chunk = (chunk + kFinThreads - 1) / kFinThreads * kFinThreads;
+    if (chunk == 0) chunk = kFinThreads;
+    ranges = (n + chunk - 1) / chunk;
+    dim3 grid((unsigned)ranges, slots);
+    k_finalize<<<grid, kFinThreads, 0, st>>>(S.store.as<uint64_t>(), n, blk0, chunk, roff, S.s1 - S.s0,
+                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog);
+    count_launch();
+    BPT_CUDA(cudaGetLastError());
+}
+
+void launch_count_accumulate(const Samples& S, uint64_t blk0, uint32_t slots, cudaStream_t st) {
+    const uint32_t n = S.g->n;
+    unsigned grid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
+    k_count_acc<<<grid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blk0, slots, S.count0.as<uint32_t>());
+    count_launch();
+    BPT_CUDA(cudaGetLastError());
+}
+
+// d_offsets[count+1] must already hold the exclusive scan of sizes (offsets[count] = total)
+void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
+                   cudaStream_t st) {
+    const uint32_t n = S.g->n;
+    const uint32_t ntiles = (uint32_t)((n + kExTile - 1) / kExTile);
+    DevBuf tcnt((uint64_t)64 * ntiles * 4), tmp(scan_temp_bytes((uint64_t)64 * ntiles));
+    const uint64_t lfirst = first - S.s0, llast = lfirst + count;  // local sample indices
+    for (uint64_t blk = lfirst / 64; blk * 64 < llast; ++blk) {
+        const uint32_t c_lo = (uint32_t)(umax64(lfirst, blk * 64) - blk * 64);
+        const uint32_t c_hi = (uint32_t)(umin64(llast, blk * 64 + 64) - blk * 64);
+        const uint64_t out_base = h_offsets[blk * 64 + c_lo - lfirst];
+        const uint64_t* V = S.store.as<uint64_t>() + (size_t)blk * n;
+        const unsigned grid = (unsigned)(((uint64_t)ntiles * 32 + 255) / 256);
+        k_extract_count<<<grid, 256, 0, st>>>(V, n, c_lo, c_hi, ntiles, tcnt.as<uint32_t>());
+        count_launch();
+        exclusive_scan_u32(tcnt.as<uint32_t>(), tcnt.as<uint32_t>(), (uint64_t)64 * ntiles, tmp.p, st);
+        k_extract_write<<<grid, 256, 0, st>>>(V, n, c_lo, c_hi, ntiles, tcnt.as<uint32_t>(), out_base, d_members);
+        count_launch();
+        BPT_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace bpt

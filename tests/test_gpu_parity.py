@@ -1,0 +1,326 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C-ABI vs the CPU oracle on the same
+seeded inputs. Bar: bit-exact RRR sets, sizes, digests, seeds and gains; sigma_hat
+identical (integers in, same f64 formula); exact E_phys / E_logical / level structure
+(DESIGN.md §Parity)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+Q31 = 1 << 31
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def bpt(cuda_required):
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2311_10201_b200 as b
+    return b
+
+
+def oracle_all(row_ptr, col, thr, model, theta, seed, colors=64, k=None, threads=None):
+    g = oracle.Graph(row_ptr, col, w_q31=thr, model=model)
+    ids = np.arange(theta, dtype=np.uint64)
+    sizes, digests, elog, offsets, mem = g.sample_many(seed, ids, threads, members=True)
+    out = {"g": g, "sizes": sizes, "digests": digests, "elog": elog, "offsets": offsets, "members": mem}
+    if k:
+        out["seeds"], out["gains"] = oracle.greedy(g.n, offsets, mem, k)
+    return out
+
+
+def check_full(bpt, s, ref, theta):
+    assert np.array_equal(s.sizes(0, theta), ref["sizes"])
+    assert np.array_equal(s.digests(0, theta), ref["digests"])
+    off, mem = s.extract(0, theta)
+    assert np.array_equal(off, ref["offsets"])
+    assert np.array_equal(mem, ref["members"])
+
+
+# ------------------------------------------------------------------ A0/A1 builder
+
+def test_reverse_csr_equals_oracle_transpose(bpt):
+    for trial in range(3):
+        row_ptr, col = graphgen.random_graph(500 + 97 * trial, 6000, seed=trial, self_loops=True)
+        # add parallel edges: duplicate every 7th edge inside its row (stable order matters, C-4)
+        rng = np.random.default_rng(trial)
+        wf = rng.random(col.shape[0]).astype(np.float32)
+        wf[::11] = 1.0
+        wf[::13] = 0.0
+        g = bpt.Graph(row_ptr, col, w_f32=wf)
+        roff, src, thr = g.reverse_csr()
+        o_roff, o_src, o_thr = oracle.Graph(row_ptr, col, w_f32=wf).reverse_csr()
+        assert np.array_equal(roff.astype(np.uint64), o_roff)
+        assert np.array_equal(src, o_src)
+        assert np.array_equal(thr, o_thr)
+
+
+def test_reverse_csr_multigraph_and_lt_prefix(bpt):
+    n = 300
+    rng = np.random.default_rng(5)
+    u = rng.integers(0, n, 5000)
+    v = rng.integers(0, n, 5000)
+    order = np.argsort(u, kind="stable")
+    u, v = u[order], v[order]  # rows by u, destinations unsorted, duplicates kept
+    row_ptr = np.zeros(n + 1, np.uint64)
+    np.add.at(row_ptr, u + 1, 1)
+    row_ptr = np.cumsum(row_ptr).astype(np.uint64)
+    col = v.astype(np.uint32)
+    thr = graphgen.weights_lt(n, col, seed=9)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    roff, src, cum = g.reverse_csr()
+    o_roff, o_src, o_thr = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT).reverse_csr()
+    assert np.array_equal(roff.astype(np.uint64), o_roff)
+    assert np.array_equal(src, o_src)
+    want = np.zeros_like(o_thr, dtype=np.uint64)
+    for x in range(n):
+        a, b = int(o_roff[x]), int(o_roff[x + 1])
+        want[a:b] = np.cumsum(o_thr[a:b].astype(np.uint64))
+    assert np.array_equal(cum.astype(np.uint64), want)
+
+
+def test_invalid_inputs_rejected(bpt):
+    rp = np.array([0, 2, 3], np.uint64)
+    col = np.array([1, 0, 1], np.uint32)
+    ok = np.array([1, 2, 3], np.uint32)
+    cases = [
+        (np.array([0, 3, 2], np.uint64), col, dict(w_q31=ok), "decreasing"),
+        (np.array([1, 2, 3], np.uint64), col, dict(w_q31=ok), "row_ptr[0]"),
+        (rp, np.array([1, 5, 1], np.uint32), dict(w_q31=ok), "col["),
+        (rp, col, dict(w_q31=np.array([1, Q31 + 1, 0], np.uint32)), "weight[1]"),
+        (rp, col, dict(w_f32=np.array([0.5, np.nan, 0.1], np.float32)), "weight[1]"),
+        (rp, col, dict(w_f32=np.array([0.5, 1.5, 0.1], np.float32)), "weight[1]"),
+    ]
+    for r, c, w, msg in cases:
+        with pytest.raises(bpt.BptError) as ei:
+            bpt.Graph(r, c, **w)
+        assert ei.value.code == bpt.BPT_EINVAL and msg in str(ei.value)
+    with pytest.raises(bpt.BptError) as ei:  # LT row sum > 2^31 at vertex 1
+        bpt.Graph(rp, col, w_q31=np.array([Q31, 0, 1], np.uint32), model=bpt.LT)
+    assert "vertex 1" in str(ei.value)
+    g = bpt.Graph(rp, col, w_q31=ok)
+    for kw in [dict(theta=0), dict(theta=64, colors=3), dict(theta=64, colors=0), dict(theta=1 << 32)]:
+        with pytest.raises(bpt.BptError) as ei:
+            g.sample(**kw)
+        assert ei.value.code == bpt.BPT_EINVAL
+    with pytest.raises(bpt.BptError):
+        bpt.bpt_sample(g._h, bpt.LT, 64, 64, 1)  # model mismatch
+    s = g.sample(100, seed=1)
+    for k in (0, 4):
+        with pytest.raises(bpt.BptError):
+            s.select_seeds(k)
+    with pytest.raises(bpt.BptError):
+        s.sizes(90, 20)
+    with pytest.raises(bpt.BptError) as ei:
+        s.extract(0, 10, members=np.empty(1, np.uint32), capacity=1)
+    assert ei.value.code == bpt.BPT_ENOMEM
+
+
+# ------------------------------------------------------------------ worked example P:139-143
+
+def test_worked_example_on_gpu(bpt):
+    fx = json.load(open(os.path.join(GOLD, "fig_fused_example.json")))
+    n = fx["n"]
+    edges = sorted((tuple(e) for e in fx["edges"]), key=lambda t: (t[0], t[1]))
+    row_ptr = np.zeros(n + 1, np.uint64)
+    for a, _, _ in edges:
+        row_ptr[a + 1] += 1
+    row_ptr = np.cumsum(row_ptr).astype(np.uint64)
+    col = np.array([b for _, b, _ in edges], np.uint32)
+    thr = np.array([t for _, _, t in edges], np.uint32)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    roff, src, _ = g.reverse_csr()
+    assert roff.tolist() == fx["reverse_csr"]["roff"] and src.tolist() == fx["reverse_csr"]["src"]
+    s = g.sample(fx["theta"], colors=64, seed=fx["seed"], batch_groups=1)
+    off, mem = s.extract(0, 4)
+    names = {v: k for k, v in fx["colors"].items()}
+    for c in range(4):
+        assert mem[off[c]:off[c + 1]].tolist() == fx["rrr"][names[c]]
+    assert mem[off[3]:off[4]].tolist() == [4, 5, 6, 7, 8]  # yellow
+    rows = s.level_stats()
+    # raw entries per level = frontier sizes (a) {1,3,5} (b) {0,4} (c) {3,6,7,8} {4} {6,7,8}
+    assert rows[:, 2].tolist() == [len(f) for f in fx["frontiers"]]
+    assert rows[:, 5].tolist() == [sum(len(c) for c in f.values()) for f in fx["frontiers"]]
+
+
+# ------------------------------------------------------------------ degenerate probabilities
+
+def test_p0_and_p1(bpt):
+    row_ptr, col = graphgen.random_graph(2000, 16000, seed=3)
+    theta, seed = 777, 31
+    g0 = bpt.Graph(row_ptr, col, w_q31=np.zeros(col.shape[0], np.uint32))
+    s0 = g0.sample(theta, seed=seed)
+    assert np.all(s0.sizes(0, theta) == 1)
+    off, mem = s0.extract(0, theta)
+    assert mem.tolist() == [oracle.start_vertex(s, 2000, seed) for s in range(theta)]
+    thr1 = np.full(col.shape[0], Q31, np.uint32)
+    g1 = bpt.Graph(row_ptr, col, w_q31=thr1)
+    s1 = g1.sample(theta, seed=seed)
+    ref = oracle_all(row_ptr, col, thr1, oracle.IC, theta, seed)  # oracle pinned to networkx at p=1
+    check_full(bpt, s1, ref, theta)
+
+
+# ------------------------------------------------------------------ C1 full parity
+
+@pytest.mark.parametrize("colors", [64, 32, 8, 1])
+def test_c1_full_parity(bpt, colors):
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    for batch in (1, 3, 16):
+        s = g.sample(cfg.theta, colors=colors, seed=cfg.seed, batch_groups=batch)
+        check_full(bpt, s, ref, cfg.theta)
+        seeds, gains, sigma = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+        assert sigma == oracle.sigma_hat(cfg.n, int(ref["gains"].sum()), cfg.theta)
+        info = s.info
+        # exact work counters: E_phys = sum over traversal groups of the
+        # distinct (v, level) pairs weighted by in-degree; E_logical = unfused reads
+        e_phys = sum(ref["g"].group_work(cfg.seed, a, a + colors)["e_phys"] for a in range(0, cfg.theta, colors))
+        assert info["e_phys"] == e_phys
+        assert info["e_logical"] == int(ref["elog"].sum())
+        assert info["members"] == int(ref["sizes"].sum())
+        assert info["e_phys"] <= info["e_logical"]  # Theorem 1
+        if colors == 1:
+            assert info["e_phys"] == info["e_logical"]
+
+
+def test_c1_level_structure_per_group(bpt):
+    """batch_groups = 1: each batch is one 64-colour group; its per-level frontier sizes and
+    edge reads equal the oracle's level sets."""
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    og = oracle.Graph(row_ptr, col, w_q31=thr)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, batch_groups=1, poll_levels=1)
+    rows = s.level_stats()
+    for b in range(cfg.theta // 64):
+        w = og.group_work(cfg.seed, 64 * b, 64 * b + 64)
+        r = rows[rows[:, 0] == b]
+        assert r[:, 2].tolist() == w["frontier"].tolist()
+        assert int(r[:, 4].sum()) == w["e_phys"]
+        assert len(r) == w["levels"]
+
+
+# ------------------------------------------------------------------ ragged and edge cases
+
+def test_ragged_theta_and_ranges(bpt):
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    for theta in (1, 63, 65, 200):
+        ref = oracle_all(row_ptr, col, thr, oracle.IC, theta, 99)
+        s = g.sample(theta, colors=64, seed=99)
+        check_full(bpt, s, ref, theta)
+        for first, count in [(0, 1), (theta - 1, 1), (theta // 3, theta - theta // 3)]:
+            off, mem = s.extract(first, count)
+            a, b = int(ref["offsets"][first]), int(ref["offsets"][first + count])
+            assert np.array_equal(mem, ref["members"][a:b])
+            assert np.array_equal(off, ref["offsets"][first:first + count + 1] - ref["offsets"][first])
+
+
+def test_graph_without_edges(bpt):
+    n = 10
+    g = bpt.Graph(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), w_q31=np.zeros(0, np.uint32))
+    s = g.sample(100, seed=4)
+    off, mem = s.extract(0, 100)
+    assert mem.tolist() == [oracle.start_vertex(i, n, 4) for i in range(100)]
+    seeds, gains, sigma = s.select_seeds(n)
+    assert sorted(seeds.tolist()) == list(range(n)) and int(gains.sum()) == 100
+
+
+def test_device_pointers_and_determinism(bpt):
+    import torch
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    gh = bpt.Graph(row_ptr, col, w_q31=thr)
+    dev = torch.device("cuda")
+    gd = bpt.Graph(torch.from_numpy(row_ptr.astype(np.int64)).to(dev), torch.from_numpy(col.astype(np.int32)).to(dev),
+                   w_q31=torch.from_numpy(thr.astype(np.int32)).to(dev), n=cfg.n, m=cfg.m)
+    a = gh.sample(cfg.theta, seed=cfg.seed)
+    b = gd.sample(cfg.theta, seed=cfg.seed)
+    c = gh.sample(cfg.theta, seed=cfg.seed, batch_groups=5, poll_levels=7)
+    for x in (b, c):
+        assert np.array_equal(a.digests(0, cfg.theta), x.digests(0, cfg.theta))
+    out = torch.empty(cfg.theta, dtype=torch.int64, device=dev)
+    a.digests(0, cfg.theta, out=out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), a.digests(0, cfg.theta))
+
+
+# ------------------------------------------------------------------ LT (C3 shape, scaled)
+
+def test_lt_parity_scaled(bpt):
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 13, theta=4096)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    for colors, batch in ((64, 0), (64, 7), (16, 3)):
+        s = g.sample(cfg.theta, colors=colors, seed=cfg.seed, batch_groups=batch)
+        check_full(bpt, s, ref, cfg.theta)
+        seeds, gains, _ = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+        assert s.info["e_phys"] == s.info["members"] == int(ref["sizes"].sum())
+
+
+# ------------------------------------------------------------------ C2 / C5 shape, scaled
+
+@pytest.fixture(scope="module")
+def c2_small():
+    cfg = graphgen.scaled(graphgen.CONFIGS["C2"], 1 << 15, theta=2048)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
+    return cfg, row_ptr, col, thr, ref
+
+
+def test_c2_shape_parity_and_colour_sweep(bpt, c2_small):
+    cfg, row_ptr, col, thr, ref = c2_small
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    prev = None
+    for colors in (1, 8, 32, 64):  # C5: fused vs unfused ablation, identical RRR sets
+        s = g.sample(cfg.theta, colors=colors, seed=cfg.seed)
+        check_full(bpt, s, ref, cfg.theta)
+        seeds, gains, sigma = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+        info = s.info
+        assert info["e_logical"] == int(ref["elog"].sum())
+        if colors == 1:
+            assert info["e_phys"] == info["e_logical"]
+        if prev is not None:
+            assert info["e_phys"] <= prev  # larger groups fuse more (Theorem 1 per group)
+        prev = info["e_phys"]
+
+
+# ------------------------------------------------------------------ full-size configs (bench launch config)
+
+@pytest.mark.slow
+def test_c2_full_size_sampled_parity(bpt):
+    """BASELINE configs[1] at full size in bench.py's launch configuration: exact per-sample
+    sizes/digests/lists on a strided subset (all of blocks 0 and G-1), plus invariants."""
+    cfg = graphgen.CONFIGS["C2"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed)
+    ids = np.unique(np.concatenate([np.arange(0, cfg.theta, 257), np.arange(64), np.arange(cfg.theta - 64, cfg.theta)]))
+    og = oracle.Graph(row_ptr, col, w_q31=thr)
+    o_sizes, o_dig, o_elog, o_off, o_mem = og.sample_many(cfg.seed, ids, members=True)
+    sizes = s.sizes(0, cfg.theta)
+    dig = s.digests(0, cfg.theta)
+    assert np.array_equal(sizes[ids], o_sizes)
+    assert np.array_equal(dig[ids], o_dig)
+    for j in (0, 1, len(ids) // 2, len(ids) - 1):
+        off, mem = s.extract(int(ids[j]), 1)
+        assert np.array_equal(mem, o_mem[o_off[j]:o_off[j + 1]])
+    info = s.info
+    assert info["members"] == int(sizes.astype(np.uint64).sum())
+    assert info["e_phys"] <= info["e_logical"]
+    seeds, gains, sigma = s.select_seeds(cfg.k)
+    assert len(set(seeds.tolist())) == cfg.k
+    assert list(gains) == sorted(gains, reverse=True)
+    assert int(gains.sum()) <= cfg.theta
+    assert sigma == cfg.n * int(gains.sum()) / cfg.theta
