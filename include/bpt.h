@@ -121,6 +121,8 @@ typedef struct {
     uint32_t batch_groups;   /* 64-sample blocks traversed concurrently; 0 = automatic */
     uint32_t poll_levels;    /* levels launched between host polls; 0 = automatic */
     uint32_t flags;          /* BPT_FLAG_* */
+    uint32_t shard_world;    /* test hook: sample only shard shard_rank of shard_world (0 = use the comm) */
+    uint32_t shard_rank;
     uint32_t reserved;
 } bpt_sample_opts;
 #define BPT_FLAG_PROFILE 1u  /* time every expansion launch with CUDA events */
@@ -151,6 +153,10 @@ typedef struct {
 } bpt_samples_info;
 
 BPT_API bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* out);
+
+/* A7 round 0: occurrences count[v] = number of this rank's samples whose RRR set contains v,
+ * for v in [0, n). counts[n] u32, host or device. */
+BPT_API bpt_status bpt_occurrences(const bpt_samples* s, uint32_t* counts);
 
 /* Per level of every batch: {batch, level, raw_entries, kept_entries, edges_or_tasks, vc_pairs}
  * as 6 u64 per row, host buffer. *rows = number of rows available (written if rows_out != NULL). */
@@ -185,6 +191,9 @@ BPT_API bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* 
                             double* sigma_hat);
 
 BPT_API void bpt_samples_free(bpt_samples* s);
+
+/* Release the device blocks the library caches between calls (its memory pool). */
+BPT_API bpt_status bpt_release_cache(void);
 
 /* Library-wide count of kernels launched by this process (evidence for gpu_launches). */
 BPT_API uint64_t bpt_kernel_launch_count(void);

@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbpt.so")
+LIB_PATH = os.environ.get("BPT_LIB") or os.path.join(_HERE, "libbpt.so")  # BPT_LIB: tuning variants only
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "bpt.h")
 
 if not os.path.exists(LIB_PATH):
@@ -32,7 +32,8 @@ _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c
 
 
 class bpt_sample_opts(ctypes.Structure):
-    _fields_ = [("batch_groups", _u32), ("poll_levels", _u32), ("flags", _u32), ("reserved", _u32)]
+    _fields_ = [("batch_groups", _u32), ("poll_levels", _u32), ("flags", _u32), ("shard_world", _u32),
+                ("shard_rank", _u32), ("reserved", _u32)]
 
 
 class bpt_samples_info(ctypes.Structure):
@@ -63,11 +64,13 @@ _SIGS = {
     "bpt_sample_ex": ([_p, _i, _u64, _u32, _u64, ctypes.POINTER(bpt_sample_opts), _p, ctypes.POINTER(_p)], _i),
     "bpt_samples_get_info": ([_p, ctypes.POINTER(bpt_samples_info)], _i),
     "bpt_level_stats": ([_p, _p, _u64, _p], _i),
+    "bpt_occurrences": ([_p, _p], _i),
     "bpt_rrr_sizes": ([_p, _u64, _u64, _p], _i),
     "bpt_rrr_digests": ([_p, _u64, _u64, _p], _i),
     "bpt_rrr_extract": ([_p, _u64, _u64, _p, _p, _u64], _i),
     "bpt_select_seeds": ([_p, _u32, _p, _p, _p], _i),
     "bpt_samples_free": ([_p], None),
+    "bpt_release_cache": ([], _i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -164,9 +167,10 @@ def bpt_graph_free(h) -> None:
 
 
 def bpt_sample(graph, model: int, theta: int, colors: int, seed: int, stream=None, batch_groups: int = 0,
-               poll_levels: int = 0, flags: int = 0):
+               poll_levels: int = 0, flags: int = 0, shard: tuple[int, int] | None = None):
     h = _p()
-    opts = bpt_sample_opts(batch_groups, poll_levels, flags, 0)
+    sw, sr = shard if shard else (0, 0)
+    opts = bpt_sample_opts(batch_groups, poll_levels, flags, sw, sr, 0)
     _check(_lib.bpt_sample_ex(graph, model, theta, colors, seed, ctypes.byref(opts), _stream(stream),
                               ctypes.byref(h)))
     return h
@@ -184,6 +188,12 @@ def bpt_level_stats(h) -> np.ndarray:
     out = np.zeros((rows.value, 6), dtype=np.uint64)
     if rows.value:
         _check(_lib.bpt_level_stats(h, _ptr(out), rows.value, None))
+    return out
+
+
+def bpt_occurrences(h, n: int, out=None):
+    out = np.empty(n, dtype=np.uint32) if out is None else out
+    _check(_lib.bpt_occurrences(h, _ptr(out)))
     return out
 
 
@@ -223,6 +233,10 @@ def bpt_select_seeds(h, k: int, seeds=None, gains=None):
 
 def bpt_samples_free(h) -> None:
     _lib.bpt_samples_free(h)
+
+
+def bpt_release_cache() -> None:
+    _check(_lib.bpt_release_cache())
 
 
 # ------------------------------------------------------------------ object wrappers
@@ -273,9 +287,9 @@ class Graph:
         return roff, src[: self.m], val[: self.m]
 
     def sample(self, theta: int, colors: int = 64, seed: int = 0, stream=None, batch_groups: int = 0,
-               poll_levels: int = 0, profile: bool = False) -> "Samples":
+               poll_levels: int = 0, profile: bool = False, shard: tuple[int, int] | None = None) -> "Samples":
         h = bpt_sample(self._h, self.model, theta, colors, seed, stream, batch_groups, poll_levels,
-                       FLAG_PROFILE if profile else 0)
+                       FLAG_PROFILE if profile else 0, shard)
         return Samples(self, h)
 
     def close(self):
@@ -304,6 +318,9 @@ class Samples:
 
     def extract(self, first: int, count: int, offsets=None, members=None, capacity=None):
         return bpt_rrr_extract(self._h, first, count, offsets, members, capacity)
+
+    def occurrences(self, out=None):
+        return bpt_occurrences(self._h, self.graph.n, out)
 
     def level_stats(self) -> np.ndarray:
         return bpt_level_stats(self._h)

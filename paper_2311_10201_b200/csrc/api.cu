@@ -3,8 +3,12 @@
 // the device-resident level loop with pipelined polling, and statistics.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 
 #include "internal.cuh"
@@ -24,10 +28,71 @@ void check_cuda(cudaError_t e, const char* what) {
     fail(BPT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------------------ device memory pool
+// Freed device blocks are cached per device and reused for later requests of a similar size
+// (best fit within +25%), so repeated bpt_graph_load / bpt_sample calls do not pay
+// cudaMalloc/cudaFree of multi-GB stores each time. Every API call synchronises its stream
+// before returning, so a block is never recycled while a kernel may still use it.
+// On allocation failure the cache is released and the allocation retried.
+namespace {
+struct Pool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks[64];  // per device: size -> block
+    size_t cached[64] = {};
+};
+Pool& pool() {
+    static Pool* p = new Pool();  // never destroyed: the CUDA context may be gone at exit
+    return *p;
+}
+size_t round_size(size_t b) {
+    if (b < 8) b = 8;
+    const size_t g = b >= (64u << 20) ? (2u << 20) : 512;
+    return (b + g - 1) / g * g;
+}
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 || d >= 64 ? 0 : d;
+}
+}  // namespace
+
+void release_cached_blocks() {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    int cur = current_device();
+    for (int d = 0; d < 64; ++d) {
+        if (P.free_blocks[d].empty()) continue;
+        cudaSetDevice(d);
+        for (auto& kv : P.free_blocks[d]) cudaFree(kv.second);
+        P.free_blocks[d].clear();
+        P.cached[d] = 0;
+    }
+    cudaSetDevice(cur);
+}
+
 void DevBuf::alloc(size_t b) {
     reset();
-    if (b == 0) b = 8;
+    b = round_size(b);
+    const int dev = current_device();
+    {
+        Pool& P = pool();
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto it = P.free_blocks[dev].lower_bound(b);
+        if (it != P.free_blocks[dev].end() && it->first <= b + b / 4) {
+            p = it->second;
+            bytes = it->first;
+            P.cached[dev] -= bytes;
+            P.free_blocks[dev].erase(it);
+            device = dev;
+            return;
+        }
+    }
     cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        release_cached_blocks();
+        e = cudaMalloc(&p, b);
+    }
     if (e != cudaSuccess) {
         p = nullptr;
         cudaGetLastError();
@@ -36,9 +101,15 @@ void DevBuf::alloc(size_t b) {
         fail(BPT_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
     bytes = b;
+    device = dev;
 }
 void DevBuf::reset() {
-    if (p) cudaFree(p);
+    if (p) {
+        Pool& P = pool();
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.free_blocks[device].emplace(bytes, p);
+        P.cached[device] += bytes;
+    }
     p = nullptr;
     bytes = 0;
 }
@@ -51,7 +122,7 @@ int num_sms() {
 }
 
 // launchers defined in other translation units
-uint32_t expand_tile();
+uint32_t expand_unit(int model);
 void launch_compact(const BatchArgs& a, int level, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st);
 void launch_expand(const BatchArgs& a, int level, const uint32_t* tstart, cudaStream_t st);
 void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
@@ -96,11 +167,15 @@ void use_device(int dev) {
 
 template <class F>
 bpt_status guarded(F&& f) {
+    // a pending error recorded by an earlier (unchecked) runtime call must not be
+    // attributed to this call's first launch check; keep it for the message
+    const cudaError_t stale = cudaGetLastError();
     try {
         f();
         return BPT_OK;
     } catch (const Error& e) {
         g_last_error = e.msg;
+        if (stale != cudaSuccess) g_last_error += std::string(" [pending before this call: ") + cudaGetErrorString(stale) + "]";
         return e.code;
     } catch (const std::bad_alloc&) {
         g_last_error = "host allocation failed";
@@ -111,23 +186,7 @@ bpt_status guarded(F&& f) {
     }
 }
 
-constexpr int kMaxLevels = 8192;
 
-struct PinnedRing {  // pinned host staging for level records
-    LevelRec* p = nullptr;
-    size_t cap = 0;
-    ~PinnedRing() { if (p) cudaFreeHost(p); }
-    void ensure(size_t n) {
-        if (n <= cap) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        size_t c = std::max(n, cap * 2);
-        BPT_CUDA(cudaMallocHost(&p, c * sizeof(LevelRec)));
-        cap = c;
-    }
-};
-
-struct EventPair { cudaEvent_t a, b; };
 
 }  // namespace
 
@@ -147,8 +206,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         BPT_CUDA(cudaStreamSynchronize(st));
         return;
     }
-    S.store.alloc((size_t)S.blocks * n * 8);
-    BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
+    S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
     const uint64_t nlocal = S.s1 - S.s0;
     S.sizes.alloc(nlocal * 4);
     S.digests.alloc(nlocal * 8);
@@ -156,27 +214,44 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     BPT_CUDA(cudaMemsetAsync(S.digests.p, 0, nlocal * 8, st));
 
     // ---- batch plan
-    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 8 : 512);
+    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 512);
     uint64_t slots = umin64(umax64(want, 1), S.blocks);
-    const uint32_t tile = expand_tile();
+    const uint32_t tile = expand_unit(S.model);
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
         raw_cap = umin64(sl * slices * n, (1ull << 28) - 1);
         q_cap = raw_cap;
         const uint64_t work = S.model == BPT_IC ? umin64(sl * slices * g.m, kEdgeMask)
                                                 : umin64(sl * 64 * n, kEdgeMask);
         ts_cap = work / tile + 2;
-        return sl * (uint64_t)n * 8 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 4;
+        return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 20;
     };
     size_t free_b = 0, total_b = 0;
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
     uint64_t raw_cap = 0, q_cap = 0, ts_cap = 0;
     while (slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
+    while (slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
     plan_bytes(slots, raw_cap, q_cap, ts_cap);
 
-    DevBuf N((size_t)slots * n * 8), raw(raw_cap * 8), q(q_cap * 16), qoff(q_cap * 8), tstart(ts_cap * 4),
-        lv((size_t)kMaxLevels * sizeof(LevelRec)), elog(8);
-    BPT_CUDA(cudaMemsetAsync(N.p, 0, N.bytes, st));
+    const uint64_t nbatches = (S.blocks + slots - 1) / slots;
+    const uint32_t stats_cap = (uint32_t)umin64(nbatches * 64 + 8192, 1ull << 22);
+    DevBuf VN((size_t)slots * n * 16), raw(raw_cap * 8), q(q_cap * 16), qoff(q_cap * 8), tstart(ts_cap * 4),
+        umask(S.model == BPT_IC ? ts_cap * 16 : 16),
+        lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
+        elog(8);
+    BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
+    BPT_CUDA(cudaMemsetAsync(lv.p, 0, lv.bytes, st));  // k_next_batch re-zeroes the levels it used
+    BPT_CUDA(cudaMemsetAsync(umask.p, 0, umask.bytes, st));  // the expansion re-zeroes every unit it reads
     BPT_CUDA(cudaMemsetAsync(elog.p, 0, 8, st));
+    Ctl c0{};
+    c0.slots = (uint32_t)umin64(slots, S.blocks);
+    c0.gblk0 = S.gb0;
+    c0.t_start = ~0ull;
+    static thread_local Ctl* c_host = nullptr;
+    if (!c_host) BPT_CUDA(cudaMallocHost(&c_host, sizeof(Ctl)));
+    *c_host = c0;
+    BPT_CUDA(cudaMemcpyAsync(ctl.p, c_host, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    using clk = std::chrono::steady_clock;
+    const auto t_alloc = clk::now();
 
     BatchArgs a{};
     a.roff = g.roff.as<uint32_t>();
@@ -185,154 +260,141 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.model = S.model;
     a.colors = C;
     a.store = S.store.as<uint64_t>();
-    a.N = N.as<uint64_t>();
+    a.VN = VN.as<ulonglong2>();
     a.raw = raw.as<unsigned long long>();
     a.raw_cap = raw_cap;
     a.q = q.as<uint4>();
+    a.umask = S.model == BPT_IC ? umask.as<uint4>() : nullptr;
     a.qoff = qoff.as<uint64_t>();
     a.q_cap = q_cap;
     a.lv = lv.as<LevelRec>();
+    a.stats = stats.as<LevelRec>();
+    a.stats_cap = stats_cap;
+    a.slots_max = (uint32_t)slots;
+    a.blocks = S.blocks;
+    a.ctl = ctl.as<Ctl>();
     a.theta = S.theta;
     a.k_ic = stream_key(S.seed, kTagIC);
     a.k_lt = stream_key(S.seed, kTagLT);
     a.k_start = stream_key(S.seed, kTagStart);
 
-    const uint32_t K = opt.poll_levels ? opt.poll_levels : (S.model == BPT_IC ? 3 : 16);
     const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
-    std::vector<EventPair> evs;
-    size_t ev_used = 0;
-    auto next_events = [&]() -> EventPair& {
-        if (ev_used == evs.size()) {
-            EventPair e{};
-            BPT_CUDA(cudaEventCreate(&e.a));
-            BPT_CUDA(cudaEventCreate(&e.b));
-            evs.push_back(e);
-        }
-        return evs[ev_used++];
-    };
-    cudaEvent_t poll_ev[2];
-    BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
-    BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
-    LevelRec* poll_host = nullptr;
-    BPT_CUDA(cudaMallocHost(&poll_host, 2 * sizeof(LevelRec)));
-    PinnedRing ring;
-    const uint64_t nbatches = (S.blocks + slots - 1) / slots;
-    ring.ensure(nbatches * 48);
-    std::vector<std::pair<size_t, int>> batch_rows;  // (ring offset, levels launched)
-    size_t ring_used = 0;
-
-    struct Cleanup {
-        std::vector<EventPair>* evs; cudaEvent_t* pe; LevelRec* ph;
-        ~Cleanup() {
-            for (auto& e : *evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-            cudaEventDestroy(pe[0]); cudaEventDestroy(pe[1]);
-            cudaFreeHost(ph);
-        }
-    } cleanup{&evs, poll_ev, poll_host};
-
-    uint64_t levels_max = 0;
-    for (uint64_t b0 = 0; b0 < S.blocks; b0 += slots) {
-        const uint32_t bs = (uint32_t)umin64(slots, S.blocks - b0);
-        a.blk0 = b0;
-        a.gblk0 = S.gb0 + b0;
-        a.slots = bs;
-        BPT_CUDA(cudaMemsetAsync(lv.p, 0, lv.bytes, st));
-        launch_init(a, st);
-        int L = 0, cur = 0;
-        bool have_prev = false, done = false;
-        while (!done) {
-            if (L + (int)K + 1 >= kMaxLevels) fail(BPT_ENOMEM, "level loop exceeded " + std::to_string(kMaxLevels) + " levels");
-            for (uint32_t i = 0; i < K; ++i, ++L) {
-                launch_compact(a, L, tstart.as<uint32_t>(), ts_cap, st);
-                if (profile) {
-                    EventPair& e = next_events();
-                    BPT_CUDA(cudaEventRecord(e.a, st));
-                    launch_expand(a, L, tstart.as<uint32_t>(), st);
-                    BPT_CUDA(cudaEventRecord(e.b, st));
-                } else {
-                    launch_expand(a, L, tstart.as<uint32_t>(), st);
+    double ev_ms = 0;
+    uint64_t ev_launches = 0, polls = 0;
+    double wait_ms = 0;
+    if (!profile) {
+        // ---- device-resident loops: one graph launch for the whole sample range
+        StoreHook hook{&S, a.VN, g.roff.as<uint32_t>(), elog.as<unsigned long long>()};
+        cudaGraphExec_t exec = build_sampling_graph(a, tstart.as<uint32_t>(), ts_cap, hook);
+        cudaError_t e = cudaGraphLaunch(exec, st);
+        cudaGraphExecDestroy(exec);  // deferred by the driver until the launch completes
+        BPT_CUDA(e);
+    } else {
+        // ---- host-driven loop with a CUDA event pair around every expansion launch (roofline
+        //      measurement). Same kernels; the host polls the control block every K levels,
+        //      pipelined one chunk behind; extra levels launched after the end are no-ops.
+        const uint32_t K = opt.poll_levels ? opt.poll_levels : (S.model == BPT_IC ? 3 : 16);
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+        struct EvCleanup {
+            std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* v;
+            ~EvCleanup() { for (auto& e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); } }
+        } evc{&evs};
+        cudaEvent_t poll_ev[2];
+        BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
+        BPT_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
+        struct PollCleanup { cudaEvent_t* e; ~PollCleanup() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); } } pc{poll_ev};
+        static thread_local Ctl* poll_host = nullptr;
+        if (!poll_host) BPT_CUDA(cudaMallocHost(&poll_host, 2 * sizeof(Ctl)));
+        for (uint64_t b = 0; b < nbatches; ++b) {
+            launch_init(a, st);
+            int cur = 0;
+            bool have_prev = false, done = false;
+            while (!done) {
+                for (uint32_t i = 0; i < K; ++i) {
+                    std::pair<cudaEvent_t, cudaEvent_t> e{};
+                    BPT_CUDA(cudaEventCreate(&e.first));
+                    BPT_CUDA(cudaEventCreate(&e.second));
+                    evs.push_back(e);
+                    launch_level(a, tstart.as<uint32_t>(), ts_cap, st, e.first, e.second);
                 }
+                BPT_CUDA(cudaMemcpyAsync(&poll_host[cur], a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+                BPT_CUDA(cudaEventRecord(poll_ev[cur], st));
+                if (have_prev) {
+                    const int prev = cur ^ 1;
+                    const auto tw = clk::now();
+                    BPT_CUDA(cudaEventSynchronize(poll_ev[prev]));
+                    wait_ms += std::chrono::duration<double, std::milli>(clk::now() - tw).count();
+                    ++polls;
+                    if (poll_host[prev].error || !poll_host[prev].cont) done = true;
+                    if (poll_host[prev].level + 2 * K + 2 >= (uint32_t)kMaxLevels) done = true;
+                }
+                have_prev = true;
+                cur ^= 1;
             }
-            BPT_CUDA(cudaMemcpyAsync(&poll_host[cur], &a.lv[L - 1], sizeof(LevelRec), cudaMemcpyDeviceToHost, st));
-            BPT_CUDA(cudaEventRecord(poll_ev[cur], st));
-            if (have_prev) {
-                const int prev = cur ^ 1;
-                BPT_CUDA(cudaEventSynchronize(poll_ev[prev]));
-                if (poll_host[prev].overflow)
-                    fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
-                if ((poll_host[prev].packed >> kPackShift) == 0) done = true;
-            }
-            have_prev = true;
-            cur ^= 1;
+            launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>());
+            launch_count_accumulate(S, a.ctl, st);
+            launch_next_batch(a, st);
         }
-        // statistics of this batch (levels [0, L)) -> pinned ring
-        if (ring_used + L > ring.cap) {
-            BPT_CUDA(cudaStreamSynchronize(st));
-            PinnedRing bigger;
-            bigger.ensure(std::max(ring.cap * 2, ring_used + L));
-            memcpy(bigger.p, ring.p, ring_used * sizeof(LevelRec));
-            std::swap(ring.p, bigger.p);
-            std::swap(ring.cap, bigger.cap);
+        BPT_CUDA(cudaStreamSynchronize(st));
+        for (auto& e : evs) {
+            float ms = 0;
+            BPT_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+            ev_ms += ms;
         }
-        BPT_CUDA(cudaMemcpyAsync(ring.p + ring_used, a.lv, (size_t)L * sizeof(LevelRec), cudaMemcpyDeviceToHost, st));
-        batch_rows.emplace_back(ring_used, L);
-        ring_used += L;
-        launch_finalize(S, b0, bs, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>());
-        launch_count_accumulate(S, b0, bs, st);
+        ev_launches = evs.size();
     }
+    const auto t_loop = clk::now();
     unsigned long long h_elog = 0;
     BPT_CUDA(cudaMemcpyAsync(&h_elog, elog.p, 8, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaMemcpyAsync(c_host, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
+    const Ctl cf = *c_host;
+    if (cf.error == 1) fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
+    if (cf.error == 2) fail(BPT_ENOMEM, "level loop exceeded " + std::to_string(kMaxLevels) + " levels");
+    const uint32_t rows = (uint32_t)umin64(cf.stats_used, stats_cap);
+    std::vector<LevelRec> R(rows);
+    if (rows) BPT_CUDA(cudaMemcpy(R.data(), stats.p, (size_t)rows * sizeof(LevelRec), cudaMemcpyDeviceToHost));
 
-    // ---- statistics
+    // ---- statistics (exact integers from the device counters)
     bpt_samples_info& I = S.info;
-    I.e_phys = I.members = I.levels_total = I.frontier_entries = I.coins = I.atomics = 0;
-    double bytes = 0;
-    S.level_rows.clear();
-    for (size_t bi = 0; bi < batch_rows.size(); ++bi) {
-        const LevelRec* R = ring.p + batch_rows[bi].first;
-        const int L = batch_rows[bi].second;
-        int last_nonempty = -1;
-        for (int l = 0; l < L; ++l) {
-            if (R[l].overflow) fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
-            const uint64_t kept = R[l].packed >> kPackShift, work = R[l].packed & kEdgeMask;
-            if (R[l].raw) last_nonempty = l;
-            I.frontier_entries += kept;
-            I.members += R[l].vc;
-            I.coins += R[l].coins;
-            I.atomics += R[l].atomics;
-            I.e_phys += S.model == BPT_IC ? work : 0;
-            const uint64_t raw_next = l + 1 < L ? R[l + 1].raw : 0;
-            bytes += S.model == BPT_IC ? 16.0 * work + 8.0 * R[l].atomics + 24.0 * kept + 8.0 * raw_next
-                                       : 24.0 * work + 8.0 * R[l].atomics + 24.0 * kept + 8.0 * raw_next;
-            if (R[l].raw) {
-                const uint64_t row[6] = {bi, (uint64_t)l, R[l].raw, kept, work, R[l].vc};
-                S.level_rows.insert(S.level_rows.end(), row, row + 6);
-            }
-        }
-        const uint64_t levels = (uint64_t)(last_nonempty + 1);
-        I.levels_total += levels;
-        levels_max = std::max(levels_max, levels);
-    }
-    if (S.model == BPT_LT) I.e_phys = I.members;
-    I.e_logical = S.model == BPT_IC ? h_elog : I.members;
-    I.levels_max = (uint32_t)levels_max;
+    I.frontier_entries = cf.entries;
+    I.members = cf.vc;
+    I.coins = cf.coins;
+    I.atomics = cf.atomics;
+    I.e_phys = S.model == BPT_IC ? cf.work : cf.vc;
+    I.e_logical = S.model == BPT_IC ? h_elog : cf.vc;
+    I.levels_total = cf.levels_total;
+    I.levels_max = cf.levels_max;
     I.batch_groups = (uint32_t)slots;
     I.batches = (uint32_t)nbatches;
     I.store_bytes = S.store.bytes;
-    I.expand_bytes = bytes;
-    I.ms_expand = 0;
-    I.expand_launches = 0;
-    if (profile) {
-        for (size_t i = 0; i < ev_used; ++i) {
-            float ms = 0;
-            BPT_CUDA(cudaEventElapsedTime(&ms, evs[i].a, evs[i].b));
-            I.ms_expand += ms;
-        }
-        I.expand_launches = ev_used;
+    S.level_rows.clear();
+    double bytes = 0;
+    for (uint32_t i = 0; i < rows; ++i) {
+        const LevelRec& r = R[i];
+        const uint64_t kept = r.packed >> kPackShift, work = r.packed & kEdgeMask;
+        const uint64_t raw_next = (i + 1 < rows && (R[i + 1].pad >> 32) == (r.pad >> 32)) ? R[i + 1].raw : 0;
+        bytes += (S.model == BPT_IC ? 16.0 : 24.0) * work + 8.0 * r.atomics + 24.0 * kept + 8.0 * raw_next;
+        const uint64_t row[6] = {r.pad >> 32, r.pad & 0xffffffffull, r.raw, kept, work, r.vc};
+        S.level_rows.insert(S.level_rows.end(), row, row + 6);
     }
+    I.expand_bytes = bytes;
+    // expansion time: CUDA events around every launch (profile mode) or the device-side
+    // %globaltimer span of every launch (graph mode)
+    I.ms_expand = profile ? ev_ms : cf.expand_ns * 1e-6;
+    I.expand_launches = profile ? ev_launches : cf.levels_total;
+    // kernels executed: per batch init + finalize + count + next_batch, per level compact + expand + advance
+    if (!profile) g_launches += 4 * nbatches + 3 * cf.levels_total;
     I.kernel_launches = g_launches - launches0;
     I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+    if (getenv("BPT_TRACE")) {
+        auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+        fprintf(stderr, "[bpt] sample (%s): alloc %.2f ms, loop %.2f ms (polls %llu, wait %.2f ms), drain+stats %.2f ms, "
+                        "total %.2f ms, batches %llu, slots %llu, levels %llu, expand %.2f ms\n",
+                profile ? "events" : "graph", ms(t_begin, t_alloc), ms(t_alloc, t_loop), (unsigned long long)polls,
+                wait_ms, ms(t_loop, clk::now()), I.ms_total, (unsigned long long)nbatches, (unsigned long long)slots,
+                (unsigned long long)cf.levels_total, I.ms_expand);
+    }
 }
 
 }  // namespace bpt
@@ -349,6 +411,10 @@ extern "C" {
 const char* bpt_last_error(void) { return g_last_error.c_str(); }
 int bpt_abi_version(void) { return BPT_ABI_VERSION; }
 uint64_t bpt_kernel_launch_count(void) { return g_launches; }
+
+bpt_status bpt_release_cache(void) {
+    return guarded([&] { release_cached_blocks(); });
+}
 
 bpt_status bpt_comm_unique_id(void* uid_out) {
     return guarded([&] {
@@ -458,12 +524,20 @@ bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, ui
         auto S = std::make_unique<bpt_samples>();
         Samples& s = S->s;
         s.g = &g->g;
+        s.n = g->g.n;
+        s.device = g->g.device;
+        s.comm = g->g.comm;
         s.model = model;
         s.theta = theta;
         s.seed = seed;
         s.colors = colors;
         const Comm* c = g->g.comm;
-        const uint64_t W = c ? c->world : 1, r = c ? c->rank : 0;
+        uint64_t W = c ? c->world : 1, r = c ? c->rank : 0;
+        if (o.shard_world) {  // test hook: one shard of a W-way split, without communication
+            if (o.shard_rank >= o.shard_world) fail(BPT_EINVAL, "shard_rank must be < shard_world");
+            W = o.shard_world;
+            r = o.shard_rank;
+        }
         const uint64_t nb = (theta + 63) / 64;
         const uint64_t b0 = r * nb / W, b1 = (r + 1) * nb / W;  // 64-sample blocks of this rank
         s.gb0 = b0;
@@ -477,6 +551,7 @@ bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, ui
         I.theta = theta; I.seed = seed; I.s0 = s.s0; I.s1 = s.s1;
         I.colors = colors; I.model = model; I.world = (uint32_t)W; I.rank = (uint32_t)r; I.n = g->g.n;
         run_sampling(s, o, (cudaStream_t)stream);
+        s.g = nullptr;  // the samples do not depend on the graph after this point
         *out = S.release();
     });
 }
@@ -490,6 +565,15 @@ bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* out) {
     return guarded([&] {
         if (!s || !out) fail(BPT_EINVAL, "NULL argument");
         *out = s->s.info;
+    });
+}
+
+bpt_status bpt_occurrences(const bpt_samples* s, uint32_t* counts) {
+    return guarded([&] {
+        if (!s || !counts) fail(BPT_EINVAL, "NULL argument");
+        use_device(s->s.device);
+        copy_out(counts, s->s.count0.p, (size_t)s->s.n * 4, 0);
+        BPT_CUDA(cudaStreamSynchronize(0));
     });
 }
 
@@ -514,7 +598,7 @@ bpt_status bpt_rrr_sizes(const bpt_samples* s, uint64_t first, uint64_t count, u
     return guarded([&] {
         if (!s || !sizes) fail(BPT_EINVAL, "NULL argument");
         check_range(s->s, first, count);
-        use_device(s->s.g->device);
+        use_device(s->s.device);
         copy_out(sizes, s->s.sizes.as<uint32_t>() + (first - s->s.s0), count * 4, 0);
         BPT_CUDA(cudaStreamSynchronize(0));
     });
@@ -524,7 +608,7 @@ bpt_status bpt_rrr_digests(const bpt_samples* s, uint64_t first, uint64_t count,
     return guarded([&] {
         if (!s || !digests) fail(BPT_EINVAL, "NULL argument");
         check_range(s->s, first, count);
-        use_device(s->s.g->device);
+        use_device(s->s.device);
         copy_out(digests, s->s.digests.as<uint64_t>() + (first - s->s.s0), count * 8, 0);
         BPT_CUDA(cudaStreamSynchronize(0));
     });
@@ -536,7 +620,7 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         if (!s || !offsets) fail(BPT_EINVAL, "NULL argument");
         const Samples& S = s->s;
         check_range(S, first, count);
-        use_device(S.g->device);
+        use_device(S.device);
         std::vector<uint32_t> sz(count);
         BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.as<uint32_t>() + (first - S.s0), count * 4, cudaMemcpyDeviceToHost));
         std::vector<uint64_t> off(count + 1, 0);
@@ -561,14 +645,14 @@ bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* seeds, u
     return guarded([&] {
         if (!s) fail(BPT_EINVAL, "samples is NULL");
         const Samples& S = s->s;
-        if (k == 0 || k > S.g->n) fail(BPT_EINVAL, "k must be in [1, n]");
-        use_device(S.g->device);
+        if (k == 0 || k > S.n) fail(BPT_EINVAL, "k must be in [1, n]");
+        use_device(S.device);
         std::vector<uint32_t> hs(k);
         std::vector<uint64_t> hg(k);
         select_seeds(S, k, hs.data(), hg.data(), 0);
         uint64_t covered = 0;
         for (uint32_t i = 0; i < k; ++i) covered += hg[i];
-        const double sig = (double)S.g->n * (double)covered / (double)S.theta;  // reading C-12
+        const double sig = (double)S.n * (double)covered / (double)S.theta;  // reading C-12
         if (seeds) BPT_CUDA(cudaMemcpy(seeds, hs.data(), k * 4, cudaMemcpyDefault));
         if (gains) BPT_CUDA(cudaMemcpy(gains, hg.data(), k * 8, cudaMemcpyDefault));
         if (sigma_hat) {
@@ -582,7 +666,7 @@ void bpt_samples_free(bpt_samples* s) {
     if (!s) return;
     int cur = -1;
     cudaGetDevice(&cur);
-    if (cur != s->s.g->device) cudaSetDevice(s->s.g->device);
+    if (cur != s->s.device) cudaSetDevice(s->s.device);
     delete s;
 }
 

@@ -59,12 +59,15 @@ struct Comm {
 struct DevBuf {  // RAII device allocation
     void* p = nullptr;
     size_t bytes = 0;
+    int device = 0;
     DevBuf() = default;
     explicit DevBuf(size_t b) { alloc(b); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
-    DevBuf& operator=(DevBuf&& o) noexcept { reset(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; return *this; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), device(o.device) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        reset(); p = o.p; bytes = o.bytes; device = o.device; o.p = nullptr; o.bytes = 0; return *this;
+    }
     ~DevBuf() { reset(); }
     void alloc(size_t b);
     void reset();
@@ -96,7 +99,10 @@ constexpr int kPackShift = 36;
 constexpr unsigned long long kEdgeMask = (1ull << kPackShift) - 1;
 
 struct Samples {
-    const Graph* g = nullptr;
+    const Graph* g = nullptr;   // valid only inside bpt_sample; the samples outlive the graph
+    uint32_t n = 0;
+    int device = 0;
+    Comm* comm = nullptr;       // must outlive the samples (selection collectives)
     int model = 0;
     uint64_t theta = 0, seed = 0, s0 = 0, s1 = 0;
     uint32_t colors = 64;
@@ -116,34 +122,71 @@ struct Samples {
 void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_col, const float* d_wf,
                        const uint32_t* d_wq, cudaStream_t st);
 // k_sample.cu
+// Device-resident control block of the level / batch loops (read by every sampling kernel,
+// advanced on the device, so the loops need no host round trip).
+struct Ctl {
+    uint32_t level;          // current level of the current batch
+    uint32_t cont;           // 1 while the current batch has a non-empty frontier
+    uint64_t blk0;           // first local 64-sample block of the current batch
+    uint64_t gblk0;          // its global block index (sample base = 64 * (gblk0 + slot))
+    uint32_t slots;          // blocks in the current batch
+    uint32_t batch;          // batch index
+    uint32_t error;          // 1 queue overflow, 2 too many levels
+    uint32_t stats_used;     // level rows written to the stats buffer
+    unsigned long long work, vc, coins, atomics, entries, levels_total;
+    unsigned long long expand_ns;        // sum over expansion launches of (last end - first start)
+    unsigned long long t_start, t_end;   // %globaltimer stamps of the running expansion launch
+    uint32_t levels_max;
+    uint32_t stats_overflow;
+};
+constexpr int kMaxLevels = 8192;
+
 struct BatchArgs {
     const uint32_t* roff;
     const uint2* rec;
     uint32_t n;
     int model;
     uint32_t colors;
-    uint64_t* store;          // V base of the local store
-    uint64_t* N;              // next-frontier accumulators [slots][n]
+    uint64_t* store;          // the local RRR store V[blocks][n] (written by the finaliser)
+    ulonglong2* VN;           // per in-flight block working masks {V visited, N next frontier} [slots][n]:
+                              // V[u] and N[u] share one 32-B sector (one gather, one atomic target)
     unsigned long long* raw;  // raw queue entries
     uint64_t raw_cap;
     uint4* q;                 // compacted entries {v, slot, mask lo, mask hi}
+    uint4* umask;             // IC: per 128-item work unit, bit i set iff an entry starts at item i
     uint64_t* qoff;           // exclusive prefix of per-entry work
     uint64_t q_cap;
-    LevelRec* lv;             // level records
-    uint64_t blk0;            // first local block of the batch
-    uint64_t gblk0;           // first global block of the batch (sample base = 64 * (gblk0 + slot))
-    uint32_t slots;           // blocks in this batch
+    LevelRec* lv;             // level records of the current batch (kMaxLevels)
+    LevelRec* stats;          // copy of every level record, tagged (batch << 32 | level) in .pad
+    uint32_t stats_cap;
+    uint32_t slots_max;       // blocks per batch
+    uint64_t blocks;          // local blocks of this rank
+    Ctl* ctl;
     uint64_t theta;           // global sample count (bits of samples >= theta stay 0)
     uint32_t k_ic, k_lt, k_start;
 };
-void launch_init(const BatchArgs& a, cudaStream_t st);
 // k_store.cu
-void launch_finalize(const Samples& S, uint64_t blk0, uint32_t slots, const uint32_t* roff, cudaStream_t st,
-                     unsigned long long* d_elog);
-void launch_count_accumulate(const Samples& S, uint64_t blk0, uint32_t slots, cudaStream_t st);
+void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
+                     cudaStream_t st, unsigned long long* d_elog);
+void launch_count_accumulate(const Samples& S, const Ctl* ctl, cudaStream_t st);
+void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
+                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last);
+// k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph
+void launch_init(const BatchArgs& a, cudaStream_t st);
+void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,
+                  cudaEvent_t ev1);
+void launch_next_batch(const BatchArgs& a, cudaStream_t st);
+struct StoreHook {  // adds the per-batch finalise nodes after the level loop
+    const Samples* S;
+    ulonglong2* VN;
+    const uint32_t* roff;
+    unsigned long long* d_elog;
+};
+cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);
 // k_select.cu
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st);
 
 int num_sms();
+void release_cached_blocks();
 
 }  // namespace bpt

@@ -194,7 +194,7 @@ void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_co
     k_validate_rows<<<grid_for(n, 256), 256, 0, st>>>(d_row_ptr, n, m, err);
     k_validate_edges<<<grid_for(m, 256), 256, 0, st>>>(d_col, n, m, d_wf, d_wq, err);
     count_launch(2);
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_validate_edges");
     BuildErr h{};
     BPT_CUDA(cudaMemcpyAsync(&h, err, sizeof(BuildErr), cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
@@ -236,11 +236,11 @@ void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_co
     }
     k_row_offsets<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(ka, m, n, g.roff.as<uint32_t>());
     count_launch();
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_row_offsets");
     if (g.model == BPT_LT && m) {
         k_lt_prefix<<<grid_for((uint64_t)n * 32, 256), 256, 0, st>>>(g.roff.as<uint32_t>(), n, g.rec.as<uint2>(), err);
         count_launch();
-        BPT_CUDA(cudaGetLastError());
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_lt_prefix");
         BPT_CUDA(cudaMemcpyAsync(&h, err, sizeof(BuildErr), cudaMemcpyDeviceToHost, st));
         BPT_CUDA(cudaStreamSynchronize(st));
         if (h.bad_lt != ~0ull)

@@ -44,6 +44,12 @@ __device__ __forceinline__ uint32_t nth_set_bit64(uint64_t x, uint32_t r) {
     return base;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned long long block_sum_ull(unsigned long long x, unsigned long long* sh) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(kFull, x, d);
@@ -59,20 +65,26 @@ __device__ __forceinline__ unsigned long long block_sum_ull(unsigned long long x
 
 // ------------------------------------------------------------------------ A2: init
 // Sample s = 64*(gblk0 + slot) + bit, colour bit of block slot. start(s) per reading C-3.
-// Listing 1 lines 1-3: frontier[start].c = 1 -> here N[slot][start] |= bit,
+// Listing 1 lines 1-3: frontier[start].c = 1 -> here VN[slot][start].N |= bit,
 // first setter of the (slot, slice) enqueues the raw entry of level 0.
-__global__ void k_init(BatchArgs a) {
-    const uint64_t total = (uint64_t)a.slots * 64;
+__global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
+    const uint64_t total = (uint64_t)a.ctl->slots * 64;
+    const uint64_t gblk0 = a.ctl->gblk0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->cont = 1;
+        a.ctl->level = 0;
+        if (use_cond) cudaGraphSetConditional(h_level, 1);
+    }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t slot = (uint32_t)(i >> 6), bit = (uint32_t)(i & 63);
-        const uint64_t s = 64ull * (a.gblk0 + slot) + bit;
+        const uint64_t s = 64ull * (gblk0 + slot) + bit;
         if (s >= a.theta) continue;
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), a.k_start);
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
         const uint32_t slice = bit / a.colors;
         const uint64_t smask = slice_mask_of(a.colors, slice);
-        const unsigned long long old = atomicOr((unsigned long long*)&a.N[(size_t)slot * a.n + start], 1ull << bit);
+        const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + start].y, 1ull << bit);
         if ((old & smask) == 0) {
             const unsigned pos = atomicAdd(&a.lv[0].raw, 1u);
             if (pos < a.raw_cap) a.raw[pos] = raw_pack(start, slot, slice);
@@ -84,63 +96,82 @@ __global__ void k_init(BatchArgs a) {
 // ------------------------------------------------------------------------ A4: compaction
 // For each discovered (v, slot, slice) of level L: mask = N & slice; N &= ~slice;
 // V |= mask (Listing 1 line 8 "visited[v] = visited[v] | fr_v"); keep the entry if v has
-// in-edges (its expansion has work); warp ballot + block prefix give the output slots,
-// one packed atomicAdd per block allocates (entries, work) consistently.
-__global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, int level, uint32_t* __restrict__ tstart,
-                                                      uint64_t tstart_cap) {
-    LevelRec* L = &a.lv[level];
-    const uint32_t nraw = min((uint64_t)L->raw, a.raw_cap);
+// in-edges (its expansion has work). 4 entries per thread (loads issued together); warp
+// shuffle scans + one packed atomicAdd per 1,024-entry block tile allocate (entries, work)
+// consistently; every work unit whose first item falls in the entry's range gets its index.
+constexpr int kCompItems = 4;
+constexpr uint32_t kCompTile = kThreads * kCompItems;
+
+__global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                      uint64_t tstart_cap, uint32_t unit) {
+    if (!a.ctl->cont) return;
+    LevelRec* L = &a.lv[a.ctl->level];
+    const uint64_t nraw = umin64(L->raw, a.raw_cap);
     __shared__ unsigned long long wsum[kWarps];
     __shared__ uint32_t wcnt[kWarps];
     __shared__ unsigned long long blk_base;
     __shared__ unsigned long long vc_acc[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
     unsigned long long vc_local = 0;
-    for (uint64_t tile0 = (uint64_t)blockIdx.x * kThreads; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kThreads) {
-        const uint64_t i = tile0 + threadIdx.x;
-        bool keep = false;
-        uint32_t v = 0, slot = 0;
-        uint64_t mask = 0, work = 0;
-        uint32_t rowstart = 0;
-        if (i < nraw) {
-            const uint64_t r = a.raw[i];
-            v = (uint32_t)r;
-            slot = (uint32_t)(r >> 32) & ((1u << 26) - 1u);
-            const uint32_t slice = (uint32_t)(r >> 58);
-            unsigned long long* Np = (unsigned long long*)&a.N[(size_t)slot * a.n + v];
-            uint64_t* Vp = &a.store[(size_t)(a.blk0 + slot) * a.n + v];
-            if (a.colors == 64) {
-                mask = *Np;
-                *Np = 0;
-                *Vp |= mask;
-            } else {
-                const uint64_t sm = slice_mask_of(a.colors, slice);
-                mask = atomicAnd(Np, ~sm) & sm;
-                atomicOr((unsigned long long*)Vp, mask);
-            }
-            vc_local += __popcll(mask);
-            rowstart = a.roff[v];
-            const uint32_t deg = a.roff[v + 1] - rowstart;
-            work = a.model == BPT_IC ? deg : (deg ? __popcll(mask) : 0);
-            keep = work != 0;
+    for (uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kCompTile) {
+        uint64_t r[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
+            r[it] = i < nraw ? a.raw[i] : ~0ull;
         }
-        // warp-level ballot + prefix (count) and shuffle prefix (work)
-        const uint32_t bal = __ballot_sync(kFull, keep);
-        const uint32_t rank = __popc(bal & lt);
-        unsigned long long wincl = work;
+        uint64_t mask[kCompItems];
+        uint32_t rs[kCompItems], re[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            mask[it] = 0;
+            rs[it] = re[it] = 0;
+            if (r[it] != ~0ull) {
+                const uint32_t v = (uint32_t)r[it];
+                const uint32_t slot = (uint32_t)(r[it] >> 32) & ((1u << 26) - 1u);
+                ulonglong2* p = &a.VN[(size_t)slot * a.n + v];
+                if (a.colors == 64) {
+                    const ulonglong2 x = *p;
+                    mask[it] = x.y;
+                    *p = make_ulonglong2(x.x | x.y, 0ull);
+                } else {
+                    const uint64_t sm = slice_mask_of(a.colors, (uint32_t)(r[it] >> 58));
+                    mask[it] = atomicAnd(&p->y, ~sm) & sm;
+                    atomicOr(&p->x, mask[it]);
+                }
+                rs[it] = __ldg(&a.roff[v]);
+                re[it] = __ldg(&a.roff[v + 1]);
+            }
+        }
+        uint32_t cnt = 0;
+        unsigned long long work_t = 0;
+        uint64_t work[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            vc_local += __popcll(mask[it]);
+            const uint32_t deg = re[it] - rs[it];
+            work[it] = a.model == BPT_IC ? deg : (deg ? __popcll(mask[it]) : 0);
+            cnt += work[it] != 0;
+            work_t += work[it];
+        }
+        // warp inclusive scans of (count, work)
+        uint32_t cincl = cnt;
+        unsigned long long wincl = work_t;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            unsigned long long y = __shfl_up_sync(kFull, wincl, d);
-            if (lane >= d) wincl += y;
+            const uint32_t yc = __shfl_up_sync(kFull, cincl, d);
+            const unsigned long long yw = __shfl_up_sync(kFull, wincl, d);
+            if (lane >= d) { cincl += yc; wincl += yw; }
         }
-        if (lane == 31) { wsum[wid] = wincl; wcnt[wid] = __popc(bal); }
+        if (lane == 31) { wsum[wid] = wincl; wcnt[wid] = cincl; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            unsigned long long ts = 0; uint32_t tc = 0;
+            unsigned long long ts = 0;
+            uint32_t tc = 0;
             for (int w = 0; w < kWarps; ++w) {
-                unsigned long long s = wsum[w]; uint32_t c = wcnt[w];
-                wsum[w] = ts; wcnt[w] = tc; ts += s; tc += c;
+                const unsigned long long s2 = wsum[w];
+                const uint32_t c2 = wcnt[w];
+                wsum[w] = ts; wcnt[w] = tc; ts += s2; tc += c2;
             }
             unsigned long long old = tc ? atomicAdd(&L->packed, ((unsigned long long)tc << kPackShift) + ts) : 0ull;
             if (tc && ((old >> kPackShift) + tc > a.q_cap || (old & kEdgeMask) + ts > kEdgeMask)) {
@@ -151,16 +182,27 @@ __global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, int level, ui
         }
         __syncthreads();
         const unsigned long long bb = blk_base;
-        if (keep && bb != ~0ull) {
-            const uint64_t qi = (bb >> kPackShift) + wcnt[wid] + rank;
-            const uint64_t off = (bb & kEdgeMask) + wsum[wid] + wincl - work;
-            a.q[qi] = make_uint4(v, slot, (uint32_t)mask, (uint32_t)(mask >> 32));
-            a.qoff[qi] = off;
-            // tiles whose first work item falls inside [off, off + work)
-            uint64_t t = (off + kTile - 1) / kTile;
-            for (; t * kTile < off + work; ++t) {
-                if (t < tstart_cap) tstart[t] = (uint32_t)qi;
-                else L->overflow = 1;
+        if (bb != ~0ull && cnt) {
+            uint64_t qi = (bb >> kPackShift) + wcnt[wid] + cincl - cnt;
+            uint64_t off = (bb & kEdgeMask) + wsum[wid] + wincl - work_t;
+#pragma unroll
+            for (int it = 0; it < kCompItems; ++it) {
+                if (!work[it]) continue;
+                const uint32_t v = (uint32_t)r[it];
+                const uint32_t slot = (uint32_t)(r[it] >> 32) & ((1u << 26) - 1u);
+                // IC entries carry delta = rowstart - off (mod 2^32): edge id e = t + delta for
+                // work item t; LT entries carry the vertex itself
+                const uint32_t x = a.model == BPT_IC ? rs[it] - (uint32_t)off : v;
+                a.q[qi] = make_uint4(x, slot, (uint32_t)mask[it], (uint32_t)(mask[it] >> 32));
+                a.qoff[qi] = off;
+                if (a.umask && (off >> 7) < tstart_cap)
+                    atomicOr(reinterpret_cast<uint32_t*>(&a.umask[off >> 7]) + ((off >> 5) & 3u), 1u << (off & 31u));
+                for (uint64_t t = (off + unit - 1) / unit; t * unit < off + work[it]; ++t) {
+                    if (t < tstart_cap) tstart[t] = (uint32_t)qi;
+                    else L->overflow = 1;
+                }
+                ++qi;
+                off += work[it];
             }
         }
         __syncthreads();
@@ -171,19 +213,12 @@ __global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, int level, ui
 }
 
 // ------------------------------------------------------------------------ A3: expansion
-struct SmemTile {
+struct SmemTile {  // LT expansion tile staging
     uint32_t rel[kTile + 1];   // max(qoff - t0, 0) per entry of the tile
-    uint32_t aux[kTile + 1];   // IC: e - t (mod 2^32); LT: row start
+    uint32_t aux[kTile + 1];   // tasks of the entry before the tile
     uint32_t v[kTile + 1];     // LT: vertex
     uint32_t slot[kTile + 1];
     unsigned long long mask[kTile + 1];
-    // per-warp coin flattening scratch
-    uint32_t f_excl[kWarps][32];
-    uint32_t f_e[kWarps][32];
-    uint32_t f_thr[kWarps][32];
-    uint32_t f_sbase[kWarps][32];
-    unsigned long long f_live[kWarps][32];
-    unsigned long long f_pass[kWarps][32];
     unsigned long long red[kWarps];
     uint32_t cnt;
 };
@@ -207,125 +242,258 @@ __device__ __forceinline__ void enqueue_warp(const BatchArgs& a, LevelRec* Lnext
 // of v: u = src[e]; live = mask & ~V[u]; every live colour c keeps its bit iff the coin
 // of (sample c, e) passes (reading C-2); surviving bits are OR-merged into N[u] (line 14,
 // the fusing step); the first setter of N[u] (per slice) enqueues u for level L+1.
-// Each edge record is read once per level for all live colours. The live (edge, colour)
-// coin tasks of a warp are flattened and evaluated 32 at a time.
-__global__ void __launch_bounds__(kThreads) k_expand_ic(BatchArgs a, int level, const uint32_t* __restrict__ tstart) {
+//
+// Warp-centric and barrier-free: a warp owns units of 128 consecutive work items (reverse
+// edge reads) as 4 windows of 32 lanes. The entry of every item comes from one coalesced
+// load of the next 128 entry offsets + a REDUX.OR of the entry starts per window (no
+// per-edge search). The 4 windows' loads are issued together (4x memory-level
+// parallelism). The live colours of all 128 edges are flattened into one list of
+// (edge, colour) coin tasks evaluated 32 at a time (full lanes, no divergence to the
+// warp's maximum colour count). Discovered vertices go through a per-warp shared buffer,
+// so the global queue counter sees one atomic per >= 32 entries.
+constexpr int kUnitIC = 128;
+constexpr int kWinIC = kUnitIC / 32;
+constexpr int kEbuf = 160;       // <= 31 pending + 128 new entries per unit
+
+struct WarpScratch {
+    uint32_t excl[32];                  // exclusive prefix of the lanes' task counts
+    uint32_t cum[32];                   // per-lane window prefix: c0 | (c0+c1) << 8 | (c0+c1+c2) << 16
+    unsigned long long live[kWinIC][32];
+    uint32_t e[kWinIC][32];
+    uint32_t thr[kWinIC][32];
+    uint32_t sbase[kWinIC][32];
+    unsigned long long pass[kWinIC][32];  // updated through its 32-bit halves: native ATOMS.OR
+    unsigned long long ebuf[kEbuf];
+    uint32_t ecount;
+};
+
+__device__ __forceinline__ void warp_flush(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane) {
+    const uint32_t cnt = W.ecount;
+    if (cnt == 0) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&Ln->raw, cnt);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t pos = (uint64_t)base + i;
+        if (pos < a.raw_cap) a.raw[pos] = W.ebuf[i];
+        else Ln->overflow = 1;
+    }
+    __syncwarp();
+    if (lane == 0) W.ecount = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, uint32_t o, uint32_t w, uint32_t bit) {
+    const uint32_t x = philox2x32_10(W.e[w][o], W.sbase[w][o] + bit, a.k_ic).x;
+    if ((x >> 1) < W.thr[w][o])
+        atomicOr(reinterpret_cast<uint32_t*>(&W.pass[w][o]) + (bit >> 5), 1u << (bit & 31));
+}
+
+// One 128-item unit. kWhole: all 128 items valid (every unit but the last of a level), so no
+// per-lane predication is needed on the loads.
+template <bool kWhole, bool kC64>
+__device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane,
+                                               uint32_t le_mask, uint64_t unit, uint64_t t0, uint32_t rem,
+                                               uint32_t jc0, uint64_t gblk0, unsigned long long& coins,
+                                               unsigned long long& atoms) {
+    const uint32_t t0l = (uint32_t)t0;
+    // ---- entry of every item: jc0 contains item 0; the compaction marked every entry start in
+    //      the unit's 128-bit mask (the unit's own mask is cleared here for the next level)
+    const uint4 um = a.umask[unit];
+    __syncwarp();
+    if (lane == 0) a.umask[unit] = make_uint4(0, 0, 0, 0);
+    const uint32_t mw[kWinIC] = {um.x & ~1u, um.y, um.z, um.w};  // an entry starting at item 0 is jc0
+    uint32_t jl[kWinIC];
+    uint32_t before = jc0;
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        jl[w] = before + __popc(mw[w] & le_mask);
+        before += __popc(mw[w]);
+    }
+    // ---- loads of the 4 windows issued together (32-bit index math: slots * n < 2^32).
+    //      Invalid items of the last unit re-read a valid item and are masked out below.
+    uint4 ent[kWinIC];
+    uint2 rc[kWinIC];
+    uint32_t vidx[kWinIC];
+    uint64_t live[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) ent[w] = a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        // an invalid item re-reads item 0 of the unit, which lies in entry jc0
+        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        rc[w] = __ldg(&a.rec[t0l + i + ent[w].x]);
+    }
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        // {V[u], N[u]}: colours visited, or already merged into u this level by another edge
+        // (a possibly stale N only skips fewer coins; the merged result is the same)
+        vidx[w] = ent[w].y * a.n + rc[w].x;
+        const ulonglong2 vn = __ldg(&a.VN[vidx[w]]);
+        live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
+        if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
+    }
+    // ---- coin tasks of the whole unit, flattened into one list
+    uint32_t c[kWinIC], tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) { c[w] = __popcll(live[w]); tot += c[w]; }
+    const uint32_t incl = warp_incl_scan_u32(tot, lane);
+    const uint32_t ntask = __shfl_sync(kFull, incl, 31);
+    uint64_t pass[kWinIC] = {0, 0, 0, 0};
+    if (ntask) {
+#pragma unroll
+        for (int w = 0; w < kWinIC; ++w) {
+            W.e[w][lane] = t0l + 32u * w + lane + ent[w].x;
+            W.thr[w][lane] = rc[w].y;
+            W.sbase[w][lane] = (uint32_t)(64ull * (gblk0 + ent[w].y));
+            W.pass[w][lane] = 0;
+        }
+        {
+            // search the owner lane and the colour bit of every task
+            W.excl[lane] = incl - tot;
+            W.cum[lane] = c[0] | ((c[0] + c[1]) << 8) | ((c[0] + c[1] + c[2]) << 16);
+#pragma unroll
+            for (int w = 0; w < kWinIC; ++w) W.live[w][lane] = live[w];
+            __syncwarp();
+            for (uint32_t b = 0; b < ntask; b += 32) {
+                const uint32_t k = b + lane;
+                if (k < ntask) {
+                    uint32_t o = 0;  // owner lane = largest lane with excl <= k
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (W.excl[o + step] <= k) o += step;
+                    uint32_t r = k - W.excl[o];
+                    const uint32_t cm = W.cum[o];
+                    const uint32_t p0 = cm & 0xffu, p1 = (cm >> 8) & 0xffu, p2 = cm >> 16;
+                    const uint32_t w = (r >= p0) + (r >= p1) + (r >= p2);
+                    r -= w == 0 ? 0u : (w == 1 ? p0 : (w == 2 ? p1 : p2));
+                    coin_task(a, W, o, w, nth_set_bit64(W.live[w][o], r));
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int w = 0; w < kWinIC; ++w) pass[w] = W.pass[w][lane];
+        __syncwarp();
+        if (lane == 0) coins += ntask;
+    }
+    // ---- merges (Listing 1 line 14) of the 4 windows issued together
+    unsigned long long old[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        old[w] = 0;
+        if (pass[w]) {
+            ++atoms;
+            old[w] = atomicOr(&a.VN[vidx[w]].y, pass[w]);
+        }
+    }
+    // ---- first setters -> per-warp buffer (one scan for the whole unit)
+    uint32_t nf = 0;
+    bool first[kWinIC];
+    uint32_t slice[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        slice[w] = 0;
+        first[w] = false;
+        if (pass[w]) {
+            const uint64_t emask = ((uint64_t)ent[w].w << 32) | ent[w].z;
+            if (kC64) {
+                first[w] = old[w] == 0;
+            } else {
+                slice[w] = (uint32_t)(__ffsll((long long)emask) - 1) / a.colors;
+                first[w] = (old[w] & slice_mask_of(a.colors, slice[w])) == 0;
+            }
+            nf += first[w];
+        }
+    }
+    if (!__any_sync(kFull, nf != 0)) return;
+    const uint32_t fincl = warp_incl_scan_u32(nf, lane);
+    const uint32_t nfirst = __shfl_sync(kFull, fincl, 31);
+    uint32_t pos = W.ecount + fincl - nf;
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w)
+        if (first[w]) W.ebuf[pos++] = raw_pack(rc[w].x, ent[w].y, slice[w]);
+    __syncwarp();
+    if (lane == 0) W.ecount += nfirst;
+    __syncwarp();
+    if (W.ecount >= 32) warp_flush(a, Ln, W, lane);
+}
+
+#ifndef BPT_EXPAND_MINB
+#define BPT_EXPAND_MINB 4
+#endif
+template <bool kC64>
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart) {
+    Ctl* ctl = a.ctl;
+    if (!ctl->cont) return;
+    const uint32_t level = ctl->level;
+    const uint64_t gblk0 = ctl->gblk0;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
     const unsigned long long packed = L->packed;
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || L->overflow) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SmemTile& sm = *reinterpret_cast<SmemTile*>(smem_raw);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    const uint64_t ntiles = (total + kTile - 1) / kTile;
-    unsigned long long coins = 0, atoms = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t t0 = tile * kTile;
-        const uint32_t j0 = tstart[tile];
-        const uint64_t jend = tile + 1 < ntiles ? (uint64_t)tstart[tile + 1] + 1 : nq;  // exclusive
-        const uint32_t cnt = (uint32_t)umin64(jend - j0, (uint64_t)kTile + 1);
-        __syncthreads();
-        for (uint32_t k = threadIdx.x; k < cnt; k += kThreads) {
-            const uint64_t j = j0 + k;
-            const uint64_t off = a.qoff[j];
-            const uint4 ent = a.q[j];
-            sm.rel[k] = off <= t0 ? 0u : (uint32_t)(off - t0);
-            sm.aux[k] = a.roff[ent.x] - (uint32_t)off;  // e = t + aux  (mod 2^32)
-            sm.slot[k] = ent.y;
-            sm.mask[k] = (unsigned long long)ent.z | ((unsigned long long)ent.w << 32);
-        }
-        if (threadIdx.x == 0) sm.cnt = cnt;
-        __syncthreads();
-#pragma unroll 1
-        for (int it = 0; it < kItems; ++it) {
-            const uint64_t t = t0 + (uint64_t)it * kThreads + threadIdx.x;
-            const bool valid = t < total;
-            uint64_t live = 0;
-            uint32_t e = 0, thr = 0, u = 0, slot = 0;
-            uint64_t emask = 0;
-            if (valid) {
-                const uint32_t target = (uint32_t)(t - t0);
-                uint32_t lo = 0, hi = cnt;  // largest k with rel[k] <= target
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (sm.rel[mid] <= target) lo = mid; else hi = mid;
-                }
-                e = (uint32_t)t + sm.aux[lo];
-                slot = sm.slot[lo];
-                emask = sm.mask[lo];
-                const uint2 r = __ldg(&a.rec[e]);
-                u = r.x;
-                thr = r.y;
-                const uint64_t Vu = __ldg((const unsigned long long*)&a.store[(size_t)(a.blk0 + slot) * a.n + u]);
-                live = emask & ~Vu;
-            }
-            // ---- coin-task flattening (warp) ----
-            const uint32_t c = __popcll(live);
-            uint32_t incl = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t y = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-            uint64_t pass = 0;
-            if (ntask) {
-                sm.f_excl[wid][lane] = incl - c;
-                sm.f_e[wid][lane] = e;
-                sm.f_thr[wid][lane] = thr;
-                sm.f_sbase[wid][lane] = (uint32_t)(64ull * (a.gblk0 + slot));
-                sm.f_live[wid][lane] = live;
-                sm.f_pass[wid][lane] = 0;
-                __syncwarp();
-                for (uint32_t b = 0; b < ntask; b += 32) {
-                    const uint32_t k = b + lane;
-                    if (k < ntask) {
-                        uint32_t lo = 0;  // owner = largest lane with excl <= k
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1)
-                            if (sm.f_excl[wid][lo + step] <= k) lo += step;
-                        const uint32_t bit = nth_set_bit64(sm.f_live[wid][lo], k - sm.f_excl[wid][lo]);
-                        const uint32_t s = sm.f_sbase[wid][lo] + bit;
-                        const uint32_t r = philox2x32_10(sm.f_e[wid][lo], s, a.k_ic).x;
-                        if ((r >> 1) < sm.f_thr[wid][lo]) atomicOr(&sm.f_pass[wid][lo], 1ull << bit);
-                    }
-                }
-                __syncwarp();
-                pass = sm.f_pass[wid][lane];
-                coins += (lane == 0) ? ntask : 0;
-            }
-            bool first = false;
-            uint64_t entry = 0;
-            if (pass) {
-                ++atoms;
-                const unsigned long long old = atomicOr((unsigned long long*)&a.N[(size_t)slot * a.n + u], pass);
-                const uint32_t slice = a.colors == 64 ? 0u : (uint32_t)(__ffsll((long long)emask) - 1) / a.colors;
-                first = (old & slice_mask_of(a.colors, slice)) == 0;
-                entry = raw_pack(u, slot, slice);
-            }
-            enqueue_warp(a, Ln, first, entry);
-        }
+    if (nq == 0 || L->overflow) {
+        if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+        return;
     }
-    unsigned long long ct = block_sum_ull(coins, sm.red);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+    __shared__ unsigned long long red[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpScratch& W = scratch[wid];
+    if (lane == 0) W.ecount = 0;
+    __syncwarp();
+    const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
+    const uint64_t nunits = (total + kUnitIC - 1) / kUnitIC;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+    unsigned long long coins = 0, atoms = 0;
+    for (uint64_t unit = (uint64_t)blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
+        const uint64_t t0 = unit * kUnitIC;
+        const uint32_t jc0 = tstart[unit];
+        if (t0 + kUnitIC <= total)
+            expand_unit_ic<true, kC64>(a, Ln, W, lane, le_mask, unit, t0, kUnitIC, jc0, gblk0, coins, atoms);
+        else
+            expand_unit_ic<false, kC64>(a, Ln, W, lane, le_mask, unit, t0, (uint32_t)(total - t0), jc0, gblk0, coins,
+                                        atoms);
+    }
+    warp_flush(a, Ln, W, lane);
+    unsigned long long ct = block_sum_ull(coins, red);
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
-    unsigned long long at = block_sum_ull(atoms, sm.red);
+    unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
+    if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
 }
 
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
 // N[u] |= bit c (fusing) and the first setter enqueues u.
-__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, int level, const uint32_t* __restrict__ tstart) {
+__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart) {
+    Ctl* ctl = a.ctl;
+    if (!ctl->cont) return;
+    const uint32_t level = ctl->level;
+    const uint64_t gblk0 = ctl->gblk0;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
     const unsigned long long packed = L->packed;
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || L->overflow) return;
+    if (nq == 0 || L->overflow) {
+        if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+        return;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemTile& sm = *reinterpret_cast<SmemTile*>(smem_raw);
     const uint64_t ntiles = (total + kTile - 1) / kTile;
@@ -363,7 +531,7 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, int level, 
                 const uint64_t emask = sm.mask[lo];
                 const uint32_t r_idx = target - sm.rel[lo] + sm.aux[lo];
                 const uint32_t bit = nth_set_bit64(emask, r_idx);
-                const uint32_t s = (uint32_t)(64ull * (a.gblk0 + slot)) + bit;
+                const uint32_t s = (uint32_t)(64ull * (gblk0 + slot)) + bit;
                 const uint32_t r = philox2x32_10(v, s, a.k_lt).x >> 1;
                 ++coins;
                 uint32_t lo2 = a.roff[v], hi2 = a.roff[v + 1];  // first j with cum[j] > r
@@ -375,10 +543,10 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, int level, 
                 if (lo2 < end) {
                     const uint32_t u = __ldg(&a.rec[lo2]).x;
                     const uint64_t b = 1ull << bit;
-                    const uint64_t Vu = a.store[(size_t)(a.blk0 + slot) * a.n + u];
+                    const uint64_t Vu = a.VN[(size_t)slot * a.n + u].x;
                     if (!(Vu & b)) {
                         ++atoms;
-                        const unsigned long long old = atomicOr((unsigned long long*)&a.N[(size_t)slot * a.n + u], b);
+                        const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + u].y, b);
                         const uint32_t slice = bit / a.colors;
                         first = (old & slice_mask_of(a.colors, slice)) == 0;
                         entry = raw_pack(u, slot, slice);
@@ -392,22 +560,91 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, int level, 
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, sm.red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
+    if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
 }
 
+// ------------------------------------------------------------------------ level / batch control
+// After expand(L): fold level L's record into the totals, keep a tagged copy for the level
+// statistics, stop the batch when level L+1 discovered nothing (or a queue overflowed), and
+// set the level-loop condition of the graph (device-resident loop, no host round trip).
+__global__ void k_advance(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
+    Ctl* c = a.ctl;
+    if (!c->cont) return;  // host-driven mode launches whole chunks; extra levels are no-ops
+    const uint32_t Lv = c->level;
+    const LevelRec R = a.lv[Lv];
+    c->work += R.packed & kEdgeMask;
+    c->entries += R.packed >> kPackShift;
+    c->vc += R.vc;
+    c->coins += R.coins;
+    c->atomics += R.atomics;
+    if (c->t_start != ~0ull && c->t_end > c->t_start) c->expand_ns += c->t_end - c->t_start;
+    c->t_start = ~0ull;
+    c->t_end = 0;
+    if (c->stats_used < a.stats_cap) {
+        LevelRec row = R;
+        row.pad = ((unsigned long long)c->batch << 32) | Lv;
+        a.stats[c->stats_used++] = row;
+    } else {
+        c->stats_overflow = 1;
+    }
+    const LevelRec& Rn = a.lv[Lv + 1];
+    const bool ovf = R.overflow || Rn.overflow;
+    if (ovf) c->error = 1;
+    bool cont = Rn.raw != 0 && !ovf;
+    if (cont && Lv + 2 >= (uint32_t)kMaxLevels) { c->error = 2; cont = false; }
+    c->level = Lv + 1;
+    if (!cont) {
+        c->cont = 0;
+        c->levels_total += Lv + 1;
+        if (Lv + 1 > c->levels_max) c->levels_max = Lv + 1;
+    }
+    if (use_cond) cudaGraphSetConditional(h_level, cont ? 1u : 0u);
+}
+
+// After a batch: clear the level records it used, move to the next batch, set the batch-loop
+// condition (stop early on an error).
+__global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, int use_cond) {
+    Ctl* c = a.ctl;
+    const uint32_t used = c->level + 2;
+    for (uint32_t i = threadIdx.x; i < used && i < (uint32_t)kMaxLevels; i += blockDim.x) {
+        LevelRec z{};
+        a.lv[i] = z;
+    }
+    if (threadIdx.x == 0) {
+        c->batch += 1;
+        c->blk0 += c->slots;
+        c->gblk0 += c->slots;
+        const uint64_t remaining = a.blocks - c->blk0;
+        c->slots = (uint32_t)umin64(a.slots_max, remaining);
+        c->level = 0;
+        c->cont = 0;
+        if (use_cond) cudaGraphSetConditional(h_batch, (remaining > 0 && !c->error) ? 1u : 0u);
+    }
+}
+
+
 int g_expand_grid = 0;
+int g_expand_grid_lt = 0;
 int g_compact_grid = 0;
 
 }  // namespace
 
-uint32_t expand_tile() { return kTile; }
+uint32_t expand_unit(int model) { return model == BPT_IC ? (uint32_t)kUnitIC : kTile; }
 
 int expand_grid() {
     if (!g_expand_grid) {
         int per_sm = 0;
-        BPT_CUDA(cudaFuncSetAttribute(k_expand_ic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
         BPT_CUDA(cudaFuncSetAttribute(k_expand_lt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic, kThreads, sizeof(SmemTile)));
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_ic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(WarpScratch) * kWarps)));
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_ic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(WarpScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true>, kThreads,
+                                                               sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
+        int per_sm_lt = 0;
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_lt, k_expand_lt, kThreads, sizeof(SmemTile)));
+        g_expand_grid_lt = num_sms() * (per_sm_lt > 0 ? per_sm_lt : 1);
         int per_sm_c = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact, kThreads, 0));
         g_compact_grid = num_sms() * (per_sm_c > 0 ? per_sm_c : 1);
@@ -415,29 +652,105 @@ int expand_grid() {
     return g_expand_grid;
 }
 
+static unsigned init_grid(const BatchArgs& a) { return (unsigned)(((uint64_t)a.slots_max * 64 + 255) / 256); }
+
 void launch_init(const BatchArgs& a, cudaStream_t st) {
-    const uint64_t total = (uint64_t)a.slots * 64;
-    const unsigned grid = (unsigned)((total + 255) / 256);
-    k_init<<<grid, 256, 0, st>>>(a);
+    k_init<<<init_grid(a), 256, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
     count_launch();
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_init");
 }
 
-void launch_compact(const BatchArgs& a, int level, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st) {
+// one level of the host-driven loop: compact(L) -> expand(L) (bracketed by ev0/ev1 if given) -> advance
+void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,
+                  cudaEvent_t ev1) {
     expand_grid();
-    k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, level, tstart, tstart_cap);
-    count_launch();
-    BPT_CUDA(cudaGetLastError());
+    k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model));
+    if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
+    if (a.model == BPT_IC && a.colors == 64)
+        k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart);
+    else if (a.model == BPT_IC)
+        k_expand_ic<false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart);
+    else
+        k_expand_lt<<<g_expand_grid_lt, kThreads, sizeof(SmemTile), st>>>(a, tstart);
+    if (ev1) BPT_CUDA(cudaEventRecord(ev1, st));
+    k_advance<<<1, 1, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
+    count_launch(3);
+    ::bpt::check_cuda(cudaGetLastError(), "launch level kernels");
 }
 
-void launch_expand(const BatchArgs& a, int level, const uint32_t* tstart, cudaStream_t st) {
-    const int grid = expand_grid();
-    if (a.model == BPT_IC)
-        k_expand_ic<<<grid, kThreads, sizeof(SmemTile), st>>>(a, level, tstart);
-    else
-        k_expand_lt<<<grid, kThreads, sizeof(SmemTile), st>>>(a, level, tstart);
+void launch_next_batch(const BatchArgs& a, cudaStream_t st) {
+    k_next_batch<<<1, 256, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
     count_launch();
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_next_batch");
+}
+
+// The whole bpt_sample loop as one CUDA graph with two nested conditional WHILE nodes:
+//   while (batches remain) { init -> while (frontier non-empty) { compact -> expand -> advance }
+//                            -> finalize -> count -> next_batch }
+// Conditions are set on the device (cudaGraphSetConditional) by k_advance / k_next_batch, so
+// the host launches the graph once and never polls (SURVEY §8(a) kernel note 4).
+cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h) {
+    expand_grid();
+    cudaGraph_t root;
+    BPT_CUDA(cudaGraphCreate(&root, 0));
+    cudaGraphConditionalHandle h_batch, h_level;
+    BPT_CUDA(cudaGraphConditionalHandleCreate(&h_batch, root, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cb{};
+    cb.type = cudaGraphNodeTypeConditional;
+    cb.conditional.handle = h_batch;
+    cb.conditional.type = cudaGraphCondTypeWhile;
+    cb.conditional.size = 1;
+    cudaGraphNode_t n_batch;
+    BPT_CUDA(cudaGraphAddNode(&n_batch, root, nullptr, 0, &cb));
+    cudaGraph_t body = cb.conditional.phGraph_out[0];
+    BPT_CUDA(cudaGraphConditionalHandleCreate(&h_level, body, 1, cudaGraphCondAssignDefault));
+
+    BatchArgs args = a;
+    int one = 1;
+    auto add_kernel = [&](cudaGraph_t g, const cudaGraphNode_t* dep, void* fn, dim3 grid, dim3 block, size_t smem,
+                          void** params) {
+        cudaKernelNodeParams p{};
+        p.func = fn;
+        p.gridDim = grid;
+        p.blockDim = block;
+        p.sharedMemBytes = (unsigned)smem;
+        p.kernelParams = params;
+        cudaGraphNode_t node;
+        BPT_CUDA(cudaGraphAddKernelNode(&node, g, dep, dep ? 1 : 0, &p));
+        return node;
+    };
+    // batch body: init
+    void* init_args[] = {&args, &h_level, &one};
+    cudaGraphNode_t n_init = add_kernel(body, nullptr, (void*)k_init, dim3(init_grid(a)), dim3(256), 0, init_args);
+    // level loop
+    cudaGraphNodeParams cl{};
+    cl.type = cudaGraphNodeTypeConditional;
+    cl.conditional.handle = h_level;
+    cl.conditional.type = cudaGraphCondTypeWhile;
+    cl.conditional.size = 1;
+    cudaGraphNode_t n_level;
+    BPT_CUDA(cudaGraphAddNode(&n_level, body, &n_init, 1, &cl));
+    cudaGraph_t lbody = cl.conditional.phGraph_out[0];
+    uint32_t unit = expand_unit(a.model);
+    void* cmp_args[] = {&args, &tstart, &tstart_cap, &unit};
+    cudaGraphNode_t n_cmp = add_kernel(lbody, nullptr, (void*)k_compact, dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
+    void* exp_args[] = {&args, &tstart};
+    cudaGraphNode_t n_exp = a.model == BPT_IC
+        ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
+                     dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
+        : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
+    void* adv_args[] = {&args, &h_level, &one};
+    add_kernel(lbody, &n_exp, (void*)k_advance, dim3(1), dim3(1), 0, adv_args);
+    // finalize + count, then next batch
+    cudaGraphNode_t n_store;
+    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);
+    void* nb_args[] = {&args, &h_batch, &one};
+    add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
+
+    cudaGraphExec_t exec;
+    BPT_CUDA(cudaGraphInstantiate(&exec, root, 0));
+    BPT_CUDA(cudaGraphDestroy(root));
+    return exec;
 }
 
 }  // namespace bpt

@@ -96,7 +96,7 @@ void scan_impl(const T* in, T* out, uint64_t count, void* temp, cudaStream_t st)
     k_scan_sums<T><<<1, kScanThreads, 0, st>>>(sums, ntiles);
     k_tile_scan<T><<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, out, count, sums);
     count_launch(3);
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_tile_scan");
 }
 
 }  // namespace

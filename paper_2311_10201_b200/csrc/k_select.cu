@@ -78,8 +78,8 @@ __global__ void k_decrement(const uint64_t* __restrict__ store, uint32_t n, cons
 }  // namespace
 
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st) {
-    const uint32_t n = S.g->n;
-    Comm* comm = S.g->comm;
+    const uint32_t n = S.n;
+    Comm* comm = S.comm;
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
     const uint64_t blocks = S.blocks;
     DevBuf count((uint64_t)S.n_pad * 4), shard(world > 1 ? (uint64_t)S.n_pad / world * 4 : 4), sel(n),
@@ -110,7 +110,7 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
         k_decrement<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
                                            newm.as<uint64_t>(), count.as<uint32_t>());
         count_launch(2);
-        BPT_CUDA(cudaGetLastError());
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_decrement");
     }
     std::vector<unsigned long long> hk(k);
     BPT_CUDA(cudaMemcpyAsync(hk.data(), keys.p, (uint64_t)k * 8, cudaMemcpyDeviceToHost, st));

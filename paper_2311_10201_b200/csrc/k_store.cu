@@ -23,9 +23,12 @@ __device__ __forceinline__ uint64_t digest_mix(uint64_t v) {
 
 constexpr int kFinThreads = 256;
 
-// grid (ranges, slots). Block (r, slot) scans vertices [r*chunk, (r+1)*chunk) of block
-// blk0+slot; thread (sub, c) accumulates colour c over a quarter of the non-zero masks.
-__global__ void __launch_bounds__(kFinThreads) k_finalize(const uint64_t* __restrict__ store, uint32_t n, uint64_t blk0,
+// grid (ranges, slots). Block (r, slot) scans vertices [r*chunk, (r+1)*chunk) of the working
+// masks of in-flight block `slot` (= local block blk0+slot): writes V to the RRR store, clears
+// the working pair for the next batch, and thread (sub, c) accumulates colour c over a quarter
+// of the non-zero masks.
+__global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict__ VN, uint64_t* __restrict__ store,
+                                                          uint32_t n, const Ctl* __restrict__ ctl,
                                                           uint64_t chunk, const uint32_t* __restrict__ roff,
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
                                                           unsigned long long* __restrict__ digests,
@@ -37,8 +40,10 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const uint64_t* __rest
     __shared__ uint32_t s_size[4][64];
     __shared__ unsigned long long s_dig[4][64];
     __shared__ unsigned long long s_el[4][64];
-    const uint64_t blk = blk0 + blockIdx.y;
-    const uint64_t* V = store + (size_t)blk * n;
+    if (blockIdx.y >= ctl->slots) return;
+    const uint64_t blk = ctl->blk0 + blockIdx.y;
+    uint64_t* V = store + (size_t)blk * n;
+    ulonglong2* W = VN + (size_t)blockIdx.y * n;
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -47,7 +52,12 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const uint64_t* __rest
     unsigned long long dig = 0, el = 0;
     for (uint64_t base = v_begin; base < v_end; base += kFinThreads) {
         const uint64_t v = base + threadIdx.x;
-        const uint64_t m = v < v_end ? V[v] : 0ull;
+        uint64_t m = 0;
+        if (v < v_end) {
+            m = W[v].x;
+            V[v] = m;
+            W[v] = make_ulonglong2(0ull, 0ull);
+        }
         const uint32_t bal = __ballot_sync(kFull, m != 0);
         __syncthreads();
         if (lane == 0) s_wcnt[wid] = __popc(bal);
@@ -92,8 +102,10 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const uint64_t* __rest
 }
 
 // count0[v] += sum over the batch's blocks of popcount(V_g[v])  (occurrences, A7 round 0)
-__global__ void k_count_acc(const uint64_t* __restrict__ store, uint32_t n, uint64_t blk0, uint32_t slots,
+__global__ void k_count_acc(const uint64_t* __restrict__ store, uint32_t n, const Ctl* __restrict__ ctl,
                             uint32_t* __restrict__ count0) {
+    const uint64_t blk0 = ctl->blk0;
+    const uint32_t slots = ctl->slots;
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t c = 0;
         for (uint32_t s = 0; s < slots; ++s) c += __popcll(store[(size_t)(blk0 + s) * n + v]);
@@ -157,34 +169,70 @@ __global__ void k_extract_write(const uint64_t* __restrict__ V, uint32_t n, uint
 
 }  // namespace
 
-void launch_finalize(const Samples& S, uint64_t blk0, uint32_t slots, const uint32_t* roff, cudaStream_t st,
-                     unsigned long long* d_elog) {
-    const uint32_t n = S.g->n;
-    uint64_t ranges = (uint64_t)num_sms() * 4 / (slots ? slots : 1);
+// launch configuration of the finaliser for batches of `slots_max` blocks
+static dim3 finalize_grid(uint32_t n, uint32_t slots_max, uint64_t* chunk_out) {
+    uint64_t ranges = (uint64_t)num_sms() * 4 / (slots_max ? slots_max : 1);
     if (ranges < 1) ranges = 1;
     uint64_t chunk = (n + ranges - 1) / ranges;
     chunk = (chunk + kFinThreads - 1) / kFinThreads * kFinThreads;
     if (chunk == 0) chunk = kFinThreads;
     ranges = (n + chunk - 1) / chunk;
-    dim3 grid((unsigned)ranges, slots);
-    k_finalize<<<grid, kFinThreads, 0, st>>>(S.store.as<uint64_t>(), n, blk0, chunk, roff, S.s1 - S.s0,
-                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog);
-    count_launch();
-    BPT_CUDA(cudaGetLastError());
+    *chunk_out = chunk;
+    return dim3((unsigned)ranges, slots_max);
 }
 
-void launch_count_accumulate(const Samples& S, uint64_t blk0, uint32_t slots, cudaStream_t st) {
-    const uint32_t n = S.g->n;
-    unsigned grid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
-    k_count_acc<<<grid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blk0, slots, S.count0.as<uint32_t>());
+static unsigned count_grid(uint32_t n) {
+    return (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
+}
+
+void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
+                     cudaStream_t st, unsigned long long* d_elog) {
+    uint64_t chunk = 0;
+    const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
+    k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
+                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog);
     count_launch();
-    BPT_CUDA(cudaGetLastError());
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
+}
+
+void launch_count_accumulate(const Samples& S, const Ctl* ctl, cudaStream_t st) {
+    k_count_acc<<<count_grid(S.n), 256, 0, st>>>(S.store.as<uint64_t>(), S.n, ctl, S.count0.as<uint32_t>());
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_count_acc");
+}
+
+// graph nodes for the same two kernels (device-resident batch loop)
+void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
+                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last) {
+    uint64_t chunk = 0;
+    const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
+    uint64_t* store = S.store.as<uint64_t>();
+    uint32_t n = S.n;
+    uint64_t nlocal = S.s1 - S.s0;
+    uint32_t* sizes = S.sizes.as<uint32_t>();
+    unsigned long long* digests = S.digests.as<unsigned long long>();
+    void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &digests, &d_elog};
+    cudaKernelNodeParams p{};
+    p.func = (void*)k_finalize;
+    p.gridDim = grid;
+    p.blockDim = dim3(kFinThreads);
+    p.kernelParams = fin_args;
+    cudaGraphNode_t fin;
+    BPT_CUDA(cudaGraphAddKernelNode(&fin, g, &dep, 1, &p));
+    uint32_t* count0 = S.count0.as<uint32_t>();
+    void* cnt_args[] = {&store, &n, (void*)&ctl, &count0};
+    cudaKernelNodeParams q{};
+    q.func = (void*)k_count_acc;
+    q.gridDim = dim3(count_grid(S.n));
+    q.blockDim = dim3(256);
+    q.kernelParams = cnt_args;
+    BPT_CUDA(cudaGraphAddKernelNode(last, g, &fin, 1, &q));
 }
 
 // d_offsets[count+1] must already hold the exclusive scan of sizes (offsets[count] = total)
 void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
                    cudaStream_t st) {
-    const uint32_t n = S.g->n;
+    const uint32_t n = S.n;
     const uint32_t ntiles = (uint32_t)((n + kExTile - 1) / kExTile);
     DevBuf tcnt((uint64_t)64 * ntiles * 4), tmp(scan_temp_bytes((uint64_t)64 * ntiles));
     const uint64_t lfirst = first - S.s0, llast = lfirst + count;  // local sample indices
@@ -199,7 +247,7 @@ void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint6
         exclusive_scan_u32(tcnt.as<uint32_t>(), tcnt.as<uint32_t>(), (uint64_t)64 * ntiles, tmp.p, st);
         k_extract_write<<<grid, 256, 0, st>>>(V, n, c_lo, c_hi, ntiles, tcnt.as<uint32_t>(), out_base, d_members);
         count_launch();
-        BPT_CUDA(cudaGetLastError());
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_extract_write");
     }
 }
 

@@ -89,7 +89,7 @@ def test_invalid_inputs_rejected(bpt):
     col = np.array([1, 0, 1], np.uint32)
     ok = np.array([1, 2, 3], np.uint32)
     cases = [
-        (np.array([0, 3, 2], np.uint64), col, dict(w_q31=ok), "decreasing"),
+        (np.array([0, 2, 1, 3], np.uint64), col, dict(w_q31=ok), "decreasing"),
         (np.array([1, 2, 3], np.uint64), col, dict(w_q31=ok), "row_ptr[0]"),
         (rp, np.array([1, 5, 1], np.uint32), dict(w_q31=ok), "col["),
         (rp, col, dict(w_q31=np.array([1, Q31 + 1, 0], np.uint32)), "weight[1]"),
@@ -324,3 +324,26 @@ def test_c2_full_size_sampled_parity(bpt):
     assert list(gains) == sorted(gains, reverse=True)
     assert int(gains.sum()) <= cfg.theta
     assert sigma == cfg.n * int(gains.sum()) / cfg.theta
+
+
+# ------------------------------------------------------------------ sharding (P-9) and occurrences (P-8)
+
+def test_shard_invariance_and_occurrences(bpt, c2_small):
+    """Every W-way shard reproduces its slice of the W=1 run; shard occurrence counts sum to
+    the W=1 counts, which equal sum_s 1[v in RR_s] from the oracle's lists (SURVEY P-8, P-9)."""
+    cfg, row_ptr, col, thr, ref = c2_small
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    full = g.sample(cfg.theta, seed=cfg.seed)
+    occ = full.occurrences()
+    assert np.array_equal(occ, np.bincount(ref["members"], minlength=cfg.n).astype(np.uint32))
+    for W in (2, 3, 5):
+        acc = np.zeros(cfg.n, np.uint64)
+        for r in range(W):
+            s = g.sample(cfg.theta, seed=cfg.seed, shard=(W, r))
+            s0, s1 = graphgen.shard_range(cfg.theta, W, r)
+            assert (s.s0, s.s1) == (s0, s1)
+            if s1 > s0:
+                assert np.array_equal(s.digests(s0, s1 - s0), ref["digests"][s0:s1])
+                assert np.array_equal(s.sizes(s0, s1 - s0), ref["sizes"][s0:s1])
+            acc += s.occurrences()
+        assert np.array_equal(acc, occ.astype(np.uint64))
