@@ -235,7 +235,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     const uint64_t nbatches = (S.blocks + slots - 1) / slots;
     const uint32_t stats_cap = (uint32_t)umin64(nbatches * 64 + 8192, 1ull << 22);
     DevBuf VN((size_t)slots * n * 16), raw(raw_cap * 8), q(q_cap * 16), qoff(q_cap * 8), tstart(ts_cap * 4),
-        umask(S.model == BPT_IC ? ts_cap * 16 : 16),
+        umask(S.model == BPT_IC ? (ts_cap * tile / 32 + 4) * 4 : 16),
         lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
         elog(8);
     BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
@@ -264,7 +264,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.raw = raw.as<unsigned long long>();
     a.raw_cap = raw_cap;
     a.q = q.as<uint4>();
-    a.umask = S.model == BPT_IC ? umask.as<uint4>() : nullptr;
+    a.umask = S.model == BPT_IC ? umask.as<uint32_t>() : nullptr;
     a.qoff = qoff.as<uint64_t>();
     a.q_cap = q_cap;
     a.lv = lv.as<LevelRec>();
@@ -332,7 +332,6 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
                 cur ^= 1;
             }
             launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>());
-            launch_count_accumulate(S, a.ctl, st);
             launch_next_batch(a, st);
         }
         BPT_CUDA(cudaStreamSynchronize(st));
@@ -383,8 +382,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     // %globaltimer span of every launch (graph mode)
     I.ms_expand = profile ? ev_ms : cf.expand_ns * 1e-6;
     I.expand_launches = profile ? ev_launches : cf.levels_total;
-    // kernels executed: per batch init + finalize + count + next_batch, per level compact + expand + advance
-    if (!profile) g_launches += 4 * nbatches + 3 * cf.levels_total;
+    // kernels executed: per batch init + finalize + next_batch, per level compact + expand
+    if (!profile) g_launches += 3 * nbatches + 2 * cf.levels_total;
     I.kernel_launches = g_launches - launches0;
     I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     if (getenv("BPT_TRACE")) {

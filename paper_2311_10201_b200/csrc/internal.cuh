@@ -138,6 +138,8 @@ struct Ctl {
     unsigned long long t_start, t_end;   // %globaltimer stamps of the running expansion launch
     uint32_t levels_max;
     uint32_t stats_overflow;
+    uint32_t blocks_done;    // expansion blocks finished (the last one advances the level)
+    uint32_t pad_;
 };
 constexpr int kMaxLevels = 8192;
 
@@ -153,7 +155,7 @@ struct BatchArgs {
     unsigned long long* raw;  // raw queue entries
     uint64_t raw_cap;
     uint4* q;                 // compacted entries {v, slot, mask lo, mask hi}
-    uint4* umask;             // IC: per 128-item work unit, bit i set iff an entry starts at item i
+    uint32_t* umask;          // IC: bit t set iff a frontier entry's work starts at item t
     uint64_t* qoff;           // exclusive prefix of per-entry work
     uint64_t q_cap;
     LevelRec* lv;             // level records of the current batch (kMaxLevels)
@@ -168,7 +170,6 @@ struct BatchArgs {
 // k_store.cu
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog);
-void launch_count_accumulate(const Samples& S, const Ctl* ctl, cudaStream_t st);
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last);
 // k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph

@@ -195,8 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, uint32_t* __r
                 const uint32_t x = a.model == BPT_IC ? rs[it] - (uint32_t)off : v;
                 a.q[qi] = make_uint4(x, slot, (uint32_t)mask[it], (uint32_t)(mask[it] >> 32));
                 a.qoff[qi] = off;
-                if (a.umask && (off >> 7) < tstart_cap)
-                    atomicOr(reinterpret_cast<uint32_t*>(&a.umask[off >> 7]) + ((off >> 5) & 3u), 1u << (off & 31u));
+                if (a.umask && off / unit < tstart_cap) atomicOr(&a.umask[off >> 5], 1u << (off & 31u));
                 for (uint64_t t = (off + unit - 1) / unit; t * unit < off + work[it]; ++t) {
                     if (t < tstart_cap) tstart[t] = (uint32_t)qi;
                     else L->overflow = 1;
@@ -238,6 +237,64 @@ __device__ __forceinline__ void enqueue_warp(const BatchArgs& a, LevelRec* Lnext
     }
 }
 
+__device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphConditionalHandle h_level, int use_cond) {
+    Ctl* c = a.ctl;
+    // counters were updated by other blocks' atomics: read them from L2 (__ldcg), not L1
+    const uint32_t Lv = __ldcg(&c->level);
+    LevelRec R;
+    R.packed = __ldcg(&a.lv[Lv].packed);
+    R.vc = __ldcg(&a.lv[Lv].vc);
+    R.coins = __ldcg(&a.lv[Lv].coins);
+    R.atomics = __ldcg(&a.lv[Lv].atomics);
+    R.raw = __ldcg(&a.lv[Lv].raw);
+    R.overflow = __ldcg(&a.lv[Lv].overflow);
+    R.pad = 0;
+    const uint32_t next_raw = __ldcg(&a.lv[Lv + 1].raw);
+    const uint32_t next_ovf = __ldcg(&a.lv[Lv + 1].overflow);
+    c->work += R.packed & kEdgeMask;
+    c->entries += R.packed >> kPackShift;
+    c->vc += R.vc;
+    c->coins += R.coins;
+    c->atomics += R.atomics;
+    const unsigned long long ts = __ldcg(&c->t_start), te = __ldcg(&c->t_end);
+    if (ts != ~0ull && te > ts) c->expand_ns += te - ts;
+    c->t_start = ~0ull;
+    c->t_end = 0;
+    if (c->stats_used < a.stats_cap) {
+        LevelRec row = R;
+        row.pad = ((unsigned long long)c->batch << 32) | Lv;
+        a.stats[c->stats_used++] = row;
+    } else {
+        c->stats_overflow = 1;
+    }
+    const bool ovf = R.overflow || next_ovf;
+    if (ovf) c->error = 1;
+    bool cont = next_raw != 0 && !ovf;
+    if (cont && Lv + 2 >= (uint32_t)kMaxLevels) { c->error = 2; cont = false; }
+    c->level = Lv + 1;
+    if (!cont) {
+        c->cont = 0;
+        c->levels_total += Lv + 1;
+        if (Lv + 1 > c->levels_max) c->levels_max = Lv + 1;
+    }
+    if (use_cond) cudaGraphSetConditional(h_level, cont ? 1u : 0u);
+}
+
+// The last block of an expansion launch to finish advances the level (fused, no extra launch).
+__device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphConditionalHandle h_level, int use_cond) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMax(&a.ctl->t_end, global_ns());
+        __threadfence();
+        const unsigned prev = atomicAdd(&a.ctl->blocks_done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            a.ctl->blocks_done = 0;
+            advance_level(a, h_level, use_cond);
+        }
+    }
+}
+
 // IC, Listing 1 lines 9-15: for each frontier entry (v, slot, mask) and each reverse edge e
 // of v: u = src[e]; live = mask & ~V[u]; every live colour c keeps its bit iff the coin
 // of (sample c, e) passes (reading C-2); surviving bits are OR-merged into N[u] (line 14,
@@ -251,9 +308,12 @@ __device__ __forceinline__ void enqueue_warp(const BatchArgs& a, LevelRec* Lnext
 // (edge, colour) coin tasks evaluated 32 at a time (full lanes, no divergence to the
 // warp's maximum colour count). Discovered vertices go through a per-warp shared buffer,
 // so the global queue counter sees one atomic per >= 32 entries.
-constexpr int kUnitIC = 128;
-constexpr int kWinIC = kUnitIC / 32;
-constexpr int kEbuf = 160;       // <= 31 pending + 128 new entries per unit
+#ifndef BPT_WIN_IC
+#define BPT_WIN_IC 3
+#endif
+constexpr int kWinIC = BPT_WIN_IC;       // 32-lane windows per warp work unit
+constexpr int kUnitIC = 32 * kWinIC;
+constexpr int kEbuf = 32 + kUnitIC;  // <= 31 pending + one unit's new entries
 
 struct WarpScratch {
     uint32_t excl[32];                  // exclusive prefix of the lanes' task counts
@@ -308,10 +368,12 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     const uint32_t t0l = (uint32_t)t0;
     // ---- entry of every item: jc0 contains item 0; the compaction marked every entry start in
     //      the unit's 128-bit mask (the unit's own mask is cleared here for the next level)
-    const uint4 um = a.umask[unit];
+    uint32_t mw[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[unit * kWinIC + w];
     __syncwarp();
-    if (lane == 0) a.umask[unit] = make_uint4(0, 0, 0, 0);
-    const uint32_t mw[kWinIC] = {um.x & ~1u, um.y, um.z, um.w};  // an entry starting at item 0 is jc0
+    if (lane < kWinIC) a.umask[unit * kWinIC + lane] = 0;
+    mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
     uint32_t jl[kWinIC];
     uint32_t before = jc0;
 #pragma unroll
@@ -348,7 +410,9 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     for (int w = 0; w < kWinIC; ++w) { c[w] = __popcll(live[w]); tot += c[w]; }
     const uint32_t incl = warp_incl_scan_u32(tot, lane);
     const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-    uint64_t pass[kWinIC] = {0, 0, 0, 0};
+    uint64_t pass[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) pass[w] = 0;
     if (ntask) {
 #pragma unroll
         for (int w = 0; w < kWinIC; ++w) {
@@ -360,7 +424,13 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         {
             // search the owner lane and the colour bit of every task
             W.excl[lane] = incl - tot;
-            W.cum[lane] = c[0] | ((c[0] + c[1]) << 8) | ((c[0] + c[1] + c[2]) << 16);
+            uint32_t cm = 0, run = 0;  // cumulative task counts of windows 0..2 (0xff: no such window)
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                if (w < kWinIC - 1) run += c[w];
+                cm |= (w < kWinIC - 1 ? run : 0xffu) << (8 * w);
+            }
+            W.cum[lane] = cm;
 #pragma unroll
             for (int w = 0; w < kWinIC; ++w) W.live[w][lane] = live[w];
             __syncwarp();
@@ -372,8 +442,8 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
                     for (int step = 16; step > 0; step >>= 1)
                         if (W.excl[o + step] <= k) o += step;
                     uint32_t r = k - W.excl[o];
-                    const uint32_t cm = W.cum[o];
-                    const uint32_t p0 = cm & 0xffu, p1 = (cm >> 8) & 0xffu, p2 = cm >> 16;
+                    const uint32_t cmo = W.cum[o];
+                    const uint32_t p0 = cmo & 0xffu, p1 = (cmo >> 8) & 0xffu, p2 = cmo >> 16;
                     const uint32_t w = (r >= p0) + (r >= p1) + (r >= p2);
                     r -= w == 0 ? 0u : (w == 1 ? p0 : (w == 2 ? p1 : p2));
                     coin_task(a, W, o, w, nth_set_bit64(W.live[w][o], r));
@@ -429,10 +499,11 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
 }
 
 #ifndef BPT_EXPAND_MINB
-#define BPT_EXPAND_MINB 4
+#define BPT_EXPAND_MINB 5
 #endif
 template <bool kC64>
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart) {
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                              cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
     if (!ctl->cont) return;
     const uint32_t level = ctl->level;
@@ -444,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
     if (nq == 0 || L->overflow) {
-        if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+        finish_expand(a, h_level, use_cond);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -472,14 +543,15 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+    finish_expand(a, h_level, use_cond);
 }
 
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
 // N[u] |= bit c (fusing) and the first setter enqueues u.
-__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart) {
+__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                      cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
     if (!ctl->cont) return;
     const uint32_t level = ctl->level;
@@ -491,7 +563,7 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
     if (nq == 0 || L->overflow) {
-        if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+        finish_expand(a, h_level, use_cond);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -560,47 +632,13 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, sm.red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    if (threadIdx.x == 0) atomicMax(&ctl->t_end, global_ns());
+    finish_expand(a, h_level, use_cond);
 }
 
 // ------------------------------------------------------------------------ level / batch control
 // After expand(L): fold level L's record into the totals, keep a tagged copy for the level
 // statistics, stop the batch when level L+1 discovered nothing (or a queue overflowed), and
 // set the level-loop condition of the graph (device-resident loop, no host round trip).
-__global__ void k_advance(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
-    Ctl* c = a.ctl;
-    if (!c->cont) return;  // host-driven mode launches whole chunks; extra levels are no-ops
-    const uint32_t Lv = c->level;
-    const LevelRec R = a.lv[Lv];
-    c->work += R.packed & kEdgeMask;
-    c->entries += R.packed >> kPackShift;
-    c->vc += R.vc;
-    c->coins += R.coins;
-    c->atomics += R.atomics;
-    if (c->t_start != ~0ull && c->t_end > c->t_start) c->expand_ns += c->t_end - c->t_start;
-    c->t_start = ~0ull;
-    c->t_end = 0;
-    if (c->stats_used < a.stats_cap) {
-        LevelRec row = R;
-        row.pad = ((unsigned long long)c->batch << 32) | Lv;
-        a.stats[c->stats_used++] = row;
-    } else {
-        c->stats_overflow = 1;
-    }
-    const LevelRec& Rn = a.lv[Lv + 1];
-    const bool ovf = R.overflow || Rn.overflow;
-    if (ovf) c->error = 1;
-    bool cont = Rn.raw != 0 && !ovf;
-    if (cont && Lv + 2 >= (uint32_t)kMaxLevels) { c->error = 2; cont = false; }
-    c->level = Lv + 1;
-    if (!cont) {
-        c->cont = 0;
-        c->levels_total += Lv + 1;
-        if (Lv + 1 > c->levels_max) c->levels_max = Lv + 1;
-    }
-    if (use_cond) cudaGraphSetConditional(h_level, cont ? 1u : 0u);
-}
-
 // After a batch: clear the level records it used, move to the next batch, set the batch-loop
 // condition (stop early on an error).
 __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, int use_cond) {
@@ -660,21 +698,22 @@ void launch_init(const BatchArgs& a, cudaStream_t st) {
     ::bpt::check_cuda(cudaGetLastError(), "launch k_init");
 }
 
-// one level of the host-driven loop: compact(L) -> expand(L) (bracketed by ev0/ev1 if given) -> advance
+// one level of the host-driven loop: compact(L) -> expand(L) (bracketed by ev0/ev1 if given; its last
+// block advances the level)
 void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,
                   cudaEvent_t ev1) {
     expand_grid();
     k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model));
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
+    const cudaGraphConditionalHandle h0 = 0;
     if (a.model == BPT_IC && a.colors == 64)
-        k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart);
+        k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
-        k_expand_ic<false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart);
+        k_expand_ic<false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else
-        k_expand_lt<<<g_expand_grid_lt, kThreads, sizeof(SmemTile), st>>>(a, tstart);
+        k_expand_lt<<<g_expand_grid_lt, kThreads, sizeof(SmemTile), st>>>(a, tstart, h0, 0);
     if (ev1) BPT_CUDA(cudaEventRecord(ev1, st));
-    k_advance<<<1, 1, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
-    count_launch(3);
+    count_launch(2);
     ::bpt::check_cuda(cudaGetLastError(), "launch level kernels");
 }
 
@@ -685,9 +724,9 @@ void launch_next_batch(const BatchArgs& a, cudaStream_t st) {
 }
 
 // The whole bpt_sample loop as one CUDA graph with two nested conditional WHILE nodes:
-//   while (batches remain) { init -> while (frontier non-empty) { compact -> expand -> advance }
+//   while (batches remain) { init -> while (frontier non-empty) { compact -> expand }
 //                            -> finalize -> count -> next_batch }
-// Conditions are set on the device (cudaGraphSetConditional) by k_advance / k_next_batch, so
+// Conditions are set on the device (cudaGraphSetConditional) by the expansion / k_next_batch, so
 // the host launches the graph once and never polls (SURVEY §8(a) kernel note 4).
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h) {
     expand_grid();
@@ -734,13 +773,12 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     uint32_t unit = expand_unit(a.model);
     void* cmp_args[] = {&args, &tstart, &tstart_cap, &unit};
     cudaGraphNode_t n_cmp = add_kernel(lbody, nullptr, (void*)k_compact, dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
-    void* exp_args[] = {&args, &tstart};
+    void* exp_args[] = {&args, &tstart, &h_level, &one};
     cudaGraphNode_t n_exp = a.model == BPT_IC
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
-    void* adv_args[] = {&args, &h_level, &one};
-    add_kernel(lbody, &n_exp, (void*)k_advance, dim3(1), dim3(1), 0, adv_args);
+    (void)n_exp;  // the expansion's last block advances the level and sets the loop condition
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
     add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);

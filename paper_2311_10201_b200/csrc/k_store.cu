@@ -25,21 +25,22 @@ constexpr int kFinThreads = 256;
 
 // grid (ranges, slots). Block (r, slot) scans vertices [r*chunk, (r+1)*chunk) of the working
 // masks of in-flight block `slot` (= local block blk0+slot): writes V to the RRR store, clears
-// the working pair for the next batch, and thread (sub, c) accumulates colour c over a quarter
-// of the non-zero masks.
+// the working pair for the next batch and adds the occurrences. Each warp walks its own
+// 32-vertex tiles; lane l accumulates colours l and l+32 over the tile's non-zero masks
+// (broadcast from shared memory), so the per-colour sums cost O(non-zero vertices).
 __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict__ VN, uint64_t* __restrict__ store,
                                                           uint32_t n, const Ctl* __restrict__ ctl,
                                                           uint64_t chunk, const uint32_t* __restrict__ roff,
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
                                                           unsigned long long* __restrict__ digests,
-                                                          unsigned long long* __restrict__ elog_total) {
-    __shared__ unsigned long long s_mask[kFinThreads];
-    __shared__ unsigned long long s_mix[kFinThreads];
-    __shared__ uint32_t s_deg[kFinThreads];
-    __shared__ uint32_t s_wcnt[kFinThreads / 32];
-    __shared__ uint32_t s_size[4][64];
-    __shared__ unsigned long long s_dig[4][64];
-    __shared__ unsigned long long s_el[4][64];
+                                                          unsigned long long* __restrict__ elog_total,
+                                                          uint32_t* __restrict__ count0, int single_slot) {
+    constexpr int kW = kFinThreads / 32;
+    __shared__ unsigned long long s_mask[kW][32];
+    __shared__ unsigned long long s_mix[kW][32];
+    __shared__ uint32_t s_size[kW][64];
+    __shared__ unsigned long long s_dig[kW][64];
+    __shared__ unsigned long long s_el[kW];
     if (blockIdx.y >= ctl->slots) return;
     const uint64_t blk = ctl->blk0 + blockIdx.y;
     uint64_t* V = store + (size_t)blk * n;
@@ -47,69 +48,60 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int sub = threadIdx.x >> 6, c = threadIdx.x & 63;
-    uint32_t size = 0;
-    unsigned long long dig = 0, el = 0;
-    for (uint64_t base = v_begin; base < v_end; base += kFinThreads) {
-        const uint64_t v = base + threadIdx.x;
+    uint32_t sz_lo = 0, sz_hi = 0;
+    unsigned long long dg_lo = 0, dg_hi = 0, el = 0;
+    for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
+        const uint64_t v = base + lane;
         uint64_t m = 0;
         if (v < v_end) {
-            m = W[v].x;
+            m = W[v].x;  // N is 0 after the last level
             V[v] = m;
-            W[v] = make_ulonglong2(0ull, 0ull);
+            if (m) {
+                W[v] = make_ulonglong2(0ull, 0ull);
+                const uint32_t pc = __popcll(m);
+                // occurrences (A7 round 0): one block owns v when the batch has one slot
+                if (single_slot) count0[v] += pc;
+                else atomicAdd(&count0[v], pc);
+                el += (unsigned long long)pc * (roff[v + 1] - roff[v]);  // E_logical: unfused reads
+            }
         }
-        const uint32_t bal = __ballot_sync(kFull, m != 0);
-        __syncthreads();
-        if (lane == 0) s_wcnt[wid] = __popc(bal);
-        __syncthreads();
-        uint32_t off = 0, tot = 0;
-        for (int w = 0; w < kFinThreads / 32; ++w) { if (w < wid) off += s_wcnt[w]; tot += s_wcnt[w]; }
-        if (m) {
-            const uint32_t pos = off + __popc(bal & ((1u << lane) - 1u));
-            s_mask[pos] = m;
-            s_mix[pos] = digest_mix(v);
-            s_deg[pos] = roff[v + 1] - roff[v];
+        uint32_t b = __ballot_sync(kFull, m != 0);
+        if (!b) continue;
+        s_mask[wid][lane] = m;
+        s_mix[wid][lane] = digest_mix(v);
+        __syncwarp();
+        while (b) {
+            const int j = __ffs(b) - 1;
+            b &= b - 1;
+            const unsigned long long mj = s_mask[wid][j], xj = s_mix[wid][j];
+            if ((mj >> lane) & 1ull) { ++sz_lo; dg_lo += xj; }
+            if ((mj >> (lane + 32)) & 1ull) { ++sz_hi; dg_hi += xj; }
         }
-        __syncthreads();
-        for (uint32_t i = sub; i < tot; i += 4) {
-            const uint32_t b = (uint32_t)(s_mask[i] >> c) & 1u;
-            size += b;
-            dig += b ? s_mix[i] : 0ull;
-            el += b ? s_deg[i] : 0u;
-        }
+        __syncwarp();
     }
-    s_size[sub][c] = size;
-    s_dig[sub][c] = dig;
-    s_el[sub][c] = el;
+    s_size[wid][lane] = sz_lo;
+    s_size[wid][lane + 32] = sz_hi;
+    s_dig[wid][lane] = dg_lo;
+    s_dig[wid][lane + 32] = dg_hi;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) el += __shfl_xor_sync(kFull, el, d);
+    if (lane == 0) s_el[wid] = el;
     __syncthreads();
     if (threadIdx.x < 64) {
+        const int c = threadIdx.x;
         uint32_t S = 0;
-        unsigned long long D = 0, E = 0;
-        for (int q = 0; q < 4; ++q) { S += s_size[q][c]; D += s_dig[q][c]; E += s_el[q][c]; }
+        unsigned long long D = 0;
+        for (int q = 0; q < kW; ++q) { S += s_size[q][c]; D += s_dig[q][c]; }
         const uint64_t li = 64ull * blk + c;  // local sample index
         if (li < nlocal) {
             if (S) atomicAdd(&sizes[li], S);
             if (D) atomicAdd(&digests[li], D);
         }
-        s_el[0][c] = E;
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long E = 0;
-        for (int q = 0; q < 64; ++q) E += s_el[0][q];
+        for (int q = 0; q < kW; ++q) E += s_el[q];
         if (E) atomicAdd(elog_total, E);
-    }
-}
-
-// count0[v] += sum over the batch's blocks of popcount(V_g[v])  (occurrences, A7 round 0)
-__global__ void k_count_acc(const uint64_t* __restrict__ store, uint32_t n, const Ctl* __restrict__ ctl,
-                            uint32_t* __restrict__ count0) {
-    const uint64_t blk0 = ctl->blk0;
-    const uint32_t slots = ctl->slots;
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t c = 0;
-        for (uint32_t s = 0; s < slots; ++s) c += __popcll(store[(size_t)(blk0 + s) * n + v]);
-        if (c) count0[v] += c;
     }
 }
 
@@ -181,27 +173,18 @@ static dim3 finalize_grid(uint32_t n, uint32_t slots_max, uint64_t* chunk_out) {
     return dim3((unsigned)ranges, slots_max);
 }
 
-static unsigned count_grid(uint32_t n) {
-    return (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
-}
-
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
-                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog);
+                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog,
+                                             S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
 }
 
-void launch_count_accumulate(const Samples& S, const Ctl* ctl, cudaStream_t st) {
-    k_count_acc<<<count_grid(S.n), 256, 0, st>>>(S.store.as<uint64_t>(), S.n, ctl, S.count0.as<uint32_t>());
-    count_launch();
-    ::bpt::check_cuda(cudaGetLastError(), "launch k_count_acc");
-}
-
-// graph nodes for the same two kernels (device-resident batch loop)
+// graph node for the finaliser (device-resident batch loop)
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last) {
     uint64_t chunk = 0;
@@ -211,22 +194,16 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     uint64_t nlocal = S.s1 - S.s0;
     uint32_t* sizes = S.sizes.as<uint32_t>();
     unsigned long long* digests = S.digests.as<unsigned long long>();
-    void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &digests, &d_elog};
+    uint32_t* count0 = S.count0.as<uint32_t>();
+    int single = slots_max == 1 ? 1 : 0;
+    void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &digests, &d_elog,
+                        &count0, &single};
     cudaKernelNodeParams p{};
     p.func = (void*)k_finalize;
     p.gridDim = grid;
     p.blockDim = dim3(kFinThreads);
     p.kernelParams = fin_args;
-    cudaGraphNode_t fin;
-    BPT_CUDA(cudaGraphAddKernelNode(&fin, g, &dep, 1, &p));
-    uint32_t* count0 = S.count0.as<uint32_t>();
-    void* cnt_args[] = {&store, &n, (void*)&ctl, &count0};
-    cudaKernelNodeParams q{};
-    q.func = (void*)k_count_acc;
-    q.gridDim = dim3(count_grid(S.n));
-    q.blockDim = dim3(256);
-    q.kernelParams = cnt_args;
-    BPT_CUDA(cudaGraphAddKernelNode(last, g, &fin, 1, &q));
+    BPT_CUDA(cudaGraphAddKernelNode(last, g, &dep, 1, &p));
 }
 
 // d_offsets[count+1] must already hold the exclusive scan of sizes (offsets[count] = total)
