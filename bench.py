@@ -162,9 +162,9 @@ def run_reference(args, rank: int, world: int):
     # per step: a bounded sample sized so that warmup + steps finish within ~3 minutes
     t0 = time.perf_counter()
     g.sample_many(cfg.seed, np.arange(threads, dtype=np.uint64), threads)
-    per = max(time.perf_counter() - t0, 1e-3) / threads
+    per = max(time.perf_counter() - t0, 1e-3) / threads  # wall seconds per sample with all threads busy
     nsteps = args.steps + args.warmup
-    per_step = int(max(threads, min(cfg.theta, 150.0 / nsteps / per * threads)))
+    per_step = int(max(threads, min(cfg.theta, 150.0 / nsteps / per)))
     times = []
     for i in range(nsteps):
         ids = np.arange(i * per_step, (i + 1) * per_step, dtype=np.uint64) % cfg.theta

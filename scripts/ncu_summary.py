@@ -60,13 +60,13 @@ def summarise_rep(rep, out_md, levels_log=None):
         d["stalls"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:6])
         launches.append(d)
     lines = [f"# ncu --set full summary: `{os.path.basename(rep)}`", "",
-             "| id | kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM % | L2 hit % | issue active % | warps active % | inst (M) | top stalls (cycles/issue) |",
+             "| id | kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM GB/s | L2 hit % | issue active % | warps active % | inst (M) | top stalls (cycles/issue) |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in launches:
         st = ", ".join(f"{k} {v:.2f}" for k, v in d["stalls"].items())
         lines.append(f"| {d['id']} | {d['kernel']} | {d.get('gpu__time_duration.sum', 0):.1f} | "
                      f"{d.get('dram__bytes_read.sum', 0) / 1e6:.1f} | {d.get('dram__bytes_write.sum', 0) / 1e6:.1f} | "
-                     f"{d.get('dram__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
+                     f"{(d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0)) / max(d.get('gpu__time_duration.sum', 1), 1e-9) / 1e3:.0f} | "
                      f"{d.get('lts__t_sector_hit_rate.pct', 0):.1f} | "
                      f"{d.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
                      f"{d.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
