@@ -348,17 +348,3 @@ def test_shard_invariance_and_occurrences(bpt, c2_small):
             acc += s.occurrences()
         assert np.array_equal(acc, occ.astype(np.uint64))
 
-
-def test_dense_and_sparse_levels_agree(bpt, c2_small, monkeypatch):
-    """Hybrid frontier: levels compacted by a dense scan of the working masks give the
-    same RRR sets, work counters and per-level discovered counts as the queue path."""
-    cfg, row_ptr, col, thr, ref = c2_small
-    g = bpt.Graph(row_ptr, col, w_q31=thr)
-    runs = {}
-    for mode in ("0", "1", "4096"):  # never dense / always dense / default-like threshold
-        monkeypatch.setenv("BPT_DENSE_MIN", mode)
-        s = g.sample(cfg.theta, seed=cfg.seed)
-        check_full(bpt, s, ref, cfg.theta)
-        rows = s.level_stats()
-        runs[mode] = (s.info["e_phys"], s.info["members"], s.info["frontier_entries"], rows[:, [0, 1, 2, 3, 4, 5]].tolist())
-    assert runs["0"] == runs["1"] == runs["4096"]
