@@ -11,6 +11,9 @@
 //   tstart[]   u32   first entry of each expansion tile (written by the compaction)
 // Level L:  compact(L): raw(L) -> V |= N, q/qoff/tstart      (Listing 1 lines 7-8)
 //           expand(L):  q -> N atomicOr, raw(L+1)             (Listing 1 lines 9-15)
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace bpt {
@@ -42,6 +45,32 @@ __device__ __forceinline__ uint32_t nth_set_bit64(uint64_t x, uint32_t r) {
     p = __popc(w & 0x3u);    if (r >= p) { r -= p; w >>= 2;  base += 2; }
     if (r >= (w & 1u)) base += 1;
     return base;
+}
+
+// Edge records stream through once per level: read them with an evict-first L2 policy so the
+// working masks (V, N: 77.6 MB per in-flight block on C2, gathered at random) stay resident in
+// the 126 MB L2; the gathers themselves use evict-last.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_first()));
+    return r;
+}
+__device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(policy_evict_last()));
+    return r;
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -393,14 +422,14 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     for (int w = 0; w < kWinIC; ++w) {
         // an invalid item re-reads item 0 of the unit, which lies in entry jc0
         const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
-        rc[w] = __ldg(&a.rec[t0l + i + ent[w].x]);
+        rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
     }
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
         // {V[u], N[u]}: colours visited, or already merged into u this level by another edge
         // (a possibly stale N only skips fewer coins; the merged result is the same)
         vidx[w] = ent[w].y * a.n + rc[w].x;
-        const ulonglong2 vn = __ldg(&a.VN[vidx[w]]);
+        const ulonglong2 vn = ld_keep(&a.VN[vidx[w]]);
         live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
         if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
     }
@@ -778,7 +807,23 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
-    (void)n_exp;  // the expansion's last block advances the level and sets the loop condition
+    // the expansion's last block advances the level and sets the loop condition
+    if (getenv("BPT_L2PERSIST")) {  // experiment: keep the working masks in the persisting L2 carve-out
+        int maxp = 0, dev = 0;
+        BPT_CUDA(cudaGetDevice(&dev));
+        BPT_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        const size_t bytes = (size_t)a.slots_max * a.n * 16;
+        BPT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
+        cudaKernelNodeAttrValue v{};
+        v.accessPolicyWindow.base_ptr = a.VN;
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = bytes > (size_t)maxp ? (float)maxp / (float)bytes : 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_exp, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+        BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_cmp, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+        if (getenv("BPT_TRACE")) fprintf(stderr, "[bpt] L2 persisting carve-out %d bytes for %zu bytes of VN\n", maxp, bytes);
+    }
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
     add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);
