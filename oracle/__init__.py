@@ -131,7 +131,10 @@ class Graph:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().or_graph_free(h)
+            try:
+                lib().or_graph_free(h)
+            except Exception:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def reverse_csr(self):
