@@ -246,6 +246,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     c0.slots = (uint32_t)umin64(slots, S.blocks);
     c0.gblk0 = S.gb0;
     c0.t_start = ~0ull;
+    c0.c_start = ~0ull;
     static thread_local Ctl* c_host = nullptr;
     if (!c_host) BPT_CUDA(cudaMallocHost(&c_host, sizeof(Ctl)));
     *c_host = c0;
@@ -389,10 +390,10 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     if (getenv("BPT_TRACE")) {
         auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
         fprintf(stderr, "[bpt] sample (%s): alloc %.2f ms, loop %.2f ms (polls %llu, wait %.2f ms), drain+stats %.2f ms, "
-                        "total %.2f ms, batches %llu, slots %llu, levels %llu, expand %.2f ms\n",
+                        "total %.2f ms, batches %llu, slots %llu, levels %llu, expand %.2f ms, compact %.2f ms\n",
                 profile ? "events" : "graph", ms(t_begin, t_alloc), ms(t_alloc, t_loop), (unsigned long long)polls,
                 wait_ms, ms(t_loop, clk::now()), I.ms_total, (unsigned long long)nbatches, (unsigned long long)slots,
-                (unsigned long long)cf.levels_total, I.ms_expand);
+                (unsigned long long)cf.levels_total, I.ms_expand, cf.compact_ns * 1e-6);
     }
 }
 

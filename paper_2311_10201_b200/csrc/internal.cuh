@@ -136,6 +136,8 @@ struct Ctl {
     unsigned long long work, vc, coins, atomics, entries, levels_total;
     unsigned long long expand_ns;        // sum over expansion launches of (last end - first start)
     unsigned long long t_start, t_end;   // %globaltimer stamps of the running expansion launch
+    unsigned long long c_start, c_end;   // ... of the running compaction launch
+    unsigned long long compact_ns;       // sum over compaction launches of (last end - first start)
     uint32_t levels_max;
     uint32_t stats_overflow;
     uint32_t blocks_done;    // expansion blocks finished (the last one advances the level)

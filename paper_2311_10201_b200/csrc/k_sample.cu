@@ -131,15 +131,22 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
 constexpr int kCompItems = 4;
 constexpr uint32_t kCompTile = kThreads * kCompItems;
 
-__global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
+__global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
                                                       uint64_t tstart_cap, uint32_t unit) {
     if (!a.ctl->cont) return;
+    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     LevelRec* L = &a.lv[a.ctl->level];
     const uint64_t nraw = umin64(L->raw, a.raw_cap);
     __shared__ unsigned long long wsum[kWarps];
     __shared__ uint32_t wcnt[kWarps];
     __shared__ unsigned long long blk_base;
     __shared__ unsigned long long vc_acc[kWarps];
+    constexpr uint32_t kBig = 64;
+    __shared__ unsigned long long big_u0[kBig], big_u1[kBig];
+    __shared__ uint32_t big_q[kBig];
+    __shared__ uint32_t big_n;
+    if (threadIdx.x == 0) big_n = 0;
+    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long vc_local = 0;
     for (uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kCompTile) {
@@ -214,6 +221,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, uint32_t* __r
         if (bb != ~0ull && cnt) {
             uint64_t qi = (bb >> kPackShift) + wcnt[wid] + cincl - cnt;
             uint64_t off = (bb & kEdgeMask) + wsum[wid] + wincl - work_t;
+            uint64_t mword = ~0ull;  // entry-start bits, merged per 32-item word before the atomic
+            uint32_t mbits = 0;
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) {
                 if (!work[it]) continue;
@@ -224,20 +233,46 @@ __global__ void __launch_bounds__(kThreads) k_compact(BatchArgs a, uint32_t* __r
                 const uint32_t x = a.model == BPT_IC ? rs[it] - (uint32_t)off : v;
                 a.q[qi] = make_uint4(x, slot, (uint32_t)mask[it], (uint32_t)(mask[it] >> 32));
                 a.qoff[qi] = off;
-                if (a.umask && off / unit < tstart_cap) atomicOr(&a.umask[off >> 5], 1u << (off & 31u));
-                for (uint64_t t = (off + unit - 1) / unit; t * unit < off + work[it]; ++t) {
-                    if (t < tstart_cap) tstart[t] = (uint32_t)qi;
-                    else L->overflow = 1;
+                if (a.umask && off / unit < tstart_cap) {
+                    if ((off >> 5) != mword) {
+                        if (mbits) atomicOr(&a.umask[mword], mbits);
+                        mword = off >> 5;
+                        mbits = 0;
+                    }
+                    mbits |= 1u << (off & 31u);
+                }
+                // work units whose first item falls inside [off, off + work)
+                const uint64_t u0 = (off + unit - 1) / unit, u1 = (off + work[it] + unit - 1) / unit;
+                if (u1 > tstart_cap) L->overflow = 1;
+                const uint64_t u1c = umin64(u1, tstart_cap);
+                if (u1c > u0 + 4) {  // long entry (hub): filled by the whole block below
+                    const uint32_t bi = atomicAdd(&big_n, 1u);
+                    if (bi < kBig) {
+                        big_u0[bi] = u0;
+                        big_u1[bi] = u1c;
+                        big_q[bi] = (uint32_t)qi;
+                    } else {
+                        for (uint64_t t = u0; t < u1c; ++t) tstart[t] = (uint32_t)qi;
+                    }
+                } else {
+                    for (uint64_t t = u0; t < u1c; ++t) tstart[t] = (uint32_t)qi;
                 }
                 ++qi;
                 off += work[it];
             }
+            if (mbits) atomicOr(&a.umask[mword], mbits);
         }
         __syncthreads();
+        const uint32_t nbig = min(big_n, (uint32_t)kBig);
+        for (uint32_t bi = 0; bi < nbig; ++bi)
+            for (uint64_t t = big_u0[bi] + threadIdx.x; t < big_u1[bi]; t += kThreads) tstart[t] = big_q[bi];
+        __syncthreads();
+        if (threadIdx.x == 0) big_n = 0;
     }
     // level statistics
     unsigned long long vc_tot = block_sum_ull(vc_local, vc_acc);
     if (threadIdx.x == 0 && vc_tot) atomicAdd(&L->vc, vc_tot);
+    if (threadIdx.x == 0) atomicMax(&a.ctl->c_end, global_ns());
 }
 
 // ------------------------------------------------------------------------ A3: expansion
@@ -288,6 +323,12 @@ __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphCondi
     const unsigned long long ts = __ldcg(&c->t_start), te = __ldcg(&c->t_end);
     if (ts != ~0ull && te > ts) c->expand_ns += te - ts;
     c->t_start = ~0ull;
+    {
+        const unsigned long long cs = __ldcg(&c->c_start), ce = __ldcg(&c->c_end);
+        if (cs != ~0ull && ce > cs) c->compact_ns += ce - cs;
+        c->c_start = ~0ull;
+        c->c_end = 0;
+    }
     c->t_end = 0;
     if (c->stats_used < a.stats_cap) {
         LevelRec row = R;

@@ -50,34 +50,45 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t sz_lo = 0, sz_hi = 0;
     unsigned long long dg_lo = 0, dg_hi = 0, el = 0;
-    for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
-        const uint64_t v = base + lane;
-        uint64_t m = 0;
-        if (v < v_end) {
-            m = W[v].x;  // N is 0 after the last level
-            V[v] = m;
-            if (m) {
-                W[v] = make_ulonglong2(0ull, 0ull);
-                const uint32_t pc = __popcll(m);
-                // occurrences (A7 round 0): one block owns v when the batch has one slot
-                if (single_slot) count0[v] += pc;
-                else atomicAdd(&count0[v], pc);
-                el += (unsigned long long)pc * (roff[v + 1] - roff[v]);  // E_logical: unfused reads
+    constexpr int kU = 4;  // tiles per warp iteration: their loads are issued together
+    for (uint64_t base = v_begin + 32ull * kU * wid; base < v_end; base += 32ull * kU * kW) {
+        uint64_t m[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t v = base + 32ull * u + lane;
+            m[u] = v < v_end ? W[v].x : 0ull;  // N is 0 after the last level
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t v = base + 32ull * u + lane;
+            if (v < v_end) {
+                V[v] = m[u];
+                if (m[u]) {
+                    W[v] = make_ulonglong2(0ull, 0ull);
+                    const uint32_t pc = __popcll(m[u]);
+                    // occurrences (A7 round 0): one block owns v when the batch has one slot
+                    if (single_slot) count0[v] += pc;
+                    else atomicAdd(&count0[v], pc);
+                    el += (unsigned long long)pc * (roff[v + 1] - roff[v]);  // E_logical: unfused reads
+                }
             }
         }
-        uint32_t b = __ballot_sync(kFull, m != 0);
-        if (!b) continue;
-        s_mask[wid][lane] = m;
-        s_mix[wid][lane] = digest_mix(v);
-        __syncwarp();
-        while (b) {
-            const int j = __ffs(b) - 1;
-            b &= b - 1;
-            const unsigned long long mj = s_mask[wid][j], xj = s_mix[wid][j];
-            if ((mj >> lane) & 1ull) { ++sz_lo; dg_lo += xj; }
-            if ((mj >> (lane + 32)) & 1ull) { ++sz_hi; dg_hi += xj; }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            uint32_t b = __ballot_sync(kFull, m[u] != 0);
+            if (!b) continue;
+            s_mask[wid][lane] = m[u];
+            s_mix[wid][lane] = digest_mix(base + 32ull * u + lane);
+            __syncwarp();
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                const unsigned long long mj = s_mask[wid][j], xj = s_mix[wid][j];
+                if ((mj >> lane) & 1ull) { ++sz_lo; dg_lo += xj; }
+                if ((mj >> (lane + 32)) & 1ull) { ++sz_hi; dg_hi += xj; }
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
     s_size[wid][lane] = sz_lo;
     s_size[wid][lane + 32] = sz_hi;
