@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* 
                 // work item t; LT entries carry the vertex itself
                 const uint32_t x = a.model == BPT_IC ? rs[it] - (uint32_t)off : v;
                 a.q[qi] = make_uint4(x, slot, (uint32_t)mask[it], (uint32_t)(mask[it] >> 32));
-                a.qoff[qi] = off;
+                if (a.model != BPT_IC) a.qoff[qi] = off;  // IC finds entries via tstart + umask
                 if (a.umask && off / unit < tstart_cap) {
                     if ((off >> 5) != mword) {
                         if (mbits) atomicOr(&a.umask[mword], mbits);
