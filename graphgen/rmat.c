@@ -164,15 +164,18 @@ int gg_rmat(uint64_t n, uint64_t m, uint64_t seed, uint64_t* out_row_ptr, uint32
         }
         uint64_t vmask = (1ULL << S) - 1;
         /* forward CSR: count, scan, scatter, sort rows */
+        /* (parallel with atomics; the order inside a row is fixed by the row sort below) */
         memset(out_row_ptr, 0, (n + 1) * sizeof(uint64_t));
-        for (uint64_t e = 0; e < m; e++) out_row_ptr[perm[sel[e] >> S] + 1]++;
+        #pragma omp parallel for schedule(static)
+        for (uint64_t e = 0; e < m; e++) __atomic_fetch_add(&out_row_ptr[perm[sel[e] >> S] + 1], 1, __ATOMIC_RELAXED);
         for (uint64_t v = 0; v < n; v++) out_row_ptr[v + 1] += out_row_ptr[v];
         uint64_t* cur = (uint64_t*)malloc(n * sizeof(uint64_t));
         if (!cur) { free(perm); free(sel); return -2; }
         memcpy(cur, out_row_ptr, n * sizeof(uint64_t));
+        #pragma omp parallel for schedule(static)
         for (uint64_t e = 0; e < m; e++) {
             uint32_t u = perm[sel[e] >> S], v = perm[sel[e] & vmask];
-            out_col[cur[u]++] = v;
+            out_col[__atomic_fetch_add(&cur[u], 1, __ATOMIC_RELAXED)] = v;
         }
         #pragma omp parallel for schedule(dynamic, 1024)
         for (uint64_t u = 0; u < n; u++) {
