@@ -115,6 +115,9 @@ struct Samples {
     uint32_t n_pad = 0;
     bpt_samples_info info{};
     std::vector<uint64_t> level_rows;  // 6 per row
+    // member lists of all local samples (selection on sparse stores), built on demand
+    bool lists_built = false, lists_ok = false;
+    DevBuf list_off, list_mem;
 };
 
 // ------------------------------------------------------------------ launchers

@@ -75,7 +75,53 @@ __global__ void k_decrement(const uint64_t* __restrict__ store, uint32_t n, cons
     }
 }
 
+// sparse stores (e.g. LT): decrement through the members of the newly covered samples,
+// read from their extracted RRR lists (one block per listed 64-sample block)
+__global__ void k_decrement_lists(const uint32_t* __restrict__ nlist, const uint32_t* __restrict__ list,
+                                  const uint64_t* __restrict__ newm, const uint64_t* __restrict__ off,
+                                  const uint32_t* __restrict__ members, uint64_t nlocal,
+                                  uint32_t* __restrict__ count) {
+    const uint32_t L = *nlist;
+    for (uint32_t i = blockIdx.x; i < L; i += gridDim.x) {
+        uint64_t m = newm[i];
+        const uint64_t base = 64ull * list[i];
+        while (m) {
+            const uint32_t c = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const uint64_t s = base + c;
+            if (s >= nlocal) break;
+            for (uint64_t j = off[s] + threadIdx.x; j < off[s + 1]; j += blockDim.x) atomicSub(&count[members[j]], 1u);
+        }
+    }
+}
+
 }  // namespace
+
+void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
+                   cudaStream_t st);
+
+// Member lists of all local samples, if they are small enough to keep (sparse stores); cached.
+static bool build_lists(const Samples& S, cudaStream_t st) {
+    if (S.lists_built) return S.lists_ok;
+    Samples& M = const_cast<Samples&>(S);
+    M.lists_built = true;
+    const uint64_t nlocal = S.s1 - S.s0;
+    const uint64_t bytes = S.info.members * 4 + (nlocal + 1) * 8;
+    size_t free_b = 0, total_b = 0;
+    BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // lists pay off when they are much smaller than one pass over the store
+    if (nlocal == 0 || bytes > free_b / 4 || bytes * 8 > S.store.bytes) return M.lists_ok = false;
+    std::vector<uint32_t> sz(nlocal);
+    BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> off(nlocal + 1, 0);
+    for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
+    M.list_off.alloc((nlocal + 1) * 8);
+    M.list_mem.alloc(off[nlocal] * 4 + 4);
+    BPT_CUDA(cudaMemcpyAsync(M.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (off[nlocal]) extract_range(S, S.s0, nlocal, off.data(), M.list_mem.as<uint32_t>(), st);
+    BPT_CUDA(cudaStreamSynchronize(st));
+    return M.lists_ok = true;
+}
 
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st) {
     const uint32_t n = S.n;
@@ -92,6 +138,7 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     const unsigned ggrid = (unsigned)umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4);
     const unsigned dgrid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
     const uint64_t shard_len = (uint64_t)S.n_pad / world;
+    const bool lists = build_lists(S, st);
     for (uint32_t r = 0; r < k; ++r) {
         unsigned long long* key = keys.as<unsigned long long>() + r;
         if (world > 1) {
@@ -107,8 +154,14 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
         }
         k_cover<<<ggrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blocks, key, cov.as<uint64_t>(), sel.as<uint8_t>(),
                                        nlist.as<uint32_t>(), list.as<uint32_t>(), newm.as<uint64_t>());
-        k_decrement<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
-                                           newm.as<uint64_t>(), count.as<uint32_t>());
+        if (lists)
+            k_decrement_lists<<<num_sms() * 4, 256, 0, st>>>(nlist.as<uint32_t>(), list.as<uint32_t>(),
+                                                             newm.as<uint64_t>(), S.list_off.as<uint64_t>(),
+                                                             S.list_mem.as<uint32_t>(), S.s1 - S.s0,
+                                                             count.as<uint32_t>());
+        else
+            k_decrement<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
+                                               newm.as<uint64_t>(), count.as<uint32_t>());
         count_launch(2);
         ::bpt::check_cuda(cudaGetLastError(), "launch k_decrement");
     }
