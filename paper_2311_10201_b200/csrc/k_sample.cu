@@ -474,29 +474,15 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
         if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
     }
-    // ---- coin tasks. Each lane first evaluates the lowest live colour of each of its windows
-    //      itself (no search); the remaining (edge, colour) tasks of the unit are flattened
-    //      into one list evaluated 32 at a time.
-    uint64_t pass[kWinIC];
-    unsigned long long ncoin = 0;
-#pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
-        pass[w] = 0;
-        if (live[w]) {
-            const uint32_t bit = __ffsll((long long)live[w]) - 1;
-            live[w] &= live[w] - 1;
-            const uint32_t x = philox2x32_10(t0l + 32u * w + lane + ent[w].x,
-                                             (uint32_t)(64ull * (gblk0 + ent[w].y)) + bit, a.k_ic).x;
-            if ((x >> 1) < rc[w].y) pass[w] = 1ull << bit;
-            ++ncoin;
-        }
-    }
+    // ---- coin tasks of the whole unit, flattened into one list
     uint32_t c[kWinIC], tot = 0;
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) { c[w] = __popcll(live[w]); tot += c[w]; }
     const uint32_t incl = warp_incl_scan_u32(tot, lane);
     const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-    coins += ncoin;
+    uint64_t pass[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) pass[w] = 0;
     if (ntask) {
 #pragma unroll
         for (int w = 0; w < kWinIC; ++w) {
@@ -536,7 +522,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         }
         __syncwarp();
 #pragma unroll
-        for (int w = 0; w < kWinIC; ++w) pass[w] |= W.pass[w][lane];
+        for (int w = 0; w < kWinIC; ++w) pass[w] = W.pass[w][lane];
         __syncwarp();
         if (lane == 0) coins += ntask;
     }
