@@ -127,6 +127,7 @@ void launch_compact(const BatchArgs& a, int level, uint32_t* tstart, uint64_t ts
 void launch_expand(const BatchArgs& a, int level, const uint32_t* tstart, cudaStream_t st);
 void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
                    cudaStream_t st);
+void compute_digests(const Samples& S, cudaStream_t st);
 void comm_unique_id(void* out);
 void comm_init(Comm* c, const void* uid);
 void comm_destroy(Comm* c);
@@ -211,7 +212,6 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     S.sizes.alloc(nlocal * 4);
     S.digests.alloc(nlocal * 8);
     BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
-    BPT_CUDA(cudaMemsetAsync(S.digests.p, 0, nlocal * 8, st));
 
     // ---- batch plan
     uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 512);
@@ -609,6 +609,11 @@ bpt_status bpt_rrr_digests(const bpt_samples* s, uint64_t first, uint64_t count,
         if (!s || !digests) fail(BPT_EINVAL, "NULL argument");
         check_range(s->s, first, count);
         use_device(s->s.device);
+        Samples& M = const_cast<Samples&>(s->s);
+        if (!M.digests_ready) {  // verification checksums: computed on first use
+            compute_digests(M, 0);
+            M.digests_ready = true;
+        }
         copy_out(digests, s->s.digests.as<uint64_t>() + (first - s->s.s0), count * 8, 0);
         BPT_CUDA(cudaStreamSynchronize(0));
     });

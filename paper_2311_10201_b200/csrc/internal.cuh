@@ -117,6 +117,7 @@ struct Samples {
     std::vector<uint64_t> level_rows;  // 6 per row
     // member lists of all local samples (selection on sparse stores), built on demand
     bool lists_built = false, lists_ok = false;
+    bool digests_ready = false;
     DevBuf list_off, list_mem;
 };
 

@@ -32,14 +32,11 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
                                                           uint32_t n, const Ctl* __restrict__ ctl,
                                                           uint64_t chunk, const uint32_t* __restrict__ roff,
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
-                                                          unsigned long long* __restrict__ digests,
                                                           unsigned long long* __restrict__ elog_total,
                                                           uint32_t* __restrict__ count0, int single_slot) {
     constexpr int kW = kFinThreads / 32;
     __shared__ unsigned long long s_mask[kW][32];
-    __shared__ unsigned long long s_mix[kW][32];
     __shared__ uint32_t s_size[kW][64];
-    __shared__ unsigned long long s_dig[kW][64];
     __shared__ unsigned long long s_el[kW];
     if (blockIdx.y >= ctl->slots) return;
     const uint64_t blk = ctl->blk0 + blockIdx.y;
@@ -49,7 +46,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t sz_lo = 0, sz_hi = 0;
-    unsigned long long dg_lo = 0, dg_hi = 0, el = 0;
+    unsigned long long el = 0;
     constexpr int kU = 4;  // tiles per warp iteration: their loads are issued together
     for (uint64_t base = v_begin + 32ull * kU * wid; base < v_end; base += 32ull * kU * kW) {
         uint64_t m[kU];
@@ -78,22 +75,19 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
             uint32_t b = __ballot_sync(kFull, m[u] != 0);
             if (!b) continue;
             s_mask[wid][lane] = m[u];
-            s_mix[wid][lane] = digest_mix(base + 32ull * u + lane);
             __syncwarp();
             while (b) {
                 const int j = __ffs(b) - 1;
                 b &= b - 1;
-                const unsigned long long mj = s_mask[wid][j], xj = s_mix[wid][j];
-                if ((mj >> lane) & 1ull) { ++sz_lo; dg_lo += xj; }
-                if ((mj >> (lane + 32)) & 1ull) { ++sz_hi; dg_hi += xj; }
+                const unsigned long long mj = s_mask[wid][j];
+                sz_lo += (uint32_t)(mj >> lane) & 1u;
+                sz_hi += (uint32_t)(mj >> (lane + 32)) & 1u;
             }
             __syncwarp();
         }
     }
     s_size[wid][lane] = sz_lo;
     s_size[wid][lane + 32] = sz_hi;
-    s_dig[wid][lane] = dg_lo;
-    s_dig[wid][lane + 32] = dg_hi;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) el += __shfl_xor_sync(kFull, el, d);
     if (lane == 0) s_el[wid] = el;
@@ -101,18 +95,59 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     if (threadIdx.x < 64) {
         const int c = threadIdx.x;
         uint32_t S = 0;
-        unsigned long long D = 0;
-        for (int q = 0; q < kW; ++q) { S += s_size[q][c]; D += s_dig[q][c]; }
+        for (int q = 0; q < kW; ++q) S += s_size[q][c];
         const uint64_t li = 64ull * blk + c;  // local sample index
-        if (li < nlocal) {
-            if (S) atomicAdd(&sizes[li], S);
-            if (D) atomicAdd(&digests[li], D);
-        }
+        if (li < nlocal && S) atomicAdd(&sizes[li], S);
     }
     if (threadIdx.x == 0) {
         unsigned long long E = 0;
         for (int q = 0; q < kW; ++q) E += s_el[q];
         if (E) atomicAdd(elog_total, E);
+    }
+}
+
+// Per-sample digests, computed on demand from the store (verification
+// checksums, not part of the method): block (r, g) accumulates colour sums of splitmix64(v)
+// over vertices [r*chunk, (r+1)*chunk) of local block g.
+__global__ void __launch_bounds__(kFinThreads) k_digests(const uint64_t* __restrict__ store, uint32_t n,
+                                                         uint64_t chunk, uint64_t nlocal,
+                                                         unsigned long long* __restrict__ digests) {
+    constexpr int kW = kFinThreads / 32;
+    __shared__ unsigned long long s_mask[kW][32];
+    __shared__ unsigned long long s_mix[kW][32];
+    __shared__ unsigned long long s_dig[kW][64];
+    const uint64_t blk = blockIdx.y;
+    const uint64_t* V = store + (size_t)blk * n;
+    const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
+    const uint64_t v_end = umin64(v_begin + chunk, n);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long dg_lo = 0, dg_hi = 0;
+    for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
+        const uint64_t v = base + lane;
+        const uint64_t m = v < v_end ? V[v] : 0ull;
+        uint32_t b = __ballot_sync(kFull, m != 0);
+        if (!b) continue;
+        s_mask[wid][lane] = m;
+        s_mix[wid][lane] = digest_mix(v);
+        __syncwarp();
+        while (b) {
+            const int j = __ffs(b) - 1;
+            b &= b - 1;
+            const unsigned long long mj = s_mask[wid][j], xj = s_mix[wid][j];
+            if ((mj >> lane) & 1ull) dg_lo += xj;
+            if ((mj >> (lane + 32)) & 1ull) dg_hi += xj;
+        }
+        __syncwarp();
+    }
+    s_dig[wid][lane] = dg_lo;
+    s_dig[wid][lane + 32] = dg_hi;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int c = threadIdx.x;
+        unsigned long long D = 0;
+        for (int q = 0; q < kW; ++q) D += s_dig[q][c];
+        const uint64_t li = 64ull * blk + c;
+        if (li < nlocal && D) atomicAdd(&digests[li], D);
     }
 }
 
@@ -184,12 +219,30 @@ static dim3 finalize_grid(uint32_t n, uint32_t slots_max, uint64_t* chunk_out) {
     return dim3((unsigned)ranges, slots_max);
 }
 
+void compute_digests(const Samples& S, cudaStream_t st) {
+    const uint64_t nlocal = S.s1 - S.s0;
+    BPT_CUDA(cudaMemsetAsync(S.digests.p, 0, nlocal * 8, st));
+    uint64_t ranges = (uint64_t)num_sms() * 4 / umax64(S.blocks, 1);
+    if (ranges < 1) ranges = 1;
+    uint64_t chunk = (S.n + ranges - 1) / ranges;
+    chunk = (chunk + 255) / 256 * 256;
+    ranges = (S.n + chunk - 1) / chunk;
+    for (uint64_t b0 = 0; b0 < S.blocks; b0 += 65535) {
+        const uint64_t nb = umin64(65535, S.blocks - b0);
+        k_digests<<<dim3((unsigned)ranges, (unsigned)nb), kFinThreads, 0, st>>>(
+            S.store.as<uint64_t>() + (size_t)b0 * S.n, S.n, chunk, nlocal - 64 * b0,
+            S.digests.as<unsigned long long>() + 64 * b0);
+        count_launch();
+    }
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_digests");
+}
+
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
-                                             S.sizes.as<uint32_t>(), S.digests.as<unsigned long long>(), d_elog,
+                                             S.sizes.as<uint32_t>(), d_elog,
                                              S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
@@ -204,10 +257,9 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     uint32_t n = S.n;
     uint64_t nlocal = S.s1 - S.s0;
     uint32_t* sizes = S.sizes.as<uint32_t>();
-    unsigned long long* digests = S.digests.as<unsigned long long>();
     uint32_t* count0 = S.count0.as<uint32_t>();
     int single = slots_max == 1 ? 1 : 0;
-    void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &digests, &d_elog,
+    void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog,
                         &count0, &single};
     cudaKernelNodeParams p{};
     p.func = (void*)k_finalize;
