@@ -432,17 +432,17 @@ __device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, ui
 // per-lane predication is needed on the loads.
 template <bool kWhole, bool kC64>
 __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane,
-                                               uint32_t le_mask, uint64_t unit, uint64_t t0, uint32_t rem,
+                                               uint32_t le_mask, uint32_t unit, uint32_t rem,
                                                uint32_t jc0, uint64_t gblk0, unsigned long long& coins,
                                                unsigned long long& atoms) {
-    const uint32_t t0l = (uint32_t)t0;
+    const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
     // ---- entry of every item: jc0 contains item 0; the compaction marked every entry start in
     //      the unit's 128-bit mask (the unit's own mask is cleared here for the next level)
     uint32_t mw[kWinIC];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[unit * kWinIC + w];
+    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[(size_t)unit * kWinIC + w];
     __syncwarp();
-    if (lane < kWinIC) a.umask[unit * kWinIC + lane] = 0;
+    if (lane < kWinIC) a.umask[(size_t)unit * kWinIC + lane] = 0;
     mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
     uint32_t jl[kWinIC];
     uint32_t before = jc0;
@@ -513,9 +513,13 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
                         if (W.excl[o + step] <= k) o += step;
                     uint32_t r = k - W.excl[o];
                     const uint32_t cmo = W.cum[o];
-                    const uint32_t p0 = cmo & 0xffu, p1 = (cmo >> 8) & 0xffu, p2 = cmo >> 16;
-                    const uint32_t w = (r >= p0) + (r >= p1) + (r >= p2);
-                    r -= w == 0 ? 0u : (w == 1 ? p0 : (w == 2 ? p1 : p2));
+                    uint32_t w = 0, base = 0;  // window of the task: last window whose prefix <= r
+#pragma unroll
+                    for (int q = 0; q < kWinIC - 1; ++q) {
+                        const uint32_t pq = (cmo >> (8 * q)) & 0xffu;
+                        if (r >= pq) { w = q + 1; base = pq; }
+                    }
+                    r -= base;
                     coin_task(a, W, o, w, nth_set_bit64(W.live[w][o], r));
                 }
             }
@@ -596,17 +600,18 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     if (lane == 0) W.ecount = 0;
     __syncwarp();
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
-    const uint64_t nunits = (total + kUnitIC - 1) / kUnitIC;
-    const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+    // 32-bit unit indices: total < 2^36 work items, so units < 2^30
+    const uint32_t nunits = (uint32_t)((total + kUnitIC - 1) / kUnitIC);
+    const uint32_t nfull = (uint32_t)(total / kUnitIC);
+    const uint32_t nwarps = gridDim.x * kWarps;
     unsigned long long coins = 0, atoms = 0;
-    for (uint64_t unit = (uint64_t)blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
-        const uint64_t t0 = unit * kUnitIC;
+    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = tstart[unit];
-        if (t0 + kUnitIC <= total)
-            expand_unit_ic<true, kC64>(a, Ln, W, lane, le_mask, unit, t0, kUnitIC, jc0, gblk0, coins, atoms);
+        if (unit < nfull)
+            expand_unit_ic<true, kC64>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms);
         else
-            expand_unit_ic<false, kC64>(a, Ln, W, lane, le_mask, unit, t0, (uint32_t)(total - t0), jc0, gblk0, coins,
-                                        atoms);
+            expand_unit_ic<false, kC64>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
+                                        jc0, gblk0, coins, atoms);
     }
     warp_flush(a, Ln, W, lane);
     unsigned long long ct = block_sum_ull(coins, red);
