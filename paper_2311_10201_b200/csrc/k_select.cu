@@ -9,6 +9,10 @@
 //           (3) count[v] -= sum over listed g of popcount(V_g[v] & new_g)
 // Each sample leaves `count` exactly once, so the decrements over all rounds cost at most one
 // pass over the store plus the few blocks touched by later rounds.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace bpt {
@@ -95,10 +99,28 @@ __global__ void k_decrement_lists(const uint32_t* __restrict__ nlist, const uint
     }
 }
 
-}  // namespace
+// One pass over the store: every set bit (block g, vertex v, colour c) appends v to the list of
+// sample 64 g + c through that sample's cursor. Lists come out unsorted -- the selection's
+// decrement only needs the member sets (bpt_rrr_extract has its own ordered path).
+__global__ void k_lists_scatter(const uint64_t* __restrict__ store, uint32_t n, uint64_t blocks, uint64_t nlocal,
+                                const uint64_t* __restrict__ off, uint32_t* __restrict__ cursor,
+                                uint32_t* __restrict__ members) {
+    for (uint64_t g = blockIdx.y; g < blocks; g += gridDim.y) {
+        const uint64_t* V = store + g * n;
+        for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+            uint64_t m = V[v];
+            while (m) {
+                const uint32_t c = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const uint64_t s = 64 * g + c;
+                if (s >= nlocal) break;
+                members[off[s] + atomicAdd(&cursor[s], 1u)] = v;
+            }
+        }
+    }
+}
 
-void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
-                   cudaStream_t st);
+}  // namespace
 
 // Member lists of all local samples, if they are small enough to keep (sparse stores); cached.
 static bool build_lists(const Samples& S, cudaStream_t st) {
@@ -118,7 +140,17 @@ static bool build_lists(const Samples& S, cudaStream_t st) {
     M.list_off.alloc((nlocal + 1) * 8);
     M.list_mem.alloc(off[nlocal] * 4 + 4);
     BPT_CUDA(cudaMemcpyAsync(M.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
-    if (off[nlocal]) extract_range(S, S.s0, nlocal, off.data(), M.list_mem.as<uint32_t>(), st);
+    if (off[nlocal]) {
+        DevBuf cursor(nlocal * 4);
+        BPT_CUDA(cudaMemsetAsync(cursor.p, 0, nlocal * 4, st));
+        const dim3 grid((unsigned)umin64((S.n + 255) / 256, 64), (unsigned)umin64(S.blocks, (uint64_t)num_sms() * 4));
+        k_lists_scatter<<<grid, 256, 0, st>>>(S.store.as<uint64_t>(), S.n, S.blocks, nlocal,
+                                                       M.list_off.as<uint64_t>(), cursor.as<uint32_t>(),
+                                                       M.list_mem.as<uint32_t>());
+        count_launch();
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_lists_scatter");
+        BPT_CUDA(cudaStreamSynchronize(st));
+    }
     BPT_CUDA(cudaStreamSynchronize(st));
     return M.lists_ok = true;
 }
@@ -138,7 +170,10 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     const unsigned ggrid = (unsigned)umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4);
     const unsigned dgrid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
     const uint64_t shard_len = (uint64_t)S.n_pad / world;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     const bool lists = build_lists(S, st);
+    const auto t1 = clk::now();
     for (uint32_t r = 0; r < k; ++r) {
         unsigned long long* key = keys.as<unsigned long long>() + r;
         if (world > 1) {
@@ -168,6 +203,11 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     std::vector<unsigned long long> hk(k);
     BPT_CUDA(cudaMemcpyAsync(hk.data(), keys.p, (uint64_t)k * 8, cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
+    if (getenv("BPT_TRACE")) {
+        auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+        fprintf(stderr, "[bpt] select k=%u: lists %s %.2f ms, rounds %.2f ms (world %d, blocks %llu)\n", k,
+                lists ? "on" : "off", ms(t0, t1), ms(t1, clk::now()), world, (unsigned long long)blocks);
+    }
     for (uint32_t r = 0; r < k; ++r) {
         h_seeds[r] = ~(uint32_t)hk[r];
         h_gains[r] = hk[r] >> 32;
