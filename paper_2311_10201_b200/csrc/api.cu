@@ -56,6 +56,12 @@ int current_device() {
 }
 }  // namespace
 
+size_t cached_bytes() {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    return P.cached[current_device()];
+}
+
 void release_cached_blocks() {
     Pool& P = pool();
     std::lock_guard<std::mutex> lk(P.mu);
@@ -214,7 +220,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
 
     // ---- batch plan
-    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 512);
+    // IC: one block per batch keeps the working masks L2-resident; LT: as many as fit (fewer,
+    // longer levels: LT frontiers are thin, per-level overhead dominates)
+    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 2048);
     uint64_t slots = umin64(umax64(want, 1), S.blocks);
     const uint32_t tile = expand_unit(S.model);
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
@@ -227,6 +235,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     };
     size_t free_b = 0, total_b = 0;
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    free_b += cached_bytes();  // the pool's cached blocks are released if an allocation needs them
     uint64_t raw_cap = 0, q_cap = 0, ts_cap = 0;
     while (slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
     while (slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices

@@ -21,8 +21,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 4;
-constexpr uint32_t kTile = kThreads * kItems;   // work items (edges / LT tasks) per tile
+#ifndef BPT_LT_ITEMS
+#define BPT_LT_ITEMS 1
+#endif
+constexpr int kItems = BPT_LT_ITEMS;    // LT tasks per thread per tile (1: thin LT levels spread over all blocks)
+constexpr uint32_t kTile = kThreads * kItems;   // LT tasks per tile
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint64_t raw_pack(uint32_t v, uint32_t slot, uint32_t slice) {
@@ -681,14 +684,34 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
                 const uint32_t s = (uint32_t)(64ull * (gblk0 + slot)) + bit;
                 const uint32_t r = philox2x32_10(v, s, a.k_lt).x >> 1;
                 ++coins;
-                uint32_t lo2 = a.roff[v], hi2 = a.roff[v + 1];  // first j with cum[j] > r
-                const uint32_t end = hi2;
-                while (lo2 < hi2) {
-                    const uint32_t mid = (lo2 + hi2) >> 1;
-                    if (__ldg(&a.rec[mid]).y > r) hi2 = mid; else lo2 = mid + 1;
+                // first j of row v with cum[j] > r (none if r >= the row sum): interpolation
+                // search (cum grows ~linearly along a row: ~2-4 dependent probes instead of
+                // log2(deg)), bisection after 4 probes
+                uint32_t lo2 = a.roff[v], hi2 = a.roff[v + 1];
+                bool found = false;
+                uint32_t u = 0;
+                if (lo2 < hi2) {
+                    uint2 hit = __ldg(&a.rec[hi2 - 1]);  // record at hi2 - 1: {src, row sum}
+                    if (r < hit.y) {
+                        // answer in [lo2, hi2): cum[lo2 - 1] = clo <= r < chi = cum[hi2 - 1]
+                        uint32_t clo = 0, chi = hit.y;
+                        for (int step = 0; hi2 - lo2 > 1; ++step) {
+                            uint32_t g;
+                            if (step < 4) {
+                                g = lo2 + (uint32_t)((uint64_t)(r - clo) * (hi2 - lo2) / (uint64_t)(chi - clo));
+                                g = min(g, hi2 - 2);
+                            } else {
+                                g = (lo2 + hi2 - 1) >> 1;
+                            }
+                            const uint2 x = __ldg(&a.rec[g]);
+                            if (x.y > r) { hi2 = g + 1; chi = x.y; hit = x; }
+                            else { lo2 = g + 1; clo = x.y; }
+                        }
+                        found = true;
+                        u = hit.x;
+                    }
                 }
-                if (lo2 < end) {
-                    const uint32_t u = __ldg(&a.rec[lo2]).x;
+                if (found) {
                     const uint64_t b = 1ull << bit;
                     const uint64_t Vu = a.VN[(size_t)slot * a.n + u].x;
                     if (!(Vu & b)) {
