@@ -392,8 +392,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     // %globaltimer span of every launch (graph mode)
     I.ms_expand = profile ? ev_ms : cf.expand_ns * 1e-6;
     I.expand_launches = profile ? ev_launches : cf.levels_total;
-    // kernels executed: per batch init + finalize + next_batch, per level compact + expand
-    if (!profile) g_launches += 3 * nbatches + 2 * cf.levels_total;
+    // kernels executed: per batch init + finalize + next_batch, per level compact + expand (LT: one
+    // cooperative level-loop launch per batch)
+    if (!profile) g_launches += level_loop_persistent(a) ? 4 * nbatches : 3 * nbatches + 2 * cf.levels_total;
     I.kernel_launches = g_launches - launches0;
     I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     if (getenv("BPT_TRACE")) {

@@ -145,8 +145,11 @@ struct Ctl {
     uint32_t levels_max;
     uint32_t stats_overflow;
     uint32_t blocks_done;    // expansion blocks finished (the last one advances the level)
+    uint32_t bar_count;      // grid barrier of the cooperative LT level loop: arrivals ...
+    uint32_t bar_gen;        // ... and generation
     uint32_t pad_;
 };
+static_assert(sizeof(Ctl) % 16 == 0, "Ctl is read with 16-B vector loads");
 constexpr int kMaxLevels = 8192;
 
 struct BatchArgs {
@@ -189,6 +192,7 @@ struct StoreHook {  // adds the per-batch finalise nodes after the level loop
     const uint32_t* roff;
     unsigned long long* d_elog;
 };
+bool level_loop_persistent(const BatchArgs& a);
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);
 // k_select.cu
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st);

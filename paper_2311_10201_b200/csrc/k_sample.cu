@@ -11,10 +11,12 @@
 //   tstart[]   u32   first entry of each expansion tile (written by the compaction)
 // Level L:  compact(L): raw(L) -> V |= N, q/qoff/tstart      (Listing 1 lines 7-8)
 //           expand(L):  q -> N atomicOr, raw(L+1)             (Listing 1 lines 9-15)
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
+
 
 namespace bpt {
 namespace {
@@ -134,12 +136,15 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
 constexpr int kCompItems = 4;
 constexpr uint32_t kCompTile = kThreads * kCompItems;
 
-__global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
-                                                      uint64_t tstart_cap, uint32_t unit) {
-    if (!a.ctl->cont) return;
+// kCoh: loads of data written earlier in the same launch bypass L1 (the persistent LT level
+// loop below runs several levels per launch; separate launches see fresh L1s anyway)
+#define LDX(ptr) (kCoh ? __ldcg(ptr) : *(ptr))
+template <bool kCoh>
+__device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __restrict__ tstart, uint64_t tstart_cap,
+                                             uint32_t unit) {
     if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
-    LevelRec* L = &a.lv[a.ctl->level];
-    const uint64_t nraw = umin64(L->raw, a.raw_cap);
+    LevelRec* L = &a.lv[LDX(&a.ctl->level)];
+    const uint64_t nraw = umin64(LDX(&L->raw), a.raw_cap);
     __shared__ unsigned long long wsum[kWarps];
     __shared__ uint32_t wcnt[kWarps];
     __shared__ unsigned long long blk_base;
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* 
 #pragma unroll
         for (int it = 0; it < kCompItems; ++it) {
             const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
-            r[it] = i < nraw ? a.raw[i] : ~0ull;
+            r[it] = i < nraw ? LDX(&a.raw[i]) : ~0ull;
         }
         uint64_t mask[kCompItems];
         uint32_t rs[kCompItems], re[kCompItems];
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* 
                 const uint32_t slot = (uint32_t)(r[it] >> 32) & ((1u << 26) - 1u);
                 ulonglong2* p = &a.VN[(size_t)slot * a.n + v];
                 if (a.colors == 64) {
-                    const ulonglong2 x = *p;
+                    const ulonglong2 x = LDX(p);
                     mask[it] = x.y;
                     *p = make_ulonglong2(x.x | x.y, 0ull);
                 } else {
@@ -278,6 +283,13 @@ __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* 
     if (threadIdx.x == 0) atomicMax(&a.ctl->c_end, global_ns());
 }
 
+
+__global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                      uint64_t tstart_cap, uint32_t unit) {
+    if (!a.ctl->cont) return;
+    compact_body<false>(a, tstart, tstart_cap, unit);
+}
+
 // ------------------------------------------------------------------------ A3: expansion
 struct SmemTile {  // LT expansion tile staging
     uint32_t rel[kTile + 1];   // max(qoff - t0, 0) per entry of the tile
@@ -306,37 +318,43 @@ __device__ __forceinline__ void enqueue_warp(const BatchArgs& a, LevelRec* Lnext
 
 __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* c = a.ctl;
-    // counters were updated by other blocks' atomics: read them from L2 (__ldcg), not L1
-    const uint32_t Lv = __ldcg(&c->level);
-    LevelRec R;
-    R.packed = __ldcg(&a.lv[Lv].packed);
-    R.vc = __ldcg(&a.lv[Lv].vc);
-    R.coins = __ldcg(&a.lv[Lv].coins);
-    R.atomics = __ldcg(&a.lv[Lv].atomics);
-    R.raw = __ldcg(&a.lv[Lv].raw);
-    R.overflow = __ldcg(&a.lv[Lv].overflow);
-    R.pad = 0;
-    const uint32_t next_raw = __ldcg(&a.lv[Lv + 1].raw);
-    const uint32_t next_ovf = __ldcg(&a.lv[Lv + 1].overflow);
-    c->work += R.packed & kEdgeMask;
-    c->entries += R.packed >> kPackShift;
-    c->vc += R.vc;
-    c->coins += R.coins;
-    c->atomics += R.atomics;
-    const unsigned long long ts = __ldcg(&c->t_start), te = __ldcg(&c->t_end);
-    if (ts != ~0ull && te > ts) c->expand_ns += te - ts;
-    c->t_start = ~0ull;
+    // The counters were updated by other blocks' atomics (and, in the cooperative LT loop, by
+    // other blocks' earlier advances): read them from L2 (.cg), all in one batch of vector
+    // loads -- this runs on the critical path of every level.
+    Ctl C;
     {
-        const unsigned long long cs = __ldcg(&c->c_start), ce = __ldcg(&c->c_end);
-        if (cs != ~0ull && ce > cs) c->compact_ns += ce - cs;
-        c->c_start = ~0ull;
-        c->c_end = 0;
+        const uint4* src = reinterpret_cast<const uint4*>(c);
+        uint4* dst = reinterpret_cast<uint4*>(&C);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(Ctl) / 16); ++i) dst[i] = __ldcg(src + i);
     }
+    const uint32_t Lv = C.level;
+    LevelRec R;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&a.lv[Lv]);
+        uint4* dst = reinterpret_cast<uint4*>(&R);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(LevelRec) / 16); ++i) dst[i] = __ldcg(src + i);
+    }
+    const uint2 nx = __ldcg(reinterpret_cast<const uint2*>(&a.lv[Lv + 1].raw));  // {raw, overflow}
+    R.pad = 0;
+    const uint32_t next_raw = nx.x, next_ovf = nx.y;
+    c->work = C.work + (R.packed & kEdgeMask);
+    c->entries = C.entries + (R.packed >> kPackShift);
+    c->vc = C.vc + R.vc;
+    c->coins = C.coins + R.coins;
+    c->atomics = C.atomics + R.atomics;
+    if (C.t_start != ~0ull && C.t_end > C.t_start) c->expand_ns = C.expand_ns + (C.t_end - C.t_start);
+    if (C.c_start != ~0ull && C.c_end > C.c_start) c->compact_ns = C.compact_ns + (C.c_end - C.c_start);
+    c->t_start = ~0ull;
     c->t_end = 0;
-    if (c->stats_used < a.stats_cap) {
+    c->c_start = ~0ull;
+    c->c_end = 0;
+    if (C.stats_used < a.stats_cap) {
         LevelRec row = R;
-        row.pad = ((unsigned long long)c->batch << 32) | Lv;
-        a.stats[c->stats_used++] = row;
+        row.pad = ((unsigned long long)C.batch << 32) | Lv;
+        a.stats[C.stats_used] = row;
+        c->stats_used = C.stats_used + 1;
     } else {
         c->stats_overflow = 1;
     }
@@ -347,8 +365,8 @@ __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphCondi
     c->level = Lv + 1;
     if (!cont) {
         c->cont = 0;
-        c->levels_total += Lv + 1;
-        if (Lv + 1 > c->levels_max) c->levels_max = Lv + 1;
+        c->levels_total = C.levels_total + Lv + 1;
+        if (Lv + 1 > C.levels_max) c->levels_max = Lv + 1;
     }
     if (use_cond) cudaGraphSetConditional(h_level, cont ? 1u : 0u);
 }
@@ -628,19 +646,19 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
 // N[u] |= bit c (fusing) and the first setter enqueues u.
-__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart,
-                                                      cudaGraphConditionalHandle h_level, int use_cond) {
+template <bool kCoh>
+__device__ __forceinline__ void expand_lt_body(const BatchArgs& a, const uint32_t* __restrict__ tstart,
+                                               cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
-    if (!ctl->cont) return;
-    const uint32_t level = ctl->level;
-    const uint64_t gblk0 = ctl->gblk0;
+    const uint32_t level = LDX(&ctl->level);
+    const uint64_t gblk0 = LDX(&ctl->gblk0);
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
     if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
-    const unsigned long long packed = L->packed;
+    const unsigned long long packed = LDX(&L->packed);
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || L->overflow) {
+    if (nq == 0 || LDX(&L->overflow)) {
         finish_expand(a, h_level, use_cond);
         return;
     }
@@ -650,14 +668,14 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
     unsigned long long coins = 0, atoms = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t t0 = tile * kTile;
-        const uint32_t j0 = tstart[tile];
-        const uint64_t jend = tile + 1 < ntiles ? (uint64_t)tstart[tile + 1] + 1 : nq;
+        const uint32_t j0 = LDX(&tstart[tile]);
+        const uint64_t jend = tile + 1 < ntiles ? (uint64_t)LDX(&tstart[tile + 1]) + 1 : nq;
         const uint32_t cnt = (uint32_t)umin64(jend - j0, (uint64_t)kTile + 1);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < cnt; k += kThreads) {
             const uint64_t j = j0 + k;
-            const uint64_t off = a.qoff[j];
-            const uint4 ent = a.q[j];
+            const uint64_t off = LDX(&a.qoff[j]);
+            const uint4 ent = LDX(&a.q[j]);
             sm.rel[k] = off <= t0 ? 0u : (uint32_t)(off - t0);
             sm.aux[k] = (uint32_t)(t0 > off ? t0 - off : 0);  // tasks of entry k before the tile
             sm.v[k] = ent.x;
@@ -713,7 +731,7 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
                 }
                 if (found) {
                     const uint64_t b = 1ull << bit;
-                    const uint64_t Vu = a.VN[(size_t)slot * a.n + u].x;
+                    const uint64_t Vu = LDX(&a.VN[(size_t)slot * a.n + u].x);
                     if (!(Vu & b)) {
                         ++atoms;
                         const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + u].y, b);
@@ -731,6 +749,45 @@ __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint3
     unsigned long long at = block_sum_ull(atoms, sm.red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
     finish_expand(a, h_level, use_cond);
+}
+
+__global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                      cudaGraphConditionalHandle h_level, int use_cond) {
+    if (!a.ctl->cont) return;
+    expand_lt_body<false>(a, tstart, h_level, use_cond);
+}
+
+// LT levels are thin (a few thousand walks) and many (~700 per batch on C3): one cooperative
+// launch runs the whole level loop of a batch, compact(L) -> grid barrier -> expand(L) (its
+// last block advances the level) -> grid barrier, instead of two launches per level.
+// Grid barrier (all blocks co-resident: cooperative launch): one arrival atomic per block, the
+// last arrival bumps the generation the others spin on.
+__device__ __forceinline__ void grid_barrier(Ctl* c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t gen = *(volatile uint32_t*)&c->bar_gen;
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+            c->bar_count = 0;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            while (*(volatile uint32_t*)&c->bar_gen == gen) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) k_levels_lt(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                      uint64_t tstart_cap) {
+    while (__ldcg(&a.ctl->cont)) {
+        compact_body<true>(a, tstart, tstart_cap, kTile);
+        grid_barrier(a.ctl);
+        expand_lt_body<true>(a, tstart, (cudaGraphConditionalHandle)0, 0);
+        grid_barrier(a.ctl);
+    }
 }
 
 // ------------------------------------------------------------------------ level / batch control
@@ -761,6 +818,7 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 
 int g_expand_grid = 0;
 int g_expand_grid_lt = 0;
+int g_levels_grid_lt = 0;
 int g_compact_grid = 0;
 
 }  // namespace
@@ -781,11 +839,24 @@ int expand_grid() {
         int per_sm_lt = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_lt, k_expand_lt, kThreads, sizeof(SmemTile)));
         g_expand_grid_lt = num_sms() * (per_sm_lt > 0 ? per_sm_lt : 1);
+        int per_sm_pl = 0;  // the cooperative level loop must be co-resident
+        BPT_CUDA(cudaFuncSetAttribute(k_levels_lt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pl, k_levels_lt, kThreads, sizeof(SmemTile)));
+        // few blocks: the levels are thin, and a grid barrier costs ~ the number of blocks
+        const char* gs = getenv("BPT_LT_BLOCKS_PER_SM");
+        const int want = gs ? atoi(gs) : 1;
+        g_levels_grid_lt = num_sms() * std::max(1, std::min(want, per_sm_pl > 0 ? per_sm_pl : 1));
         int per_sm_c = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact, kThreads, 0));
         g_compact_grid = num_sms() * (per_sm_c > 0 ? per_sm_c : 1);
     }
     return g_expand_grid;
+}
+
+// LT batches run their level loop as one cooperative launch (BPT_LT_PERSIST=0: per-level launches)
+bool level_loop_persistent(const BatchArgs& a) {
+    const char* pl = getenv("BPT_LT_PERSIST");
+    return a.model != BPT_IC && !(pl && pl[0] == '0');
 }
 
 static unsigned init_grid(const BatchArgs& a) { return (unsigned)(((uint64_t)a.slots_max * 64 + 255) / 256); }
@@ -840,7 +911,9 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     cudaGraphNode_t n_batch;
     BPT_CUDA(cudaGraphAddNode(&n_batch, root, nullptr, 0, &cb));
     cudaGraph_t body = cb.conditional.phGraph_out[0];
-    BPT_CUDA(cudaGraphConditionalHandleCreate(&h_level, body, 1, cudaGraphCondAssignDefault));
+    const bool lt_persist = level_loop_persistent(a);
+    h_level = 0;
+    if (!lt_persist) BPT_CUDA(cudaGraphConditionalHandleCreate(&h_level, body, 1, cudaGraphCondAssignDefault));
 
     BatchArgs args = a;
     int one = 1;
@@ -856,9 +929,27 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         BPT_CUDA(cudaGraphAddKernelNode(&node, g, dep, dep ? 1 : 0, &p));
         return node;
     };
+    int zero = 0;
     // batch body: init
-    void* init_args[] = {&args, &h_level, &one};
+    void* init_args[] = {&args, &h_level, lt_persist ? &zero : &one};
     cudaGraphNode_t n_init = add_kernel(body, nullptr, (void*)k_init, dim3(init_grid(a)), dim3(256), 0, init_args);
+    if (lt_persist) {
+        // LT: the whole level loop as one cooperative launch (grid barriers between phases)
+        void* lv_args[] = {&args, &tstart, &tstart_cap};
+        cudaGraphNode_t n_lv = add_kernel(body, &n_init, (void*)k_levels_lt, dim3(g_levels_grid_lt), dim3(kThreads),
+                                          sizeof(SmemTile), lv_args);
+        cudaLaunchAttributeValue coop{};
+        coop.cooperative = 1;
+        BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
+        cudaGraphNode_t n_store;
+        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);
+        void* nb_args[] = {&args, &h_batch, &one};
+        add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
+        cudaGraphExec_t exec;
+        BPT_CUDA(cudaGraphInstantiate(&exec, root, 0));
+        BPT_CUDA(cudaGraphDestroy(root));
+        return exec;
+    }
     // level loop
     cudaGraphNodeParams cl{};
     cl.type = cudaGraphNodeTypeConditional;
