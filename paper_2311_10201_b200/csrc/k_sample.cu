@@ -78,6 +78,14 @@ __device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p) {
     return r;
 }
 
+// coherent (L2) variant for loops that run several levels in one launch
+__device__ __forceinline__ ulonglong2 ld_keep_cg(const ulonglong2* p) {
+    ulonglong2 r;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(policy_evict_last()));
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -451,7 +459,7 @@ __device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, ui
 
 // One 128-item unit. kWhole: all 128 items valid (every unit but the last of a level), so no
 // per-lane predication is needed on the loads.
-template <bool kWhole, bool kC64>
+template <bool kWhole, bool kC64, bool kCoh>
 __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane,
                                                uint32_t le_mask, uint32_t unit, uint32_t rem,
                                                uint32_t jc0, uint64_t gblk0, unsigned long long& coins,
@@ -461,7 +469,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     //      the unit's 128-bit mask (the unit's own mask is cleared here for the next level)
     uint32_t mw[kWinIC];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[(size_t)unit * kWinIC + w];
+    for (int w = 0; w < kWinIC; ++w) mw[w] = LDX(&a.umask[(size_t)unit * kWinIC + w]);
     __syncwarp();
     if (lane < kWinIC) a.umask[(size_t)unit * kWinIC + lane] = 0;
     mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
@@ -479,7 +487,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     uint32_t vidx[kWinIC];
     uint64_t live[kWinIC];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) ent[w] = a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0];
+    for (int w = 0; w < kWinIC; ++w) ent[w] = LDX(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
         // an invalid item re-reads item 0 of the unit, which lies in entry jc0
@@ -491,7 +499,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         // {V[u], N[u]}: colours visited, or already merged into u this level by another edge
         // (a possibly stale N only skips fewer coins; the merged result is the same)
         vidx[w] = ent[w].y * a.n + rc[w].x;
-        const ulonglong2 vn = ld_keep(&a.VN[vidx[w]]);
+        const ulonglong2 vn = kCoh ? ld_keep_cg(&a.VN[vidx[w]]) : ld_keep(&a.VN[vidx[w]]);
         live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
         if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
     }
@@ -596,20 +604,19 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
 #ifndef BPT_EXPAND_MINB
 #define BPT_EXPAND_MINB 5
 #endif
-template <bool kC64>
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
-                                                              cudaGraphConditionalHandle h_level, int use_cond) {
+template <bool kC64, bool kCoh>
+__device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_t* __restrict__ tstart,
+                                               cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
-    if (!ctl->cont) return;
-    const uint32_t level = ctl->level;
-    const uint64_t gblk0 = ctl->gblk0;
+    const uint32_t level = LDX(&ctl->level);
+    const uint64_t gblk0 = LDX(&ctl->gblk0);
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
     if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
-    const unsigned long long packed = L->packed;
+    const unsigned long long packed = LDX(&L->packed);
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || L->overflow) {
+    if (nq == 0 || LDX(&L->overflow)) {
         finish_expand(a, h_level, use_cond);
         return;
     }
@@ -627,11 +634,11 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     const uint32_t nwarps = gridDim.x * kWarps;
     unsigned long long coins = 0, atoms = 0;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
-        const uint32_t jc0 = tstart[unit];
+        const uint32_t jc0 = LDX(&tstart[unit]);
         if (unit < nfull)
-            expand_unit_ic<true, kC64>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms);
+            expand_unit_ic<true, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms);
         else
-            expand_unit_ic<false, kC64>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
+            expand_unit_ic<false, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
                                         jc0, gblk0, coins, atoms);
     }
     warp_flush(a, Ln, W, lane);
@@ -640,6 +647,13 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
     finish_expand(a, h_level, use_cond);
+}
+
+template <bool kC64>
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                              cudaGraphConditionalHandle h_level, int use_cond) {
+    if (!a.ctl->cont) return;
+    expand_ic_body<kC64, false>(a, tstart, h_level, use_cond);
 }
 
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
@@ -780,6 +794,18 @@ __device__ __forceinline__ void grid_barrier(Ctl* c) {
     __syncthreads();
 }
 
+// IC: the same cooperative level loop (BPT_IC_PERSIST=1); same-launch data is read through L2.
+template <bool kC64>
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_levels_ic(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                                       uint64_t tstart_cap) {
+    while (__ldcg(&a.ctl->cont)) {
+        compact_body<true>(a, tstart, tstart_cap, kUnitIC);
+        grid_barrier(a.ctl);
+        expand_ic_body<kC64, true>(a, tstart, (cudaGraphConditionalHandle)0, 0);
+        grid_barrier(a.ctl);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_levels_lt(BatchArgs a, uint32_t* __restrict__ tstart,
                                                       uint64_t tstart_cap) {
     while (__ldcg(&a.ctl->cont)) {
@@ -819,6 +845,7 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 int g_expand_grid = 0;
 int g_expand_grid_lt = 0;
 int g_levels_grid_lt = 0;
+int g_levels_grid_ic = 0;
 int g_compact_grid = 0;
 
 }  // namespace
@@ -846,6 +873,13 @@ int expand_grid() {
         const char* gs = getenv("BPT_LT_BLOCKS_PER_SM");
         const int want = gs ? atoi(gs) : 1;
         g_levels_grid_lt = num_sms() * std::max(1, std::min(want, per_sm_pl > 0 ? per_sm_pl : 1));
+        int per_sm_pi = 0;
+        for (void* f : {(void*)k_levels_ic<true>, (void*)k_levels_ic<false>})
+            BPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(WarpScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pi, k_levels_ic<true>, kThreads,
+                                                               sizeof(WarpScratch) * kWarps));
+        g_levels_grid_ic = num_sms() * (per_sm_pi > 0 ? per_sm_pi : 1);
         int per_sm_c = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact, kThreads, 0));
         g_compact_grid = num_sms() * (per_sm_c > 0 ? per_sm_c : 1);
@@ -855,8 +889,12 @@ int expand_grid() {
 
 // LT batches run their level loop as one cooperative launch (BPT_LT_PERSIST=0: per-level launches)
 bool level_loop_persistent(const BatchArgs& a) {
+    if (a.model == BPT_IC) {
+        const char* pi = getenv("BPT_IC_PERSIST");
+        return pi && pi[0] == '1';
+    }
     const char* pl = getenv("BPT_LT_PERSIST");
-    return a.model != BPT_IC && !(pl && pl[0] == '0');
+    return !(pl && pl[0] == '0');
 }
 
 static unsigned init_grid(const BatchArgs& a) { return (unsigned)(((uint64_t)a.slots_max * 64 + 255) / 256); }
@@ -934,10 +972,14 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     void* init_args[] = {&args, &h_level, lt_persist ? &zero : &one};
     cudaGraphNode_t n_init = add_kernel(body, nullptr, (void*)k_init, dim3(init_grid(a)), dim3(256), 0, init_args);
     if (lt_persist) {
-        // LT: the whole level loop as one cooperative launch (grid barriers between phases)
+        // the whole level loop as one cooperative launch (grid barriers between phases)
         void* lv_args[] = {&args, &tstart, &tstart_cap};
-        cudaGraphNode_t n_lv = add_kernel(body, &n_init, (void*)k_levels_lt, dim3(g_levels_grid_lt), dim3(kThreads),
-                                          sizeof(SmemTile), lv_args);
+        cudaGraphNode_t n_lv =
+            a.model == BPT_IC
+                ? add_kernel(body, &n_init, a.colors == 64 ? (void*)k_levels_ic<true> : (void*)k_levels_ic<false>,
+                             dim3(g_levels_grid_ic), dim3(kThreads), sizeof(WarpScratch) * kWarps, lv_args)
+                : add_kernel(body, &n_init, (void*)k_levels_lt, dim3(g_levels_grid_lt), dim3(kThreads),
+                             sizeof(SmemTile), lv_args);
         cudaLaunchAttributeValue coop{};
         coop.cooperative = 1;
         BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
