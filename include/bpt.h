@@ -108,8 +108,8 @@ BPT_API void bpt_graph_free(bpt_graph* g);
  *     iff (r >> 1) < thr(e) (readings C-1, C-2). LT: one draw per (s, v) picks <= 1
  *     in-edge (reading C-6).
  *   Result: RRR sets stored in fused form (per 64-sample block, a u64 colour mask per
- *     vertex = Listing 1's visited[]), plus per-sample sizes and digests
- *     (DESIGN.md "Digest"). RRR sets are identical for any colors, batch size and number
+ *     vertex = Listing 1's visited[]), plus per-sample sizes; per-sample digests
+ *      are computed from the store on the first bpt_rrr_digests call. RRR sets are identical for any colors, batch size and number
  *     of ranks (readings C-9, C-14).
  *   colors must divide 64 (1, 2, 4, 8, 16, 32, 64). theta in [1, 2^32).
  *   Multi-rank: every rank calls with identical arguments; rank r samples the 64-sample
@@ -166,7 +166,8 @@ BPT_API bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t
  * A5/A6: per-sample results for global sample ids [first, first+count), which must lie
  * in this rank's range (else EINVAL).
  *   sizes[count] u32 = |RR_s|; digests[count] u64 = sum over v in RR_s of
- *   splitmix64(v) mod 2^64.
+ *   splitmix64(v) mod 2^64 (the first digests call on a handle runs
+ *   one pass over the local store, later calls read the cached values).
  *   bpt_rrr_extract: Listing 1 lines 18-21 -- RRR lists, sorted ascending,
  *   start included (reading C-10). offsets[count+1] u64 (offsets[0] = 0), members
  *   u32[capacity]. If capacity < offsets[count] -> ENOMEM (message gives the size) and
