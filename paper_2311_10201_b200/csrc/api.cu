@@ -223,12 +223,16 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     // IC: one block per batch keeps the working masks L2-resident; LT: as many as fit (fewer,
     // longer levels: LT frontiers are thin, per-level overhead dominates)
     uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 2048);
-    uint64_t slots = umin64(umax64(want, 1), S.blocks);
-    const uint32_t tile = expand_unit(S.model);
+    // wide fusion (IC, 64 colours): kWide blocks share one frontier (k_sample.cu "wide fusion")
+    const char* wide_env = getenv("BPT_WIDE");
+    const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups && wide_env && wide_env[0] == '1';
+    if (wide) want = kWide;
+    uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
+    const uint32_t tile = wide ? kUnitWide : expand_unit(S.model);
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
-        raw_cap = umin64(sl * slices * n, (1ull << 28) - 1);
+        raw_cap = umin64(wide ? n : sl * slices * n, (1ull << 28) - 1);  // wide: one entry per vertex
         q_cap = raw_cap;
-        const uint64_t work = S.model == BPT_IC ? umin64(sl * slices * g.m, kEdgeMask)
+        const uint64_t work = S.model == BPT_IC ? umin64((wide ? 1 : sl * slices) * g.m, kEdgeMask)
                                                 : umin64(sl * 64 * n, kEdgeMask);
         ts_cap = work / tile + 2;
         return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 20;
@@ -237,8 +241,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
     free_b += cached_bytes();  // the pool's cached blocks are released if an allocation needs them
     uint64_t raw_cap = 0, q_cap = 0, ts_cap = 0;
-    while (slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
-    while (slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
+    while (!wide && slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
+    while (!wide && slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
+    if (wide && (uint64_t)kWide * n >= (1ull << 32)) fail(BPT_EINVAL, "wide fusion needs kWide * n < 2^32");
     plan_bytes(slots, raw_cap, q_cap, ts_cap);
 
     const uint64_t nbatches = (S.blocks + slots - 1) / slots;
@@ -248,6 +253,13 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
         elog(8);
     BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
+    DevBuf vflag, qd, qmask;
+    if (wide) {
+        vflag.alloc((uint64_t)n * 4 + 4);
+        qd.alloc(q_cap * 4 + 4);
+        qmask.alloc(q_cap * kWide * 8 + 16);
+        BPT_CUDA(cudaMemsetAsync(vflag.p, 0, vflag.bytes, st));  // the compaction re-zeroes what it reads
+    }
     BPT_CUDA(cudaMemsetAsync(lv.p, 0, lv.bytes, st));  // k_next_batch re-zeroes the levels it used
     BPT_CUDA(cudaMemsetAsync(umask.p, 0, umask.bytes, st));  // the expansion re-zeroes every unit it reads
     BPT_CUDA(cudaMemsetAsync(elog.p, 0, 8, st));
@@ -287,6 +299,10 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.k_ic = stream_key(S.seed, kTagIC);
     a.k_lt = stream_key(S.seed, kTagLT);
     a.k_start = stream_key(S.seed, kTagStart);
+    a.wide = wide ? 1 : 0;
+    a.vflag = wide ? vflag.as<uint32_t>() : nullptr;
+    a.qd = wide ? qd.as<uint32_t>() : nullptr;
+    a.qmask = wide ? qmask.as<unsigned long long>() : nullptr;
 
     const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
     double ev_ms = 0;
@@ -294,7 +310,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     double wait_ms = 0;
     if (!profile) {
         // ---- device-resident loops: one graph launch for the whole sample range
-        StoreHook hook{&S, a.VN, g.roff.as<uint32_t>(), elog.as<unsigned long long>()};
+        StoreHook hook{&S, a.VN, g.roff.as<uint32_t>(), elog.as<unsigned long long>(), wide};
         cudaGraphExec_t exec = build_sampling_graph(a, tstart.as<uint32_t>(), ts_cap, hook);
         cudaError_t e = cudaGraphLaunch(exec, st);
         cudaGraphExecDestroy(exec);  // deferred by the driver until the launch completes
@@ -341,7 +357,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
                 have_prev = true;
                 cur ^= 1;
             }
-            launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>());
+            launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>(),
+                            a.wide != 0);
             launch_next_batch(a, st);
         }
         BPT_CUDA(cudaStreamSynchronize(st));

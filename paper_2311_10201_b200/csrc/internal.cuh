@@ -175,12 +175,22 @@ struct BatchArgs {
     Ctl* ctl;
     uint64_t theta;           // global sample count (bits of samples >= theta stay 0)
     uint32_t k_ic, k_lt, k_start;
+    // wide fusion (IC, 64 colours): the slots_max = kWide blocks of a
+    // batch share one frontier. Working masks vertex-major VN[v * kWide + b]; one frontier entry
+    // per vertex with kWide masks; vflag[v] = v already queued for the next level.
+    int wide;                 // 0: slot-major layout (one entry per (vertex, block, slice))
+    uint32_t* vflag;
+    uint32_t* qd;             // entry: rowstart - work offset (edge id = item + qd)
+    unsigned long long* qmask;  // entry masks [j * kWide + b]
 };
+constexpr uint32_t kWide = 2;         // blocks (x 64 colours) per wide frontier entry
+constexpr uint32_t kUnitWide = 64;    // work items per wide expansion unit (2 windows)
 // k_store.cu
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog);
+                     cudaStream_t st, unsigned long long* d_elog, bool wide);
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
-                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last);
+                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
+                     bool wide);
 // k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph
 void launch_init(const BatchArgs& a, cudaStream_t st);
 void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,
@@ -191,6 +201,7 @@ struct StoreHook {  // adds the per-batch finalise nodes after the level loop
     ulonglong2* VN;
     const uint32_t* roff;
     unsigned long long* d_elog;
+    bool wide;
 };
 bool level_loop_persistent(const BatchArgs& a);
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);

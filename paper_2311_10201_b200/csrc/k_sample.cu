@@ -656,6 +656,372 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     expand_ic_body<kC64, false>(a, tstart, h_level, use_cond);
 }
 
+// ------------------------------------------------------------------------ wide fusion (IC)
+// the kWide = 2 blocks of a batch (128 colours) share one
+// frontier. A frontier entry is a vertex with kWide masks; each reverse edge of it is read once
+// for all 128 colours, and the working masks are vertex-major, so {V, N}[u] of both blocks is
+// one 32-B sector. Measured with the oracle (C2 shape): 1.79x fewer edge reads per sample
+// than 64-colour groups. Same coins (keyed by the global sample id), hence the same RRR sets.
+constexpr int kWinW = (int)kUnitWide / 32;   // edge windows per unit
+constexpr int kVW = kWinW * (int)kWide;      // virtual windows (edge window, block)
+
+__global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
+    const uint64_t total = (uint64_t)a.ctl->slots * 64;
+    const uint64_t gblk0 = a.ctl->gblk0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->cont = 1;
+        a.ctl->level = 0;
+        if (use_cond) cudaGraphSetConditional(h_level, 1);
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(i >> 6), bit = (uint32_t)(i & 63);
+        const uint64_t s = 64ull * (gblk0 + b) + bit;
+        if (s >= a.theta) continue;
+        const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), a.k_start);
+        const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
+        const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
+        const unsigned long long old = atomicOr(&a.VN[(size_t)start * kWide + b].y, 1ull << bit);
+        if (old == 0 && atomicOr(&a.vflag[start], 1u) == 0) {
+            const unsigned pos = atomicAdd(&a.lv[0].raw, 1u);
+            if (pos < a.raw_cap) a.raw[pos] = start;
+            else a.lv[0].overflow = 1;
+        }
+    }
+}
+
+// A4 for wide entries: for each queued vertex v: masks m_b = N_b; V_b |= N_b; N_b = 0; vflag = 0.
+__global__ void __launch_bounds__(kThreads, 5) k_compact_w(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                        uint64_t tstart_cap) {
+    if (!a.ctl->cont) return;
+    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
+    LevelRec* L = &a.lv[a.ctl->level];
+    const uint64_t nraw = umin64(L->raw, a.raw_cap);
+    constexpr uint32_t unit = kUnitWide;
+    __shared__ unsigned long long wsum[kWarps];
+    __shared__ uint32_t wcnt[kWarps];
+    __shared__ unsigned long long blk_base;
+    __shared__ unsigned long long vc_acc[kWarps];
+    constexpr uint32_t kBig = 64;
+    __shared__ unsigned long long big_u0[kBig], big_u1[kBig];
+    __shared__ uint32_t big_q[kBig];
+    __shared__ uint32_t big_n;
+    if (threadIdx.x == 0) big_n = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long vc_local = 0;
+    for (uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kCompTile) {
+        uint32_t vv[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
+            vv[it] = i < nraw ? (uint32_t)a.raw[i] : ~0u;
+        }
+        uint64_t mask[kCompItems][kWide];
+        uint32_t rs[kCompItems], re[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            rs[it] = re[it] = 0;
+#pragma unroll
+            for (uint32_t b = 0; b < kWide; ++b) mask[it][b] = 0;
+            if (vv[it] != ~0u) {
+                const uint32_t v = vv[it];
+                ulonglong2* p = &a.VN[(size_t)v * kWide];
+#pragma unroll
+                for (uint32_t b = 0; b < kWide; ++b) {
+                    const ulonglong2 x = p[b];
+                    mask[it][b] = x.y;
+                    if (x.y) p[b] = make_ulonglong2(x.x | x.y, 0ull);
+                }
+                a.vflag[v] = 0;
+                rs[it] = __ldg(&a.roff[v]);
+                re[it] = __ldg(&a.roff[v + 1]);
+            }
+        }
+        uint32_t cnt = 0;
+        unsigned long long work_t = 0;
+        uint64_t work[kCompItems];
+#pragma unroll
+        for (int it = 0; it < kCompItems; ++it) {
+            uint64_t any = 0;
+#pragma unroll
+            for (uint32_t b = 0; b < kWide; ++b) { vc_local += __popcll(mask[it][b]); any |= mask[it][b]; }
+            work[it] = any ? re[it] - rs[it] : 0;
+            cnt += work[it] != 0;
+            work_t += work[it];
+        }
+        uint32_t cincl = cnt;
+        unsigned long long wincl = work_t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t yc = __shfl_up_sync(kFull, cincl, d);
+            const unsigned long long yw = __shfl_up_sync(kFull, wincl, d);
+            if (lane >= d) { cincl += yc; wincl += yw; }
+        }
+        if (lane == 31) { wsum[wid] = wincl; wcnt[wid] = cincl; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long ts = 0;
+            uint32_t tc = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                const unsigned long long s2 = wsum[w];
+                const uint32_t c2 = wcnt[w];
+                wsum[w] = ts; wcnt[w] = tc; ts += s2; tc += c2;
+            }
+            unsigned long long old = tc ? atomicAdd(&L->packed, ((unsigned long long)tc << kPackShift) + ts) : 0ull;
+            if (tc && ((old >> kPackShift) + tc > a.q_cap || (old & kEdgeMask) + ts > kEdgeMask)) {
+                L->overflow = 1;
+                old = ~0ull;
+            }
+            blk_base = old;
+        }
+        __syncthreads();
+        const unsigned long long bb = blk_base;
+        if (bb != ~0ull && cnt) {
+            uint64_t qi = (bb >> kPackShift) + wcnt[wid] + cincl - cnt;
+            uint64_t off = (bb & kEdgeMask) + wsum[wid] + wincl - work_t;
+            uint64_t mword = ~0ull;
+            uint32_t mbits = 0;
+#pragma unroll
+            for (int it = 0; it < kCompItems; ++it) {
+                if (!work[it]) continue;
+                a.qd[qi] = rs[it] - (uint32_t)off;
+#pragma unroll
+                for (uint32_t b = 0; b < kWide; ++b) a.qmask[qi * kWide + b] = mask[it][b];
+                if (off / unit < tstart_cap) {
+                    if ((off >> 5) != mword) {
+                        if (mbits) atomicOr(&a.umask[mword], mbits);
+                        mword = off >> 5;
+                        mbits = 0;
+                    }
+                    mbits |= 1u << (off & 31u);
+                }
+                const uint64_t u0 = (off + unit - 1) / unit, u1 = (off + work[it] + unit - 1) / unit;
+                if (u1 > tstart_cap) L->overflow = 1;
+                const uint64_t u1c = umin64(u1, tstart_cap);
+                if (u1c > u0 + 4) {
+                    const uint32_t bi = atomicAdd(&big_n, 1u);
+                    if (bi < kBig) {
+                        big_u0[bi] = u0;
+                        big_u1[bi] = u1c;
+                        big_q[bi] = (uint32_t)qi;
+                    } else {
+                        for (uint64_t t = u0; t < u1c; ++t) tstart[t] = (uint32_t)qi;
+                    }
+                } else {
+                    for (uint64_t t = u0; t < u1c; ++t) tstart[t] = (uint32_t)qi;
+                }
+                ++qi;
+                off += work[it];
+            }
+            if (mbits) atomicOr(&a.umask[mword], mbits);
+        }
+        __syncthreads();
+        const uint32_t nbig = min(big_n, (uint32_t)kBig);
+        for (uint32_t bi = 0; bi < nbig; ++bi)
+            for (uint64_t t = big_u0[bi] + threadIdx.x; t < big_u1[bi]; t += kThreads) tstart[t] = big_q[bi];
+        __syncthreads();
+        if (threadIdx.x == 0) big_n = 0;
+    }
+    unsigned long long vc_tot = block_sum_ull(vc_local, vc_acc);
+    if (threadIdx.x == 0 && vc_tot) atomicAdd(&L->vc, vc_tot);
+    if (threadIdx.x == 0) atomicMax(&a.ctl->c_end, global_ns());
+}
+
+struct WarpScratchW {
+    uint32_t excl[32];
+    uint32_t cum[32];                      // byte q: tasks of virtual windows 0..q (q < kVW - 1)
+    unsigned long long live[kVW][32];
+    uint32_t e[kWinW][32];
+    uint32_t thr[kWinW][32];
+    unsigned long long pass[kVW][32];      // 32-bit halves: native ATOMS.OR
+    unsigned long long ebuf[32 + kUnitWide];
+    uint32_t ecount;
+};
+
+__device__ __forceinline__ void warp_flush_w(const BatchArgs& a, LevelRec* Ln, WarpScratchW& W, int lane) {
+    const uint32_t cnt = W.ecount;
+    if (cnt == 0) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&Ln->raw, cnt);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t pos = (uint64_t)base + i;
+        if (pos < a.raw_cap) a.raw[pos] = W.ebuf[i];
+        else Ln->overflow = 1;
+    }
+    __syncwarp();
+    if (lane == 0) W.ecount = 0;
+    __syncwarp();
+}
+
+template <bool kWhole>
+__device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, WarpScratchW& W, int lane,
+                                              uint32_t le_mask, uint32_t unit, uint32_t rem, uint32_t jc0,
+                                              uint32_t sb0, unsigned long long& coins, unsigned long long& atoms) {
+    const uint32_t t0l = unit * kUnitWide;
+    uint32_t mw[kWinW];
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) mw[w] = a.umask[(size_t)unit * kWinW + w];
+    __syncwarp();
+    if (lane < kWinW) a.umask[(size_t)unit * kWinW + lane] = 0;
+    mw[0] &= ~1u;
+    uint32_t jl[kWinW];
+    uint32_t before = jc0;
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+        jl[w] = before + __popc(mw[w] & le_mask);
+        before += __popc(mw[w]);
+        if (!kWhole && 32u * w + lane >= rem) jl[w] = jc0;
+    }
+    uint32_t d[kWinW];
+    ulonglong2 M[kWinW];  // {mask of block 0, mask of block 1}
+    uint2 rc[kWinW];
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+        d[w] = a.qd[jl[w]];
+        M[w] = reinterpret_cast<const ulonglong2*>(a.qmask)[jl[w]];
+    }
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        rc[w] = ld_stream(&a.rec[t0l + i + d[w]]);
+    }
+    uint64_t live[kVW];
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+        const ulonglong2* p = &a.VN[(size_t)rc[w].x * kWide];
+        const ulonglong2 v0 = ld_keep(p), v1 = ld_keep(p + 1);
+        live[w * kWide + 0] = M[w].x & ~(v0.x | v0.y);
+        live[w * kWide + 1] = M[w].y & ~(v1.x | v1.y);
+        if (!kWhole && 32u * w + lane >= rem) live[w * kWide + 0] = live[w * kWide + 1] = 0;
+    }
+    uint32_t c[kVW], tot = 0;
+#pragma unroll
+    for (int q = 0; q < kVW; ++q) { c[q] = __popcll(live[q]); tot += c[q]; }
+    const uint32_t incl = warp_incl_scan_u32(tot, lane);
+    const uint32_t ntask = __shfl_sync(kFull, incl, 31);
+    uint64_t pass[kVW];
+#pragma unroll
+    for (int q = 0; q < kVW; ++q) pass[q] = 0;
+    if (ntask) {
+#pragma unroll
+        for (int w = 0; w < kWinW; ++w) {
+            W.e[w][lane] = t0l + 32u * w + lane + d[w];
+            W.thr[w][lane] = rc[w].y;
+        }
+#pragma unroll
+        for (int q = 0; q < kVW; ++q) { W.pass[q][lane] = 0; W.live[q][lane] = live[q]; }
+        W.excl[lane] = incl - tot;
+        uint32_t cm = 0, run = 0;
+#pragma unroll
+        for (int q = 0; q < kVW - 1; ++q) { run += c[q]; cm |= run << (8 * q); }  // <= 192 per byte
+        W.cum[lane] = cm;
+        __syncwarp();
+        for (uint32_t b = 0; b < ntask; b += 32) {
+            const uint32_t k = b + lane;
+            if (k < ntask) {
+                uint32_t o = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (W.excl[o + step] <= k) o += step;
+                uint32_t r = k - W.excl[o];
+                const uint32_t cmo = W.cum[o];
+                uint32_t q = 0, base = 0;
+#pragma unroll
+                for (int qq = 0; qq < kVW - 1; ++qq) {
+                    const uint32_t pq = (cmo >> (8 * qq)) & 0xffu;
+                    if (r >= pq) { q = qq + 1; base = pq; }
+                }
+                r -= base;
+                const uint32_t bit = nth_set_bit64(W.live[q][o], r);
+                const uint32_t w = q / kWide, blk = q % kWide;
+                const uint32_t x = philox2x32_10(W.e[w][o], sb0 + 64u * blk + bit, a.k_ic).x;
+                if ((x >> 1) < W.thr[w][o])
+                    atomicOr(reinterpret_cast<uint32_t*>(&W.pass[q][o]) + (bit >> 5), 1u << (bit & 31));
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kVW; ++q) pass[q] = W.pass[q][lane];
+        __syncwarp();
+        if (lane == 0) coins += ntask;
+    }
+    // merges; a vertex is queued once per level (vflag) by the first setter of any of its words
+    unsigned long long old[kVW];
+#pragma unroll
+    for (int q = 0; q < kVW; ++q) {
+        old[q] = ~0ull;
+        if (pass[q]) {
+            ++atoms;
+            old[q] = atomicOr(&a.VN[(size_t)rc[q / kWide].x * kWide + (q % kWide)].y, pass[q]);
+        }
+    }
+    uint32_t nf = 0;
+    bool first[kWinW];
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+        first[w] = false;
+        const bool fw = old[w * kWide] == 0 || old[w * kWide + 1] == 0;
+        if (fw && atomicOr(&a.vflag[rc[w].x], 1u) == 0) first[w] = true;
+        nf += first[w];
+    }
+    if (!__any_sync(kFull, nf != 0)) return;
+    const uint32_t fincl = warp_incl_scan_u32(nf, lane);
+    const uint32_t nfirst = __shfl_sync(kFull, fincl, 31);
+    uint32_t pos = W.ecount + fincl - nf;
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w)
+        if (first[w]) W.ebuf[pos++] = rc[w].x;
+    __syncwarp();
+    if (lane == 0) W.ecount += nfirst;
+    __syncwarp();
+    if (W.ecount >= 32) warp_flush_w(a, Ln, W, lane);
+}
+
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                             cudaGraphConditionalHandle h_level, int use_cond) {
+    Ctl* ctl = a.ctl;
+    if (!ctl->cont) return;
+    const uint32_t level = ctl->level;
+    const uint64_t gblk0 = ctl->gblk0;
+    const LevelRec* L = &a.lv[level];
+    LevelRec* Ln = &a.lv[level + 1];
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    const unsigned long long packed = L->packed;
+    const uint64_t nq = packed >> kPackShift;
+    const uint64_t total = packed & kEdgeMask;
+    if (nq == 0 || L->overflow) {
+        finish_expand(a, h_level, use_cond);
+        return;
+    }
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpScratchW* scratch = reinterpret_cast<WarpScratchW*>(smem_raw);
+    __shared__ unsigned long long red[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpScratchW& W = scratch[wid];
+    if (lane == 0) W.ecount = 0;
+    __syncwarp();
+    const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
+    const uint32_t nunits = (uint32_t)((total + kUnitWide - 1) / kUnitWide);
+    const uint32_t nfull = (uint32_t)(total / kUnitWide);
+    const uint32_t sb0 = (uint32_t)(64ull * gblk0);
+    unsigned long long coins = 0, atoms = 0;
+    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += gridDim.x * kWarps) {
+        const uint32_t jc0 = tstart[unit];
+        if (unit < nfull)
+            expand_unit_w<true>(a, Ln, W, lane, le_mask, unit, kUnitWide, jc0, sb0, coins, atoms);
+        else
+            expand_unit_w<false>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitWide), jc0,
+                                 sb0, coins, atoms);
+    }
+    warp_flush_w(a, Ln, W, lane);
+    unsigned long long ct = block_sum_ull(coins, red);
+    if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
+    unsigned long long at = block_sum_ull(atoms, red);
+    if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
+    finish_expand(a, h_level, use_cond);
+}
+
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
@@ -843,6 +1209,7 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 
 
 int g_expand_grid = 0;
+int g_expand_grid_w = 0;
 int g_expand_grid_lt = 0;
 int g_levels_grid_lt = 0;
 int g_levels_grid_ic = 0;
@@ -863,6 +1230,12 @@ int expand_grid() {
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true>, kThreads,
                                                                sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
+        int per_sm_w = 0;
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(WarpScratchW) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, k_expand_w, kThreads,
+                                                               sizeof(WarpScratchW) * kWarps));
+        g_expand_grid_w = num_sms() * (per_sm_w > 0 ? per_sm_w : 1);
         int per_sm_lt = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_lt, k_expand_lt, kThreads, sizeof(SmemTile)));
         g_expand_grid_lt = num_sms() * (per_sm_lt > 0 ? per_sm_lt : 1);
@@ -889,6 +1262,7 @@ int expand_grid() {
 
 // LT batches run their level loop as one cooperative launch (BPT_LT_PERSIST=0: per-level launches)
 bool level_loop_persistent(const BatchArgs& a) {
+    if (a.wide) return false;
     if (a.model == BPT_IC) {
         const char* pi = getenv("BPT_IC_PERSIST");
         return pi && pi[0] == '1';
@@ -900,7 +1274,8 @@ bool level_loop_persistent(const BatchArgs& a) {
 static unsigned init_grid(const BatchArgs& a) { return (unsigned)(((uint64_t)a.slots_max * 64 + 255) / 256); }
 
 void launch_init(const BatchArgs& a, cudaStream_t st) {
-    k_init<<<init_grid(a), 256, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
+    if (a.wide) k_init_w<<<init_grid(a), 256, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
+    else k_init<<<init_grid(a), 256, 0, st>>>(a, (cudaGraphConditionalHandle)0, 0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_init");
 }
@@ -910,9 +1285,18 @@ void launch_init(const BatchArgs& a, cudaStream_t st) {
 void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,
                   cudaEvent_t ev1) {
     expand_grid();
+    const cudaGraphConditionalHandle h0 = 0;
+    if (a.wide) {
+        k_compact_w<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap);
+        if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
+        k_expand_w<<<g_expand_grid_w, kThreads, sizeof(WarpScratchW) * kWarps, st>>>(a, tstart, h0, 0);
+        if (ev1) BPT_CUDA(cudaEventRecord(ev1, st));
+        count_launch(2);
+        ::bpt::check_cuda(cudaGetLastError(), "launch wide level kernels");
+        return;
+    }
     k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model));
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
-    const cudaGraphConditionalHandle h0 = 0;
     if (a.model == BPT_IC && a.colors == 64)
         k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
@@ -970,7 +1354,8 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     int zero = 0;
     // batch body: init
     void* init_args[] = {&args, &h_level, lt_persist ? &zero : &one};
-    cudaGraphNode_t n_init = add_kernel(body, nullptr, (void*)k_init, dim3(init_grid(a)), dim3(256), 0, init_args);
+    cudaGraphNode_t n_init =
+        add_kernel(body, nullptr, a.wide ? (void*)k_init_w : (void*)k_init, dim3(init_grid(a)), dim3(256), 0, init_args);
     if (lt_persist) {
         // the whole level loop as one cooperative launch (grid barriers between phases)
         void* lv_args[] = {&args, &tstart, &tstart_cap};
@@ -984,7 +1369,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         coop.cooperative = 1;
         BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
         cudaGraphNode_t n_store;
-        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);
+        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0);
         void* nb_args[] = {&args, &h_batch, &one};
         add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
         cudaGraphExec_t exec;
@@ -1003,9 +1388,15 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     cudaGraph_t lbody = cl.conditional.phGraph_out[0];
     uint32_t unit = expand_unit(a.model);
     void* cmp_args[] = {&args, &tstart, &tstart_cap, &unit};
-    cudaGraphNode_t n_cmp = add_kernel(lbody, nullptr, (void*)k_compact, dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
+    void* cmpw_args[] = {&args, &tstart, &tstart_cap};
+    cudaGraphNode_t n_cmp = a.wide
+        ? add_kernel(lbody, nullptr, (void*)k_compact_w, dim3(g_compact_grid), dim3(kThreads), 0, cmpw_args)
+        : add_kernel(lbody, nullptr, (void*)k_compact, dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
     void* exp_args[] = {&args, &tstart, &h_level, &one};
-    cudaGraphNode_t n_exp = a.model == BPT_IC
+    cudaGraphNode_t n_exp = a.wide
+        ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),
+                     sizeof(WarpScratchW) * kWarps, exp_args)
+        : a.model == BPT_IC
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
@@ -1028,7 +1419,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     }
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
-    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store);
+    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0);
     void* nb_args[] = {&args, &h_batch, &one};
     add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
 

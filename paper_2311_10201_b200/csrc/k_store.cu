@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
                                                           uint64_t chunk, const uint32_t* __restrict__ roff,
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
                                                           unsigned long long* __restrict__ elog_total,
-                                                          uint32_t* __restrict__ count0, int single_slot) {
+                                                          uint32_t* __restrict__ count0, int single_slot,
+                                                          uint32_t vstride, uint64_t sstride) {
     constexpr int kW = kFinThreads / 32;
     __shared__ unsigned long long s_mask[kW][32];
     __shared__ uint32_t s_size[kW][64];
@@ -41,7 +42,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     if (blockIdx.y >= ctl->slots) return;
     const uint64_t blk = ctl->blk0 + blockIdx.y;
     uint64_t* V = store + (size_t)blk * n;
-    ulonglong2* W = VN + (size_t)blockIdx.y * n;
+    // working mask of vertex v of this block: W[v * vstride] (slot-major: vstride 1, sstride n;
+    // wide vertex-major: vstride kWide, sstride 1)
+    ulonglong2* W = VN + (size_t)blockIdx.y * sstride;
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const uint64_t v = base + 32ull * u + lane;
-            m[u] = v < v_end ? W[v].x : 0ull;  // N is 0 after the last level
+            m[u] = v < v_end ? W[v * vstride].x : 0ull;  // N is 0 after the last level
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
             if (v < v_end) {
                 V[v] = m[u];
                 if (m[u]) {
-                    W[v] = make_ulonglong2(0ull, 0ull);
+                    W[v * vstride] = make_ulonglong2(0ull, 0ull);
                     const uint32_t pc = __popcll(m[u]);
                     // occurrences (A7 round 0): one block owns v when the batch has one slot
                     if (single_slot) count0[v] += pc;
@@ -238,19 +241,21 @@ void compute_digests(const Samples& S, cudaStream_t st) {
 }
 
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog) {
+                     cudaStream_t st, unsigned long long* d_elog, bool wide) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
                                              S.sizes.as<uint32_t>(), d_elog,
-                                             S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0);
+                                             S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0,
+                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
 }
 
 // graph node for the finaliser (device-resident batch loop)
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
-                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last) {
+                     uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
+                     bool wide) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     uint64_t* store = S.store.as<uint64_t>();
@@ -259,8 +264,10 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     uint32_t* sizes = S.sizes.as<uint32_t>();
     uint32_t* count0 = S.count0.as<uint32_t>();
     int single = slots_max == 1 ? 1 : 0;
+    uint32_t vstride = wide ? kWide : 1u;
+    uint64_t sstride = wide ? 1 : (uint64_t)n;
     void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog,
-                        &count0, &single};
+                        &count0, &single, &vstride, &sstride};
     cudaKernelNodeParams p{};
     p.func = (void*)k_finalize;
     p.gridDim = grid;

@@ -301,6 +301,34 @@ def test_level_loop_variants(bpt, monkeypatch, model):
     assert infos[:half] == infos[half:]
 
 
+@pytest.mark.parametrize("which", ["C1", "C2s"])
+def test_wide_fusion(bpt, monkeypatch, which):
+    """Wide fusion (BPT_WIDE=1: 2 blocks = 128 colours share one frontier):
+    identical RRR sets, seeds and gains; E_phys equals the oracle's group work of the 128-sample
+    groups (the same distinct-(v, level) formula), and stays <= E_logical."""
+    monkeypatch.setenv("BPT_WIDE", "1")
+    if which == "C1":
+        cfg = graphgen.CONFIGS["C1"]
+    else:
+        cfg = graphgen.scaled(graphgen.CONFIGS["C2"], 1 << 14, theta=1024 + 64 + 17)  # ragged last batch
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    for profile in (False, True):
+        s = g.sample(cfg.theta, colors=64, seed=cfg.seed, profile=profile)
+        check_full(bpt, s, ref, cfg.theta)
+        seeds, gains, _ = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+        info = s.info
+        assert info["batch_groups"] == 2
+        e_phys = sum(ref["g"].group_work(cfg.seed, a, min(a + 128, cfg.theta))["e_phys"]
+                     for a in range(0, cfg.theta, 128))
+        assert info["e_phys"] == e_phys
+        assert info["e_logical"] == int(ref["elog"].sum())
+        assert info["e_phys"] <= info["e_logical"]
+        s.close()
+
+
 # ------------------------------------------------------------------ C2 / C5 shape, scaled
 
 @pytest.fixture(scope="module")
