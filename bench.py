@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batch-groups", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-wide", action="store_true", help="skip the wide-fusion (128-colour) side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0, help="oracle sample size (0 = auto)")
     return ap.parse_args()
@@ -212,14 +213,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
 
-    def step(profile: bool, host: dict | None = None):
+    def step(profile: bool, host: dict | None = None, wide: bool = False):
         if host is None:
             g = bpt.Graph(d_row, d_col, w_q31=d_thr, model=model, comm=comm, n=cfg.n, m=cfg.m, stream=stream)
         else:
             g = bpt.Graph(host["row"], host["col"], w_q31=host["thr"], model=model, comm=comm, n=cfg.n, m=cfg.m,
                           stream=stream)
         s = g.sample(cfg.theta, colors=cfg.colors, seed=cfg.seed, stream=stream, batch_groups=args.batch_groups,
-                     profile=profile)
+                     profile=profile, wide=wide)
         first = s.s0
         cnt = min(EXTRACT_SAMPLES, s.s1 - s.s0)
         d2h = 0
@@ -310,6 +311,35 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = {"value": cfg.theta / (float(et.item()) / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": float(et.item())}
 
+    # wide fusion (BPT_FLAG_WIDE: 128 colours per frontier entry), the same
+    # step with two 64-sample blocks sharing one frontier; reported beside the 64-colour headline
+    wide = None
+    if cfg.model == "IC" and cfg.colors == 64 and not args.batch_groups and not args.no_wide:
+        step(False, wide=True)
+        barrier()
+        torch.cuda.synchronize()
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        n_w = max(1, min(args.steps, 3))
+        winfos = []
+        for _ in range(n_w):
+            wi, _, _ = step(False, wide=True)
+            winfos.append(wi)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        wt = torch.tensor([w0.elapsed_time(w1) / n_w], dtype=torch.float64)
+        wa = torch.tensor([float(np.mean([i["e_phys"] for i in winfos]))], dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+            dist.all_reduce(wa, op=dist.ReduceOp.SUM)
+        wms = float(wt.item())
+        wide = {"value": cfg.theta / (wms / 1000.0), "unit": UNIT, "ms_per_step": wms, "steps": n_w,
+                "colors_per_frontier_entry": 128, "edges_visited_per_step": float(wa.item()),
+                "fusion_factor": e_log_all / float(wa.item()) if wa.item() else None,
+                "note": "same step and RRR sets; two 64-sample blocks share one frontier (vertex-major masks)"}
+
     if rank != 0:
         return
     peak, peak_src = measured_peak_hbm()
@@ -345,6 +375,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "wide_fusion": wide,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk,

@@ -126,6 +126,11 @@ typedef struct {
     uint32_t reserved;
 } bpt_sample_opts;
 #define BPT_FLAG_PROFILE 1u  /* time every expansion launch with CUDA events */
+/* Wide fusion (the paper fuses up to 1024 colours): IC with
+ * colors = 64 and batch_groups = 0 only -- two 64-sample blocks (128 colours) share one
+ * frontier, so each reverse edge of a frontier vertex is read once for 128 samples. Same RRR
+ * sets (coins are keyed by the global sample id); E_phys counts the 128-sample groups. */
+#define BPT_FLAG_WIDE 2u
 
 BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
                       void* stream, bpt_samples** out);

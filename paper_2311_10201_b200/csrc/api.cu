@@ -225,7 +225,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 2048);
     // wide fusion (IC, 64 colours): kWide blocks share one frontier (k_sample.cu "wide fusion")
     const char* wide_env = getenv("BPT_WIDE");
-    const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups && wide_env && wide_env[0] == '1';
+    const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups &&
+                      ((opt.flags & BPT_FLAG_WIDE) || (wide_env && wide_env[0] == '1'));
     if (wide) want = kWide;
     uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
     const uint32_t tile = wide ? kUnitWide : expand_unit(S.model);

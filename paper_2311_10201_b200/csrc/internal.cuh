@@ -184,7 +184,10 @@ struct BatchArgs {
     unsigned long long* qmask;  // entry masks [j * kWide + b]
 };
 constexpr uint32_t kWide = 2;         // blocks (x 64 colours) per wide frontier entry
-constexpr uint32_t kUnitWide = 64;    // work items per wide expansion unit (2 windows)
+#ifndef BPT_UNIT_WIDE
+#define BPT_UNIT_WIDE 64
+#endif
+constexpr uint32_t kUnitWide = BPT_UNIT_WIDE;  // work items per wide expansion unit (windows of 32)
 // k_store.cu
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog, bool wide);

@@ -302,11 +302,10 @@ def test_level_loop_variants(bpt, monkeypatch, model):
 
 
 @pytest.mark.parametrize("which", ["C1", "C2s"])
-def test_wide_fusion(bpt, monkeypatch, which):
-    """Wide fusion (BPT_WIDE=1: 2 blocks = 128 colours share one frontier):
+def test_wide_fusion(bpt, which):
+    """Wide fusion (BPT_FLAG_WIDE: 2 blocks = 128 colours share one frontier):
     identical RRR sets, seeds and gains; E_phys equals the oracle's group work of the 128-sample
     groups (the same distinct-(v, level) formula), and stays <= E_logical."""
-    monkeypatch.setenv("BPT_WIDE", "1")
     if which == "C1":
         cfg = graphgen.CONFIGS["C1"]
     else:
@@ -315,7 +314,7 @@ def test_wide_fusion(bpt, monkeypatch, which):
     ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
     for profile in (False, True):
-        s = g.sample(cfg.theta, colors=64, seed=cfg.seed, profile=profile)
+        s = g.sample(cfg.theta, colors=64, seed=cfg.seed, profile=profile, wide=True)
         check_full(bpt, s, ref, cfg.theta)
         seeds, gains, _ = s.select_seeds(cfg.k)
         assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
