@@ -183,7 +183,10 @@ struct BatchArgs {
     uint32_t* qd;             // entry: rowstart - work offset (edge id = item + qd)
     unsigned long long* qmask;  // entry masks [j * kWide + b]
 };
-constexpr uint32_t kWide = 2;         // blocks (x 64 colours) per wide frontier entry
+#ifndef BPT_WIDE_BLOCKS
+#define BPT_WIDE_BLOCKS 2
+#endif
+constexpr uint32_t kWide = BPT_WIDE_BLOCKS;  // blocks (x 64 colours) per wide frontier entry (even)
 #ifndef BPT_UNIT_WIDE
 #define BPT_UNIT_WIDE 64
 #endif

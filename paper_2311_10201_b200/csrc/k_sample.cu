@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
 // than 64-colour groups. Same coins (keyed by the global sample id), hence the same RRR sets.
 constexpr int kWinW = (int)kUnitWide / 32;   // edge windows per unit
 constexpr int kVW = kWinW * (int)kWide;      // virtual windows (edge window, block)
+static_assert(kVW <= 4 && kWide % 2 == 0, "task prefixes of kVW - 1 virtual windows are packed in 32 bits");
 
 __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
     const uint64_t total = (uint64_t)a.ctl->slots * 64;
@@ -874,12 +875,18 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
         if (!kWhole && 32u * w + lane >= rem) jl[w] = jc0;
     }
     uint32_t d[kWinW];
-    ulonglong2 M[kWinW];  // {mask of block 0, mask of block 1}
+    uint64_t M[kWinW][kWide];  // the entry's mask per block
     uint2 rc[kWinW];
 #pragma unroll
     for (int w = 0; w < kWinW; ++w) {
         d[w] = a.qd[jl[w]];
-        M[w] = reinterpret_cast<const ulonglong2*>(a.qmask)[jl[w]];
+        const ulonglong2* mp = reinterpret_cast<const ulonglong2*>(a.qmask + (size_t)jl[w] * kWide);
+#pragma unroll
+        for (uint32_t b = 0; b < kWide; b += 2) {
+            const ulonglong2 x = mp[b / 2];
+            M[w][b] = x.x;
+            M[w][b + 1] = x.y;
+        }
     }
 #pragma unroll
     for (int w = 0; w < kWinW; ++w) {
@@ -890,10 +897,11 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
 #pragma unroll
     for (int w = 0; w < kWinW; ++w) {
         const ulonglong2* p = &a.VN[(size_t)rc[w].x * kWide];
-        const ulonglong2 v0 = ld_keep(p), v1 = ld_keep(p + 1);
-        live[w * kWide + 0] = M[w].x & ~(v0.x | v0.y);
-        live[w * kWide + 1] = M[w].y & ~(v1.x | v1.y);
-        if (!kWhole && 32u * w + lane >= rem) live[w * kWide + 0] = live[w * kWide + 1] = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < kWide; ++b) {
+            const ulonglong2 vn = ld_keep(p + b);
+            live[w * kWide + b] = (!kWhole && 32u * w + lane >= rem) ? 0ull : M[w][b] & ~(vn.x | vn.y);
+        }
     }
     uint32_t c[kVW], tot = 0;
 #pragma unroll
@@ -961,7 +969,9 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
 #pragma unroll
     for (int w = 0; w < kWinW; ++w) {
         first[w] = false;
-        const bool fw = old[w * kWide] == 0 || old[w * kWide + 1] == 0;
+        bool fw = false;
+#pragma unroll
+        for (uint32_t b = 0; b < kWide; ++b) fw |= old[w * kWide + b] == 0;
         if (fw && atomicOr(&a.vflag[rc[w].x], 1u) == 0) first[w] = true;
         nf += first[w];
     }

@@ -319,9 +319,10 @@ def test_wide_fusion(bpt, which):
         seeds, gains, _ = s.select_seeds(cfg.k)
         assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
         info = s.info
-        assert info["batch_groups"] == 2
-        e_phys = sum(ref["g"].group_work(cfg.seed, a, min(a + 128, cfg.theta))["e_phys"]
-                     for a in range(0, cfg.theta, 128))
+        B = info["batch_groups"]  # blocks sharing one frontier (2 in the product build)
+        assert B >= 2
+        e_phys = sum(ref["g"].group_work(cfg.seed, a, min(a + 64 * B, cfg.theta))["e_phys"]
+                     for a in range(0, cfg.theta, 64 * B))
         assert info["e_phys"] == e_phys
         assert info["e_logical"] == int(ref["elog"].sum())
         assert info["e_phys"] <= info["e_logical"]
