@@ -30,6 +30,18 @@ def test_library_exports_every_header_symbol():
     assert bpt.bpt_abi_version() == 1
 
 
+def test_header_constants_match_binding():
+    """Every #define / enum value of include/bpt.h that the binding mirrors has the same value."""
+    import paper_2311_10201_b200 as bpt
+    hdr = open(os.path.join(ROOT, "include", "bpt.h")).read()
+    defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z]+) (\w+)", hdr)}
+    assert defs == {"BPT_FLAG_PROFILE": bpt.FLAG_PROFILE, "BPT_FLAG_WIDE": bpt.FLAG_WIDE}
+    enums = dict((k, int(v)) for k, v in re.findall(r"(BPT_E[A-Z]+|BPT_OK)\s*=\s*(-?\d+)", hdr))
+    for k in ("BPT_OK", "BPT_EINVAL", "BPT_ENOMEM", "BPT_ECUDA", "BPT_ENCCL", "BPT_ESTATE"):
+        assert enums[k] == getattr(bpt, k)
+    assert dict(re.findall(r"(BPT_IC|BPT_LT)\s*=\s*(\d+)", hdr)) == {"BPT_IC": str(bpt.IC), "BPT_LT": str(bpt.LT)}
+
+
 def test_library_is_sm100a_cuda():
     import paper_2311_10201_b200 as bpt
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", bpt.LIB_PATH], capture_output=True,
