@@ -219,6 +219,68 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     S.digests.alloc(nlocal * 8);
     BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
 
+    // ---- LT: one reverse walk per thread (k_sample.cu "LT reverse walks"); BPT_LT_FUSED=1 runs
+    //      the level-synchronous fused loop instead (same sets)
+    {
+        const char* ltf = getenv("BPT_LT_FUSED");
+        if (S.model == BPT_LT && !(ltf && ltf[0] == '1')) {
+            BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
+            DevBuf totals(16);
+            BPT_CUDA(cudaMemsetAsync(totals.p, 0, 16, st));
+            cudaEvent_t e0, e1;
+            BPT_CUDA(cudaEventCreate(&e0));
+            BPT_CUDA(cudaEventCreate(&e1));
+            BPT_CUDA(cudaEventRecord(e0, st));
+            launch_walk_lt(S.store.as<uint64_t>(), n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal,
+                           stream_key(S.seed, kTagStart), stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(),
+                           S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
+            BPT_CUDA(cudaEventRecord(e1, st));
+            unsigned long long tot[2] = {0, 0};
+            BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 16, cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaStreamSynchronize(st));
+            float ms = 0;
+            BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            BPT_CUDA(cudaEventDestroy(e0));
+            BPT_CUDA(cudaEventDestroy(e1));
+            // member lists for the selection's decrement, by re-walking (cheaper than a pass over the
+            // dense store); bpt_select_seeds finds them built
+            {
+                std::vector<uint32_t> sz(nlocal);
+                BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+                std::vector<uint64_t> off(nlocal + 1, 0);
+                for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
+                S.list_off.alloc((nlocal + 1) * 8);
+                S.list_mem.alloc(off[nlocal] * 4 + 4);
+                BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
+                launch_walk_lt_lists(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal,
+                                     stream_key(S.seed, kTagStart), stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(),
+                                     S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), st);
+                BPT_CUDA(cudaStreamSynchronize(st));
+                S.lists_built = S.lists_ok = true;
+            }
+            bpt_samples_info& I = S.info;
+            I.members = tot[0];
+            I.frontier_entries = tot[0];
+            I.coins = tot[0];    // one coinLT draw per member vertex
+            I.atomics = tot[0];  // one store atomicOr per member vertex (+ the stopping probe)
+            I.e_phys = I.e_logical = tot[0];  // (vertex, colour) expansions, SURVEY §8(d)
+            I.levels_total = I.levels_max = tot[1];
+            I.batch_groups = (uint32_t)S.blocks;
+            I.batches = 1;
+            I.store_bytes = S.store.bytes;
+            I.ms_expand = ms;
+            I.expand_launches = 1;
+            I.expand_bytes = 24.0 * (double)tot[0];  // row bounds 8 + chosen record 8 + store RMW 8 per member
+            S.level_rows.clear();
+            I.kernel_launches = g_launches - launches0;
+            I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+            if (getenv("BPT_TRACE"))
+                fprintf(stderr, "[bpt] sample (LT walks): %llu members, longest %llu, walks %.2f ms, total %.2f ms\n",
+                        tot[0], tot[1], ms, I.ms_total);
+            return;
+        }
+    }
+
     // ---- batch plan
     // IC: one block per batch keeps the working masks L2-resident; LT: as many as fit (fewer,
     // longer levels: LT frontiers are thin, per-level overhead dominates)

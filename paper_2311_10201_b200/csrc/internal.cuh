@@ -210,6 +210,15 @@ struct StoreHook {  // adds the per-batch finalise nodes after the level loop
     bool wide;
 };
 bool level_loop_persistent(const BatchArgs& a);
+// LT: every local sample's reverse walk in one launch (store must be zero; sizes written;
+// totals[0] += members, totals[1] = max walk length)
+void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                    uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0, unsigned long long* totals,
+                    cudaStream_t st);
+// LT: re-walk every local sample and write its members at off[i] (unsorted; for the selection)
+void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                          uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,
+                          uint32_t* members, cudaStream_t st);
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);
 // k_select.cu
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st);

@@ -1032,6 +1032,98 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     finish_expand(a, h_level, use_cond);
 }
 
+// ------------------------------------------------------------------------ LT reverse walks
+// Under LT (reading C-6) an RRR set is a single reverse walk: each sample is at ONE vertex per
+// level, so the 64 colours of a block never share an edge read (E_phys = E_logical = sum |RR|,
+// fusion saves nothing -- SURVEY §8(d)), and the level-synchronous fused loop costs ~50 us of
+// dependent latency per level for a few thousand walks. Here every thread walks one sample to
+// its end: coinLT(s, v) picks the in-edge (interpolation search of the row's cumulative
+// thresholds), and the visited set of sample s IS its bit in the RRR store (atomicOr; the walk
+// stops at a vertex already in the set, a vertex without in-edges, or on "no edge"). Same coins,
+// same sets as the fused loop (tests: BPT_LT_FUSED=1 runs the fused loop).
+__device__ __forceinline__ bool lt_pick(const uint32_t* __restrict__ roff, const uint2* __restrict__ rec, uint32_t v,
+                                        uint32_t r, uint32_t* u_out) {
+    uint32_t lo = __ldg(&roff[v]), hi = __ldg(&roff[v + 1]);
+    if (lo >= hi) return false;
+    uint2 hit = __ldg(&rec[hi - 1]);  // {src, row sum}
+    if (r >= hit.y) return false;
+    uint32_t clo = 0, chi = hit.y;
+    for (int step = 0; hi - lo > 1; ++step) {
+        uint32_t g;
+        if (step < 4) {
+            g = lo + (uint32_t)((uint64_t)(r - clo) * (hi - lo) / (uint64_t)(chi - clo));
+            g = min(g, hi - 2);
+        } else {
+            g = (lo + hi - 1) >> 1;
+        }
+        const uint2 x = __ldg(&rec[g]);
+        if (x.y > r) { hi = g + 1; chi = x.y; hit = x; }
+        else { lo = g + 1; clo = x.y; }
+    }
+    *u_out = hit.x;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_walk_lt(uint64_t* __restrict__ store, uint32_t n,
+                                                 const uint32_t* __restrict__ roff, const uint2* __restrict__ rec,
+                                                 uint64_t s0, uint64_t nlocal, uint32_t k_start, uint32_t k_lt,
+                                                 uint32_t* __restrict__ sizes, uint32_t* __restrict__ count0,
+                                                 unsigned long long* __restrict__ totals) {
+    unsigned long long members = 0;
+    uint32_t longest = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nlocal; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = s0 + i;  // s0 is block aligned: local block i / 64, colour bit s % 64
+        uint64_t* V = store + (i >> 6) * (uint64_t)n;
+        const unsigned long long bit = 1ull << (s & 63);
+        const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), k_start);
+        uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
+        atomicOr((unsigned long long*)&V[v], bit);
+        atomicAdd(&count0[v], 1u);
+        uint32_t size = 1, u = 0;
+        while (lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
+            if (atomicOr((unsigned long long*)&V[u], bit) & bit) break;  // already in RR_s
+            atomicAdd(&count0[u], 1u);
+            ++size;
+            v = u;
+        }
+        sizes[i] = size;
+        members += size;
+        longest = max(longest, size);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        members += __shfl_xor_sync(kFull, members, d);
+        longest = max(longest, __shfl_xor_sync(kFull, longest, d));
+    }
+    if ((threadIdx.x & 31) == 0 && members) {
+        atomicAdd(&totals[0], members);
+        atomicMax(&totals[1], (unsigned long long)longest);
+    }
+}
+
+// Second pass for the selection: re-walk each sample (same coins, same path; the walk length is
+// known from pass 1) and write its members to its slot of the member-list buffer.
+__global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_t* __restrict__ roff,
+                                                       const uint2* __restrict__ rec, uint64_t s0, uint64_t nlocal,
+                                                       uint32_t k_start, uint32_t k_lt,
+                                                       const uint32_t* __restrict__ sizes,
+                                                       const uint64_t* __restrict__ off, uint32_t* __restrict__ members) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nlocal; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = s0 + i;
+        const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), k_start);
+        uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
+        uint32_t* out = members + off[i];
+        const uint32_t size = sizes[i];
+        out[0] = v;
+        for (uint32_t j = 1; j < size; ++j) {
+            uint32_t u = 0;
+            lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u);
+            out[j] = u;
+            v = u;
+        }
+    }
+}
+
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
@@ -1226,6 +1318,24 @@ int g_levels_grid_ic = 0;
 int g_compact_grid = 0;
 
 }  // namespace
+
+void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                    uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0, unsigned long long* totals,
+                    cudaStream_t st) {
+    const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
+    k_walk_lt<<<grid ? grid : 1, 256, 0, st>>>(store, n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals);
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt");
+}
+
+void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                          uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,
+                          uint32_t* members, cudaStream_t st) {
+    const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
+    k_walk_lt_lists<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, off, members);
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_lists");
+}
 
 uint32_t expand_unit(int model) { return model == BPT_IC ? (uint32_t)kUnitIC : kTile; }
 

@@ -270,35 +270,43 @@ def test_lt_parity_scaled(bpt):
 
 @pytest.mark.parametrize("model", ["IC", "LT"])
 def test_level_loop_variants(bpt, monkeypatch, model):
-    """The two execution models of the level loop give the same RRR sets and the same exact
-    work counters: per-level launches inside the graph's conditional WHILE node, and one
-    cooperative launch per batch with grid barriers (LT default; IC opt-in BPT_IC_PERSIST=1),
-    each also in the host-driven profiling mode."""
+    """The execution models of the sampling loop give the same RRR sets, seeds and exact work
+    counters: per-level launches inside the graph's conditional WHILE node, one cooperative
+    launch per batch with grid barriers (LT fused default; IC opt-in BPT_IC_PERSIST=1), the
+    host-driven profiling mode, and for LT the one-walk-per-thread sampler (LT default)."""
     if model == "IC":
         cfg = graphgen.CONFIGS["C1"]
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr)
-        env, variants = "BPT_IC_PERSIST", ("1", "0")
+        variants = [{"BPT_IC_PERSIST": "1"}, {"BPT_IC_PERSIST": "0"}]
     else:
         cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 12, theta=2048)
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
-        env, variants = "BPT_LT_PERSIST", ("0", "1")
+        variants = [{"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "0"}, {"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "1"},
+                    {"BPT_LT_FUSED": "0"}]
     infos = []
-    for v in variants:
-        monkeypatch.setenv(env, v)
+    for env in variants:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        rows = []
         for colors, batch, profile in ((64, 1, False), (64, 5, False), (8, 2, False), (64, 3, True)):
             s = g.sample(cfg.theta, colors=colors, seed=cfg.seed, batch_groups=batch, profile=profile)
             check_full(bpt, s, ref, cfg.theta)
             seeds, gains, _ = s.select_seeds(cfg.k)
             assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
             info = s.info
-            infos.append((colors, batch, info["e_phys"], info["e_logical"], info["members"], info["levels_total"]))
+            walker = model == "LT" and env.get("BPT_LT_FUSED") == "0"
+            rows.append((info["e_phys"], info["e_logical"], info["members"]) if walker else
+                        (colors, batch, info["e_phys"], info["e_logical"], info["members"], info["levels_total"]))
             s.close()
-    half = len(infos) // 2
-    assert infos[:half] == infos[half:]
+        infos.append(rows)
+    assert infos[0] == infos[1]
+    if model == "LT":  # walks: same work counters as the fused loop (E_phys = E_logical = sum |RR|)
+        assert [r[2:5] for r in infos[0]] == infos[2]
+        assert all(r[0] == r[1] == r[2] == int(ref["sizes"].sum()) for r in infos[2])
 
 
 @pytest.mark.parametrize("which", ["C1", "C2s"])
