@@ -1521,22 +1521,6 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
     // the expansion's last block advances the level and sets the loop condition
-    if (getenv("BPT_L2PERSIST")) {  // experiment: keep the working masks in the persisting L2 carve-out
-        int maxp = 0, dev = 0;
-        BPT_CUDA(cudaGetDevice(&dev));
-        BPT_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-        const size_t bytes = (size_t)a.slots_max * a.n * 16;
-        BPT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
-        cudaKernelNodeAttrValue v{};
-        v.accessPolicyWindow.base_ptr = a.VN;
-        v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = bytes > (size_t)maxp ? (float)maxp / (float)bytes : 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_exp, cudaKernelNodeAttributeAccessPolicyWindow, &v));
-        BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_cmp, cudaKernelNodeAttributeAccessPolicyWindow, &v));
-        if (getenv("BPT_TRACE")) fprintf(stderr, "[bpt] L2 persisting carve-out %d bytes for %zu bytes of VN\n", maxp, bytes);
-    }
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
     add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0);
