@@ -146,10 +146,16 @@ def cpu_baseline(cfg, row_ptr, col, thr, nsamples: int | None = None, budget_s: 
     t0 = time.perf_counter()
     sizes, _, elog = g.sample_many(cfg.seed, ids, threads)
     dt = time.perf_counter() - t0
+    # single-thread rate on a small slice of the same ids (SURVEY §8(d) oracle timing)
+    n1 = max(1, min(nsamples, int(nsamples / max(threads, 1) / 2)))
+    t1 = time.perf_counter()
+    g.sample_many(cfg.seed, ids[:n1], 1)
+    dt1 = max(time.perf_counter() - t1, 1e-6)
     return {"value": nsamples / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{nsamples} of {cfg.theta} samples (ids 0..{nsamples - 1}) of {cfg.name}, unfused "
                       f"one-BPT-at-a-time oracle, {threads} threads, {dt:.1f} s",
-            "e_logical_per_s": float(elog.sum()) / dt, "seconds": dt}
+            "e_logical_per_s": float(elog.sum()) / dt, "seconds": dt,
+            "single_thread_value": n1 / dt1, "single_thread_sample": f"ids 0..{n1 - 1}, 1 thread, {dt1:.1f} s"}
 
 
 def run_reference(args, rank: int, world: int):
@@ -204,22 +210,27 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     row_ptr, col, thr = graphgen.make_graph(cfg)
     model = bpt.IC if cfg.model == "IC" else bpt.LT
-    d_row = torch.from_numpy(row_ptr.view(np.int64)).to(dev)
-    d_col = torch.from_numpy(col.view(np.int32)).to(dev)
-    d_thr = torch.from_numpy(thr.view(np.int32)).to(dev)
+    # (the generator's arrays are cached read-only; torch wants writable host arrays)
+    d_row = torch.from_numpy(row_ptr.view(np.int64).copy()).to(dev)
+    d_col = torch.from_numpy(col.view(np.int32).copy()).to(dev)
+    d_thr = torch.from_numpy(thr.view(np.int32).copy()).to(dev)
     stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    step_no = [0]  # sampling seeds rotate over cfg.seed + {0, 1, 2} (SURVEY §8(d) throughput protocol)
+
     def step(profile: bool, host: dict | None = None, wide: bool = False):
+        seed = cfg.seed + step_no[0] % 3
+        step_no[0] += 1
         if host is None:
             g = bpt.Graph(d_row, d_col, w_q31=d_thr, model=model, comm=comm, n=cfg.n, m=cfg.m, stream=stream)
         else:
             g = bpt.Graph(host["row"], host["col"], w_q31=host["thr"], model=model, comm=comm, n=cfg.n, m=cfg.m,
                           stream=stream)
-        s = g.sample(cfg.theta, colors=cfg.colors, seed=cfg.seed, stream=stream, batch_groups=args.batch_groups,
+        s = g.sample(cfg.theta, colors=cfg.colors, seed=seed, stream=stream, batch_groups=args.batch_groups,
                      profile=profile, wide=wide)
         first = s.s0
         cnt = min(EXTRACT_SAMPLES, s.s1 - s.s0)
@@ -287,9 +298,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # end-to-end through the C-ABI with pinned HOST buffers (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        host = {"row": torch.from_numpy(row_ptr.view(np.int64)).pin_memory(),
-                "col": torch.from_numpy(col.view(np.int32)).pin_memory(),
-                "thr": torch.from_numpy(thr.view(np.int32)).pin_memory()}
+        host = {"row": torch.from_numpy(row_ptr.view(np.int64).copy()).pin_memory(),
+                "col": torch.from_numpy(col.view(np.int32).copy()).pin_memory(),
+                "thr": torch.from_numpy(thr.view(np.int32).copy()).pin_memory()}
         h2d = row_ptr.nbytes + col.nbytes + thr.nbytes
         step(False, host)
         barrier()
@@ -366,11 +377,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "theta": cfg.theta, "colors": cfg.colors, "k": cfg.k,
                    "step": f"graph_load + sample + extract({EXTRACT_SAMPLES}/rank) + select_seeds(k={cfg.k})",
+                   "seeds": f"sampling seed rotates over {cfg.seed:#x} + (0, 1, 2) across steps",
                    "l2": "inputs and 39.7 GB store >> 126 MB L2 (no flush needed)",
                    "parallelism": f"sample-sharded x{world} (NCCL in selection only)"},
         "edges_visited_per_s": e_phys_all / (ms_max / 1000.0),
         "unfused_equiv_edges_per_s": e_log_all / (ms_max / 1000.0),
         "fusion_factor": e_log_all / e_phys_all if e_phys_all else None,
+        "frontier_occupancy": (float(np.mean([i["members"] for i in infos])) /
+                               (64.0 * float(np.mean([i["frontier_entries"] for i in infos])))
+                               if infos and infos[0]["frontier_entries"] else None),
         "ms_sample_per_step": ms_sample,
         "roofline": roofline,
         "cpu_baseline": cpu,
