@@ -270,7 +270,7 @@ def test_fused_equals_unfused_and_theorem1(trial):
     g = oracle.Graph(row_ptr, col, w_q31=thr)
     rev = g.reverse_csr()
     seed = 1000 + trial
-    for C in (1, 8, 64):
+    for C in (1, 8, 64, 128):  # 128: the wide-fusion groups (two 64-sample blocks)
         for s0 in range(0, 128, C):
             s1 = s0 + C
             vis, reads, levels = fused_level_sync(rev, seed, s0, s1)
@@ -284,7 +284,7 @@ def test_fused_equals_unfused_and_theorem1(trial):
             for c in range(C):
                 mem, _, _ = g.sample_one(seed, s0 + c)
                 assert [v for v in range(n) if vis[v] >> c & 1] == mem.tolist()
-            if C == 64:
+            if C >= 64:
                 break
 
 
