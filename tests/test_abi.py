@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -40,6 +41,14 @@ def test_header_constants_match_binding():
     for k in ("BPT_OK", "BPT_EINVAL", "BPT_ENOMEM", "BPT_ECUDA", "BPT_ENCCL", "BPT_ESTATE"):
         assert enums[k] == getattr(bpt, k)
     assert dict(re.findall(r"(BPT_IC|BPT_LT)\s*=\s*(\d+)", hdr)) == {"BPT_IC": str(bpt.IC), "BPT_LT": str(bpt.LT)}
+
+
+def test_import_before_torch():
+    """Loading libbpt.so before torch must not pin an older NCCL under the shared soname
+    (torch's libtorch_cuda needs the NCCL it was built with)."""
+    r = subprocess.run([sys.executable, "-c", "import paper_2311_10201_b200, torch; print('ok')"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_library_is_sm100a_cuda():
