@@ -13,6 +13,7 @@
 //           expand(L):  q -> N atomicOr, raw(L+1)             (Listing 1 lines 9-15)
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -664,7 +665,11 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
 // than 64-colour groups. Same coins (keyed by the global sample id), hence the same RRR sets.
 constexpr int kWinW = (int)kUnitWide / 32;   // edge windows per unit
 constexpr int kVW = kWinW * (int)kWide;      // virtual windows (edge window, block)
-static_assert(kVW <= 4 && kWide % 2 == 0, "task prefixes of kVW - 1 virtual windows are packed in 32 bits");
+static_assert(kVW <= 8 && kWide % 2 == 0, "task prefixes of kVW - 1 virtual windows must fit the cum word");
+// per-lane task prefixes of virtual windows 0..kVW-2: 8-bit fields of a u32 (<= 3 x 64) or
+// 9-bit fields of a u64 (<= 7 x 64)
+using CumW = std::conditional_t<(kVW <= 4), uint32_t, unsigned long long>;
+constexpr int kCumBits = kVW <= 4 ? 8 : 9;
 
 __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
     const uint64_t total = (uint64_t)a.ctl->slots * 64;
@@ -830,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_compact_w(BatchArgs a, uint32_t
 
 struct WarpScratchW {
     uint32_t excl[32];
-    uint32_t cum[32];                      // byte q: tasks of virtual windows 0..q (q < kVW - 1)
+    CumW cum[32];                          // field q: tasks of virtual windows 0..q (q < kVW - 1)
     unsigned long long live[kVW][32];
     uint32_t e[kWinW][32];
     uint32_t thr[kWinW][32];
@@ -875,32 +880,54 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
         if (!kWhole && 32u * w + lane >= rem) jl[w] = jc0;
     }
     uint32_t d[kWinW];
-    uint64_t M[kWinW][kWide];  // the entry's mask per block
     uint2 rc[kWinW];
-#pragma unroll
-    for (int w = 0; w < kWinW; ++w) {
-        d[w] = a.qd[jl[w]];
-        const ulonglong2* mp = reinterpret_cast<const ulonglong2*>(a.qmask + (size_t)jl[w] * kWide);
-#pragma unroll
-        for (uint32_t b = 0; b < kWide; b += 2) {
-            const ulonglong2 x = mp[b / 2];
-            M[w][b] = x.x;
-            M[w][b + 1] = x.y;
-        }
-    }
-#pragma unroll
-    for (int w = 0; w < kWinW; ++w) {
-        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
-        rc[w] = ld_stream(&a.rec[t0l + i + d[w]]);
-    }
     uint64_t live[kVW];
+    if constexpr (kWide == 2) {
+        ulonglong2 M[kWinW];  // {mask of block 0, mask of block 1}
 #pragma unroll
-    for (int w = 0; w < kWinW; ++w) {
-        const ulonglong2* p = &a.VN[(size_t)rc[w].x * kWide];
+        for (int w = 0; w < kWinW; ++w) {
+            d[w] = a.qd[jl[w]];
+            M[w] = reinterpret_cast<const ulonglong2*>(a.qmask)[jl[w]];
+        }
 #pragma unroll
-        for (uint32_t b = 0; b < kWide; ++b) {
-            const ulonglong2 vn = ld_keep(p + b);
-            live[w * kWide + b] = (!kWhole && 32u * w + lane >= rem) ? 0ull : M[w][b] & ~(vn.x | vn.y);
+        for (int w = 0; w < kWinW; ++w) {
+            const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+            rc[w] = ld_stream(&a.rec[t0l + i + d[w]]);
+        }
+#pragma unroll
+        for (int w = 0; w < kWinW; ++w) {
+            const ulonglong2* p = &a.VN[(size_t)rc[w].x * kWide];
+            const ulonglong2 v0 = ld_keep(p), v1 = ld_keep(p + 1);
+            live[w * kWide + 0] = M[w].x & ~(v0.x | v0.y);
+            live[w * kWide + 1] = M[w].y & ~(v1.x | v1.y);
+            if (!kWhole && 32u * w + lane >= rem) live[w * kWide + 0] = live[w * kWide + 1] = 0;
+        }
+    } else {
+        uint64_t M[kWinW][kWide];  // the entry's mask per block
+#pragma unroll
+        for (int w = 0; w < kWinW; ++w) {
+            d[w] = a.qd[jl[w]];
+            const ulonglong2* mp = reinterpret_cast<const ulonglong2*>(a.qmask + (size_t)jl[w] * kWide);
+#pragma unroll
+            for (uint32_t b = 0; b < kWide; b += 2) {
+                const ulonglong2 x = mp[b / 2];
+                M[w][b] = x.x;
+                M[w][b + 1] = x.y;
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < kWinW; ++w) {
+            const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+            rc[w] = ld_stream(&a.rec[t0l + i + d[w]]);
+        }
+#pragma unroll
+        for (int w = 0; w < kWinW; ++w) {
+            const ulonglong2* p = &a.VN[(size_t)rc[w].x * kWide];
+#pragma unroll
+            for (uint32_t b = 0; b < kWide; ++b) {
+                const ulonglong2 vn = ld_keep(p + b);
+                live[w * kWide + b] = (!kWhole && 32u * w + lane >= rem) ? 0ull : M[w][b] & ~(vn.x | vn.y);
+            }
         }
     }
     uint32_t c[kVW], tot = 0;
@@ -920,9 +947,10 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
 #pragma unroll
         for (int q = 0; q < kVW; ++q) { W.pass[q][lane] = 0; W.live[q][lane] = live[q]; }
         W.excl[lane] = incl - tot;
-        uint32_t cm = 0, run = 0;
+        CumW cm = 0;
+        uint32_t run = 0;
 #pragma unroll
-        for (int q = 0; q < kVW - 1; ++q) { run += c[q]; cm |= run << (8 * q); }  // <= 192 per byte
+        for (int q = 0; q < kVW - 1; ++q) { run += c[q]; cm |= (CumW)run << (kCumBits * q); }
         W.cum[lane] = cm;
         __syncwarp();
         for (uint32_t b = 0; b < ntask; b += 32) {
@@ -933,11 +961,11 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
                 for (int step = 16; step > 0; step >>= 1)
                     if (W.excl[o + step] <= k) o += step;
                 uint32_t r = k - W.excl[o];
-                const uint32_t cmo = W.cum[o];
+                const CumW cmo = W.cum[o];
                 uint32_t q = 0, base = 0;
 #pragma unroll
                 for (int qq = 0; qq < kVW - 1; ++qq) {
-                    const uint32_t pq = (cmo >> (8 * qq)) & 0xffu;
+                    const uint32_t pq = (uint32_t)(cmo >> (kCumBits * qq)) & ((1u << kCumBits) - 1u);
                     if (r >= pq) { q = qq + 1; base = pq; }
                 }
                 r -= base;
@@ -969,9 +997,14 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
 #pragma unroll
     for (int w = 0; w < kWinW; ++w) {
         first[w] = false;
-        bool fw = false;
+        bool fw;
+        if constexpr (kWide == 2) {
+            fw = old[w * kWide] == 0 || old[w * kWide + 1] == 0;
+        } else {
+            fw = false;
 #pragma unroll
-        for (uint32_t b = 0; b < kWide; ++b) fw |= old[w * kWide + b] == 0;
+            for (uint32_t b = 0; b < kWide; ++b) fw |= old[w * kWide + b] == 0;
+        }
         if (fw && atomicOr(&a.vflag[rc[w].x], 1u) == 0) first[w] = true;
         nf += first[w];
     }
