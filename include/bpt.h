@@ -131,6 +131,9 @@ typedef struct {
  * frontier, so each reverse edge of a frontier vertex is read once for 128 samples. Same RRR
  * sets (coins are keyed by the global sample id); E_phys counts the 128-sample groups. */
 #define BPT_FLAG_WIDE 2u
+/* LT samples are drawn as one reverse walk per thread (the RRR store is each sample's visited
+ * set; same coins and sets as the fused level-synchronous form, which the environment variable
+ * BPT_LT_FUSED=1 selects); batch_groups and BPT_FLAG_PROFILE do not apply to the walks. */
 
 BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
                       void* stream, bpt_samples** out);
@@ -140,12 +143,12 @@ BPT_API bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t t
 typedef struct {
     uint64_t theta, seed, s0, s1;          /* this rank owns global samples [s0, s1) */
     uint32_t colors, model, world, rank;
-    uint32_t n, batch_groups, batches, levels_max;  /* levels_max: deepest batch */
+    uint32_t n, batch_groups, batches, levels_max;  /* levels_max: deepest batch (LT: longest walk) */
     uint64_t e_phys;        /* IC: reverse-edge records read by the fused expansion;
                                LT: (vertex, colour) expansions = sum |RR_s| */
     uint64_t e_logical;     /* IC: sum_s sum_{v in RR_s} indeg(v) (unfused reads); LT: sum |RR_s| */
     uint64_t members;       /* sum_s |RR_s| over this rank's samples */
-    uint64_t levels_total;  /* sum over batches of levels traversed */
+    uint64_t levels_total;  /* sum over batches of levels traversed (LT walks: the longest walk) */
     uint64_t frontier_entries; /* (vertex, slice) frontier entries expanded */
     uint64_t coins;         /* coin evaluations (schedule-dependent, informational) */
     uint64_t atomics;       /* atomicOr merges issued (schedule-dependent) */
@@ -153,7 +156,8 @@ typedef struct {
     uint64_t kernel_launches;
     uint64_t expand_launches;
     double ms_total;        /* host wall time of bpt_sample */
-    double ms_expand;       /* sum of CUDA-event times of expansion launches (BPT_FLAG_PROFILE) */
+    double ms_expand;       /* expansion time: CUDA events per launch (BPT_FLAG_PROFILE), else device
+                               %globaltimer spans of the launches; LT walks: the walk kernel */
     double expand_bytes;    /* algorithmic bytes moved by expansion launches */
 } bpt_samples_info;
 
