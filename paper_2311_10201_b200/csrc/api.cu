@@ -227,7 +227,11 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
             BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
             DevBuf totals(16);
             BPT_CUDA(cudaMemsetAsync(totals.p, 0, 16, st));
-            cudaEvent_t e0, e1;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            struct EvPair {
+                cudaEvent_t* a; cudaEvent_t* b;
+                ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+            } ev_guard{&e0, &e1};
             BPT_CUDA(cudaEventCreate(&e0));
             BPT_CUDA(cudaEventCreate(&e1));
             BPT_CUDA(cudaEventRecord(e0, st));
@@ -240,8 +244,6 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
             BPT_CUDA(cudaStreamSynchronize(st));
             float ms = 0;
             BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            BPT_CUDA(cudaEventDestroy(e0));
-            BPT_CUDA(cudaEventDestroy(e1));
             // member lists for the selection's decrement, by re-walking (cheaper than a pass over the
             // dense store); bpt_select_seeds finds them built
             {
