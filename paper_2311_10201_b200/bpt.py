@@ -27,6 +27,7 @@ BPT_OK, BPT_EINVAL, BPT_ENOMEM, BPT_ECUDA, BPT_ENCCL, BPT_ESTATE = 0, -1, -2, -3
 IC, LT = 0, 1
 FLAG_PROFILE = 1
 FLAG_WIDE = 2  # 128 colours per frontier entry (IC, colors=64, batch_groups=0)
+FLAG_SPARSE = 4  # LT: sorted member lists instead of the dense store
 _STATUS = {0: "BPT_OK", -1: "BPT_EINVAL", -2: "BPT_ENOMEM", -3: "BPT_ECUDA", -4: "BPT_ENCCL", -5: "BPT_ESTATE"}
 
 _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
@@ -289,8 +290,8 @@ class Graph:
 
     def sample(self, theta: int, colors: int = 64, seed: int = 0, stream=None, batch_groups: int = 0,
                poll_levels: int = 0, profile: bool = False, shard: tuple[int, int] | None = None,
-               wide: bool = False) -> "Samples":
-        flags = (FLAG_PROFILE if profile else 0) | (FLAG_WIDE if wide else 0)
+               wide: bool = False, sparse: bool = False) -> "Samples":
+        flags = (FLAG_PROFILE if profile else 0) | (FLAG_WIDE if wide else 0) | (FLAG_SPARSE if sparse else 0)
         h = bpt_sample(self._h, self.model, theta, colors, seed, stream, batch_groups, poll_levels, flags, shard)
         return Samples(self, h)
 

@@ -213,11 +213,72 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         BPT_CUDA(cudaStreamSynchronize(st));
         return;
     }
-    S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
     const uint64_t nlocal = S.s1 - S.s0;
     S.sizes.alloc(nlocal * 4);
     S.digests.alloc(nlocal * 8);
     BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
+
+    // ---- LT sparse store (BPT_FLAG_SPARSE): walks with per-thread visited sets, sorted member
+    //      lists as the store -- no n x blocks bitmap
+    if (S.model == BPT_LT && (opt.flags & BPT_FLAG_SPARSE)) {
+        DevBuf totals(24), err(4);
+        BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
+        BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+        const uint32_t ks = stream_key(S.seed, kTagStart), kl = stream_key(S.seed, kTagLT);
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        struct EvPair {
+            cudaEvent_t* a; cudaEvent_t* b;
+            ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+        } ev_guard{&e0, &e1};
+        BPT_CUDA(cudaEventCreate(&e0));
+        BPT_CUDA(cudaEventCreate(&e1));
+        BPT_CUDA(cudaEventRecord(e0, st));
+        launch_walk_lt_sparse(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, ks, kl,
+                              S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
+        BPT_CUDA(cudaEventRecord(e1, st));
+        unsigned long long tot[3] = {0, 0, 0};
+        BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
+        if (tot[2]) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
+                                     "BPT_FLAG_SPARSE");
+        float ms = 0;
+        BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        std::vector<uint32_t> sz(nlocal);
+        BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> off(nlocal + 1, 0);
+        for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
+        S.list_off.alloc((nlocal + 1) * 8);
+        S.list_mem.alloc(off[nlocal] * 4 + 4);
+        BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
+        launch_walk_lt_lists(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, ks, kl,
+                             S.sizes.as<uint32_t>(), S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), st);
+        launch_sort_lists(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal, err.as<uint32_t>(), st);
+        uint32_t h_err = 0;
+        BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
+        if (h_err) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's list sort; sample without "
+                                    "BPT_FLAG_SPARSE");
+        S.sparse = true;
+        S.lists_built = S.lists_ok = true;
+        bpt_samples_info& I = S.info;
+        I.members = I.frontier_entries = I.coins = I.atomics = tot[0];
+        I.e_phys = I.e_logical = tot[0];
+        I.levels_total = I.levels_max = tot[1];
+        I.batch_groups = (uint32_t)S.blocks;
+        I.batches = 1;
+        I.store_bytes = S.list_mem.bytes + S.list_off.bytes;
+        I.ms_expand = ms;
+        I.expand_launches = 1;
+        I.expand_bytes = 24.0 * (double)tot[0];
+        S.level_rows.clear();
+        I.kernel_launches = g_launches - launches0;
+        I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+        if (getenv("BPT_TRACE"))
+            fprintf(stderr, "[bpt] sample (LT sparse walks): %llu members, longest %llu, walks %.2f ms, total %.2f ms\n",
+                    tot[0], tot[1], ms, I.ms_total);
+        return;
+    }
+    S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
 
     // ---- LT: one reverse walk per thread (k_sample.cu "LT reverse walks"); BPT_LT_FUSED=1 runs
     //      the level-synchronous fused loop instead (same sets)
@@ -726,7 +787,11 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         if (capacity < total)
             fail(BPT_ENOMEM, "members capacity " + std::to_string(capacity) + " < required " + std::to_string(total));
         if (total && !members) fail(BPT_EINVAL, "members is NULL");
-        if (total) {
+        if (total && S.sparse) {  // the store is the sorted lists: one contiguous slice
+            uint64_t b = 0;
+            BPT_CUDA(cudaMemcpy(&b, S.list_off.as<uint64_t>() + (first - S.s0), 8, cudaMemcpyDeviceToHost));
+            BPT_CUDA(cudaMemcpy(members, S.list_mem.as<uint32_t>() + b, total * 4, cudaMemcpyDefault));
+        } else if (total) {
             DevBuf tmp;
             uint32_t* dm = members;
             if (!is_device_ptr(members)) { tmp.alloc(total * 4); dm = tmp.as<uint32_t>(); }

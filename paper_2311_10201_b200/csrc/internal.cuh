@@ -119,6 +119,10 @@ struct Samples {
     bool lists_built = false, lists_ok = false;
     bool digests_ready = false;
     DevBuf list_off, list_mem;
+    // sparse LT store (BPT_FLAG_SPARSE): no dense store; the RRR sets ARE the sorted member
+    // lists (list_off, list_mem); the selection uses a vertex -> samples index built on demand
+    bool sparse = false;
+    DevBuf inv_off, inv_s;
 };
 
 // ------------------------------------------------------------------ launchers
@@ -215,6 +219,13 @@ bool level_loop_persistent(const BatchArgs& a);
 void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
                     uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0, unsigned long long* totals,
                     cudaStream_t st);
+// LT sparse store: walks with a per-thread visited hash set (no dense store); sizes, count0,
+// totals[0..1] as launch_walk_lt, totals[2] = 1 if a walk outgrew the hash set
+void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                           uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
+                           unsigned long long* totals, cudaStream_t st);
+// sort every list ascending in place (one block per list of <= 4096 members; longer lists set *err)
+void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, uint32_t* err, cudaStream_t st);
 // LT: re-walk every local sample and write its members at off[i] (unsorted; for the selection)
 void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
                           uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,

@@ -1157,6 +1157,93 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
     }
 }
 
+// Sparse LT store: the visited set of a walk is a per-thread open-addressing hash set in local
+// memory (2,048 slots; a walk longer than 1,536 vertices is reported, the dense store handles
+// those), so no dense n x blocks bitmap exists at all.
+constexpr uint32_t kWalkHash = 2048, kWalkMax = 1536;
+
+__global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32_t* __restrict__ roff,
+                                                        const uint2* __restrict__ rec, uint64_t s0, uint64_t nlocal,
+                                                        uint32_t k_start, uint32_t k_lt,
+                                                        uint32_t* __restrict__ sizes, uint32_t* __restrict__ count0,
+                                                        unsigned long long* __restrict__ totals) {
+    uint32_t ht[kWalkHash];
+    unsigned long long members = 0;
+    uint32_t longest = 0, too_long = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nlocal; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = s0 + i;
+#pragma unroll 8
+        for (uint32_t h = 0; h < kWalkHash; ++h) ht[h] = ~0u;
+        auto insert = [&](uint32_t u) -> bool {  // false if u was already in the set
+            uint32_t h = (u * 0x9E3779B1u) >> 21;
+            while (true) {
+                const uint32_t x = ht[h];
+                if (x == u) return false;
+                if (x == ~0u) { ht[h] = u; return true; }
+                h = (h + 1) & (kWalkHash - 1);
+            }
+        };
+        const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), k_start);
+        uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
+        insert(v);
+        atomicAdd(&count0[v], 1u);
+        uint32_t size = 1, u = 0;
+        while (lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
+            if (!insert(u)) break;  // already in RR_s
+            atomicAdd(&count0[u], 1u);
+            ++size;
+            v = u;
+            if (size >= kWalkMax) { too_long = 1; break; }
+        }
+        sizes[i] = size;
+        members += size;
+        longest = max(longest, size);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        members += __shfl_xor_sync(kFull, members, d);
+        longest = max(longest, __shfl_xor_sync(kFull, longest, d));
+        too_long |= __shfl_xor_sync(kFull, too_long, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (members) atomicAdd(&totals[0], members);
+        if (longest) atomicMax(&totals[1], (unsigned long long)longest);
+        if (too_long) atomicMax(&totals[2], 1ull);
+    }
+}
+
+// Bitonic sort of one member list per block in shared memory (padded to a power of two).
+constexpr uint32_t kSortMax = 4096;
+__global__ void __launch_bounds__(256) k_sort_lists(const uint64_t* __restrict__ off, uint32_t* __restrict__ members,
+                                                    uint64_t nlists, uint32_t* __restrict__ err) {
+    __shared__ uint32_t sh[kSortMax];
+    for (uint64_t l = blockIdx.x; l < nlists; l += gridDim.x) {
+        const uint64_t b = off[l], len = off[l + 1] - b;
+        if (len <= 1) continue;
+        if (len > kSortMax) {
+            if (threadIdx.x == 0) *err = 1;
+            continue;
+        }
+        uint32_t P = 1;
+        while (P < len) P <<= 1;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sh[i] = i < len ? members[b + i] : ~0u;
+        __syncthreads();
+        for (uint32_t k = 2; k <= P; k <<= 1)
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                    const uint32_t ix = i ^ j;
+                    if (ix > i) {
+                        const uint32_t x = sh[i], y = sh[ix];
+                        if (((i & k) == 0) == (x > y)) { sh[i] = y; sh[ix] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) members[b + i] = sh[i];
+    }
+}
+
 // LT (reading C-6): work items are (entry, colour) pairs. For colour c at v: r = coinLT(s_c, v)
 // >> 1, chosen in-edge j = first with cum[j] > r (binary search of the row, rows are
 // cumulative thresholds); none if r >= row sum. If u = src[j] has not been visited by c,
@@ -1359,6 +1446,23 @@ void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uin
     k_walk_lt<<<grid ? grid : 1, 256, 0, st>>>(store, n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt");
+}
+
+void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+                           uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
+                           unsigned long long* totals, cudaStream_t st) {
+    const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
+    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals);
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_sparse");
+}
+
+void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, uint32_t* err, cudaStream_t st) {
+    const unsigned grid = (unsigned)umin64(nlists, (uint64_t)num_sms() * 16);
+    if (!grid) return;
+    k_sort_lists<<<grid, 256, 0, st>>>(off, members, nlists, err);
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_sort_lists");
 }
 
 void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,

@@ -120,6 +120,34 @@ __global__ void k_lists_scatter(const uint64_t* __restrict__ store, uint32_t n, 
     }
 }
 
+// sparse store: vertex -> local samples index (inv_off = exclusive scan of the occurrence counts)
+__global__ void k_inv_scatter(const uint64_t* __restrict__ off, const uint32_t* __restrict__ members, uint64_t nlists,
+                              const uint64_t* __restrict__ inv_off, uint32_t* __restrict__ cursor,
+                              uint32_t* __restrict__ inv_s) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < nlists; l += (uint64_t)gridDim.x * blockDim.x)
+        for (uint64_t j = off[l]; j < off[l + 1]; ++j) {
+            const uint32_t w = members[j];
+            inv_s[inv_off[w] + atomicAdd(&cursor[w], 1u)] = (uint32_t)l;
+        }
+}
+
+// sparse store, one round: the samples containing v* that are not covered yet become covered
+// and leave the counts of all their members
+__global__ void k_cover_sparse(const unsigned long long* __restrict__ key, const uint64_t* __restrict__ inv_off,
+                               const uint32_t* __restrict__ inv_s, const uint64_t* __restrict__ off,
+                               const uint32_t* __restrict__ members, uint32_t* __restrict__ covered,
+                               uint8_t* __restrict__ selected, uint32_t* __restrict__ count) {
+    const uint32_t vstar = ~(uint32_t)(*key);
+    if (blockIdx.x == 0 && threadIdx.x == 0) selected[vstar] = 1;
+    if (*key == 0) return;  // no gain left on any rank's shard: nothing to cover
+    const uint64_t b = inv_off[vstar], e = inv_off[vstar + 1];
+    for (uint64_t j = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t l = inv_s[j];
+        if (atomicExch(&covered[l], 1u)) continue;
+        for (uint64_t t = off[l]; t < off[l + 1]; ++t) atomicSub(&count[members[t]], 1u);
+    }
+}
+
 }  // namespace
 
 // Member lists of all local samples, if they are small enough to keep (sparse stores); cached.
@@ -173,6 +201,30 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     const bool lists = build_lists(S, st);
+    DevBuf covered(S.sparse ? (S.s1 - S.s0) * 4 + 4 : 4);
+    if (S.sparse) {
+        BPT_CUDA(cudaMemsetAsync(covered.p, 0, covered.bytes, st));
+        if (!S.inv_off.p) {  // vertex -> samples index, built once per handle
+            Samples& M = const_cast<Samples&>(S);
+            std::vector<uint32_t> cnt(n);
+            BPT_CUDA(cudaMemcpy(cnt.data(), S.count0.p, (uint64_t)n * 4, cudaMemcpyDeviceToHost));
+            std::vector<uint64_t> io(n + 1, 0);
+            for (uint32_t v = 0; v < n; ++v) io[v + 1] = io[v] + cnt[v];
+            M.inv_off.alloc((uint64_t)(n + 1) * 8);
+            M.inv_s.alloc(io[n] * 4 + 4);
+            BPT_CUDA(cudaMemcpyAsync(M.inv_off.p, io.data(), (uint64_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));
+            DevBuf cursor((uint64_t)n * 4);
+            BPT_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes, st));
+            const uint64_t nl = S.s1 - S.s0;
+            const unsigned g = (unsigned)umin64((nl + 255) / 256, (uint64_t)num_sms() * 8);
+            if (g) k_inv_scatter<<<g, 256, 0, st>>>(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nl,
+                                                    M.inv_off.as<uint64_t>(), cursor.as<uint32_t>(),
+                                                    M.inv_s.as<uint32_t>());
+            count_launch();
+            ::bpt::check_cuda(cudaGetLastError(), "launch k_inv_scatter");
+            BPT_CUDA(cudaStreamSynchronize(st));
+        }
+    }
     const auto t1 = clk::now();
     for (uint32_t r = 0; r < k; ++r) {
         unsigned long long* key = keys.as<unsigned long long>() + r;
@@ -186,6 +238,15 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
             k_argmax<<<vgrid, kSelThreads, 0, st>>>(count.as<uint32_t>(), n, 0, n, sel.as<uint8_t>(), key,
                                                     nlist.as<uint32_t>());
             count_launch();
+        }
+        if (S.sparse) {
+            k_cover_sparse<<<num_sms() * 4, 256, 0, st>>>(key, S.inv_off.as<uint64_t>(), S.inv_s.as<uint32_t>(),
+                                                           S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(),
+                                                           covered.as<uint32_t>(), sel.as<uint8_t>(),
+                                                           count.as<uint32_t>());
+            count_launch();
+            ::bpt::check_cuda(cudaGetLastError(), "launch k_cover_sparse");
+            continue;
         }
         k_cover<<<ggrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blocks, key, cov.as<uint64_t>(), sel.as<uint8_t>(),
                                        nlist.as<uint32_t>(), list.as<uint32_t>(), newm.as<uint64_t>());

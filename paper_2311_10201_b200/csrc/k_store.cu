@@ -222,8 +222,28 @@ static dim3 finalize_grid(uint32_t n, uint32_t slots_max, uint64_t* chunk_out) {
     return dim3((unsigned)ranges, slots_max);
 }
 
+namespace {
+// sparse store: digest of list l = sum of splitmix64 over its members
+__global__ void k_digests_lists(const uint64_t* __restrict__ off, const uint32_t* __restrict__ members, uint64_t nlists,
+                                unsigned long long* __restrict__ digests) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < nlists; l += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long d = 0;
+        for (uint64_t j = off[l]; j < off[l + 1]; ++j) d += digest_mix(members[j]);
+        digests[l] = d;
+    }
+}
+}  // namespace
+
 void compute_digests(const Samples& S, cudaStream_t st) {
     const uint64_t nlocal = S.s1 - S.s0;
+    if (S.sparse) {
+        const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
+        if (grid) k_digests_lists<<<grid, 256, 0, st>>>(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal,
+                                                        S.digests.as<unsigned long long>());
+        count_launch();
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_digests_lists");
+        return;
+    }
     BPT_CUDA(cudaMemsetAsync(S.digests.p, 0, nlocal * 8, st));
     uint64_t ranges = (uint64_t)num_sms() * 4 / umax64(S.blocks, 1);
     if (ranges < 1) ranges = 1;

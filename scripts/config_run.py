@@ -25,6 +25,8 @@ ap.add_argument("--colors", type=int, default=0)
 ap.add_argument("--check", type=int, default=256, help="samples checked against the oracle")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--k", type=int, default=0)
+ap.add_argument("--sparse", action="store_true", help="LT: sorted member lists instead of the dense store")
+ap.add_argument("--wide", action="store_true", help="IC: 128 colours per frontier entry")
 a = ap.parse_args()
 cfg = graphgen.CONFIGS[a.config]
 theta = a.theta or cfg.theta
@@ -43,7 +45,7 @@ for r in range(a.reps):
         s.close()
     torch.cuda.synchronize()
     t = time.perf_counter()
-    s = g.sample(theta, colors=colors, seed=cfg.seed)
+    s = g.sample(theta, colors=colors, seed=cfg.seed, sparse=a.sparse, wide=a.wide)
     times.append(time.perf_counter() - t)
     t = time.perf_counter()
     seeds, gains, sigma = s.select_seeds(k)
@@ -67,6 +69,7 @@ for j in range(0, len(ids), max(1, len(ids) // 16)):
 best = min(times)
 print(json.dumps({
     "config": cfg.name, "theta": theta, "colors": colors, "model": cfg.model, "n": cfg.n, "m": cfg.m,
+    "mode": "sparse lists" if a.sparse else ("wide fusion" if a.wide else "default"),
     "gen_s": gen_s, "sample_s": times, "select_s": sel_times, "rrr_sets_per_s": theta / best,
     "e_phys": info["e_phys"], "e_logical": info["e_logical"], "members": info["members"],
     "edges_per_s": info["e_phys"] / best, "levels_total": info["levels_total"], "levels_max": info["levels_max"],

@@ -36,7 +36,8 @@ def test_header_constants_match_binding():
     import paper_2311_10201_b200 as bpt
     hdr = open(os.path.join(ROOT, "include", "bpt.h")).read()
     defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z]+) (\w+)", hdr)}
-    assert defs == {"BPT_FLAG_PROFILE": bpt.FLAG_PROFILE, "BPT_FLAG_WIDE": bpt.FLAG_WIDE}
+    assert defs == {"BPT_FLAG_PROFILE": bpt.FLAG_PROFILE, "BPT_FLAG_WIDE": bpt.FLAG_WIDE,
+                    "BPT_FLAG_SPARSE": bpt.FLAG_SPARSE}
     enums = dict((k, int(v)) for k, v in re.findall(r"(BPT_E[A-Z]+|BPT_OK)\s*=\s*(-?\d+)", hdr))
     for k in ("BPT_OK", "BPT_EINVAL", "BPT_ENOMEM", "BPT_ECUDA", "BPT_ENCCL", "BPT_ESTATE"):
         assert enums[k] == getattr(bpt, k)

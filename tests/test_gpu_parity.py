@@ -337,6 +337,31 @@ def test_wide_fusion(bpt, which):
         s.close()
 
 
+def test_lt_sparse_store(bpt):
+    """BPT_FLAG_SPARSE (LT): the RRR sets kept as sorted member lists, no dense store; sizes,
+    digests, extraction (ragged ranges), occurrences and seeds/gains identical to the oracle."""
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 13, theta=4096 + 64 + 5)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, sparse=True)
+    check_full(bpt, s, ref, cfg.theta)
+    off, mem = s.extract(77, 300)
+    o0 = ref["offsets"]
+    assert np.array_equal(mem, ref["members"][o0[77]:o0[377]])
+    occ = np.bincount(ref["members"].astype(np.int64), minlength=cfg.n)
+    assert np.array_equal(s.occurrences()[:cfg.n], occ)
+    seeds, gains, sigma = s.select_seeds(cfg.k)
+    assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+    assert sigma == oracle.sigma_hat(cfg.n, int(ref["gains"].sum()), cfg.theta)
+    info = s.info
+    assert info["members"] == info["e_phys"] == int(ref["sizes"].sum())
+    assert info["store_bytes"] < (cfg.theta // 64 + 1) * cfg.n * 8 // 4  # lists, not the bitmap
+    seeds2, gains2, _ = s.select_seeds(cfg.k)  # the selection does not mutate the store
+    assert np.array_equal(seeds2, seeds) and np.array_equal(gains2, gains)
+    s.close()
+
+
 # ------------------------------------------------------------------ C2 / C5 shape, scaled
 
 @pytest.fixture(scope="module")
