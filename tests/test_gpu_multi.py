@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q):
+def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -46,7 +46,7 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q):
     dist.broadcast_object_list(uid, src=0)
     comm = bpt.Comm(world, rank, rank, uid[0])
     g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.IC if cfg.model == "IC" else bpt.LT, comm=comm)
-    s = g.sample(theta, colors=64, seed=cfg.seed)
+    s = g.sample(theta, colors=64, seed=cfg.seed, **(kw or {}))
     sizes = s.sizes(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint32)
     digests = s.digests(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint64)
     seeds, gains, sigma = s.select_seeds(cfg.k)
@@ -57,18 +57,24 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q):
     dist.destroy_process_group()
 
 
+MODES = {"ic": ("C2", 1 << 14, {}), "ic_wide": ("C2", 1 << 14, {"wide": True}),
+         "lt": ("C3", 1 << 13, {}), "lt_sparse": ("C3", 1 << 13, {"sparse": True})}
+
+
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_selection_parity(cuda_required, world):
+@pytest.mark.parametrize("mode", list(MODES))
+def test_multi_gpu_selection_parity(cuda_required, world, mode):
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
-    cfg = graphgen.scaled(graphgen.CONFIGS["C2"], 1 << 14, theta=1024 + 64 * 3)
+    name, n_scaled, kw = MODES[mode]
+    cfg = graphgen.scaled(graphgen.CONFIGS[name], n_scaled, theta=1024 + 64 * 3)
     theta = cfg.theta
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_rank_main, args=(r, world, port, "C2", 1 << 14, theta, q)) for r in range(world)]
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, name, n_scaled, theta, q, kw)) for r in range(world)]
     for p in ps:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda t: t[0])
@@ -76,7 +82,7 @@ def test_multi_gpu_selection_parity(cuda_required, world):
         p.join(timeout=120)
         assert p.exitcode == 0
     row_ptr, col, thr = graphgen.make_graph(cfg)
-    g = oracle.Graph(row_ptr, col, w_q31=thr)
+    g = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.IC if cfg.model == "IC" else oracle.LT)
     sizes, digests, _, off, mem = g.sample_many(cfg.seed, np.arange(theta, dtype=np.uint64), members=True)
     seeds, gains = oracle.greedy(cfg.n, off, mem, cfg.k)
     sigma = oracle.sigma_hat(cfg.n, int(gains.sum()), theta)
