@@ -131,10 +131,11 @@ typedef struct {
  * frontier, so each reverse edge of a frontier vertex is read once for 128 samples. Same RRR
  * sets (coins are keyed by the global sample id); E_phys counts the 128-sample groups. */
 #define BPT_FLAG_WIDE 2u
-/* LT only: keep the RRR sets as sorted member lists instead of the dense n x blocks bitmap
- * (SURVEY A5 "compressed rows": C3 ~0.1 GB instead of 100 GB). Walks keep their visited set in
- * a per-thread hash set; a walk longer than 1,536 vertices makes the call fail with ENOMEM
- * (sample without the flag). Sizes, digests, extraction and selection read the lists. */
+/* LT only: REQUIRE the sparse store -- the RRR sets kept as sorted member lists instead of the
+ * dense n x blocks bitmap (SURVEY A5 "compressed rows": C3 ~0.1 GB instead of 100 GB). LT uses
+ * it by default too, falling back to the dense store when a walk outgrows the per-thread
+ * visited set (1,536 vertices); with this flag that case fails with ENOMEM instead. Sizes,
+ * digests, extraction and selection read whichever form the handle holds. */
 #define BPT_FLAG_SPARSE 4u
 /* LT samples are drawn as one reverse walk per thread (the RRR store is each sample's visited
  * set; same coins and sets as the fused level-synchronous form, which the environment variable

@@ -220,27 +220,45 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
 
     // ---- LT sparse store (BPT_FLAG_SPARSE): walks with per-thread visited sets, sorted member
     //      lists as the store -- no n x blocks bitmap
-    if (S.model == BPT_LT && (opt.flags & BPT_FLAG_SPARSE)) {
-        DevBuf totals(24), err(4);
+    // LT default: the sparse store (transparent to every consumer); a walk longer than the
+    // per-thread visited set falls back to the dense-store walks unless BPT_FLAG_SPARSE demands it.
+    // BPT_LT_DENSE=1 / BPT_LT_FUSED=1 select the dense forms.
+    const char* lt_dense = getenv("BPT_LT_DENSE");
+    const char* lt_fused = getenv("BPT_LT_FUSED");
+    const bool lt_sparse = S.model == BPT_LT && ((opt.flags & BPT_FLAG_SPARSE) ||
+                                                 (!(lt_dense && lt_dense[0] == '1') && !(lt_fused && lt_fused[0] == '1')));
+    bool sparse_overflow = false;
+    DevBuf totals, err;
+    unsigned long long tot[3] = {0, 0, 0};
+    const uint32_t ks = stream_key(S.seed, kTagStart), kl = stream_key(S.seed, kTagLT);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    struct EvPair {
+        cudaEvent_t* a; cudaEvent_t* b;
+        ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+    } ev_guard{&e0, &e1};
+    if (lt_sparse) {
+        totals.alloc(24);
+        err.alloc(4);
         BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
         BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
-        const uint32_t ks = stream_key(S.seed, kTagStart), kl = stream_key(S.seed, kTagLT);
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        struct EvPair {
-            cudaEvent_t* a; cudaEvent_t* b;
-            ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
-        } ev_guard{&e0, &e1};
         BPT_CUDA(cudaEventCreate(&e0));
         BPT_CUDA(cudaEventCreate(&e1));
         BPT_CUDA(cudaEventRecord(e0, st));
         launch_walk_lt_sparse(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, ks, kl,
                               S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
         BPT_CUDA(cudaEventRecord(e1, st));
-        unsigned long long tot[3] = {0, 0, 0};
         BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
         BPT_CUDA(cudaStreamSynchronize(st));
-        if (tot[2]) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
-                                     "BPT_FLAG_SPARSE");
+        if (tot[2] && (opt.flags & BPT_FLAG_SPARSE))
+            fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
+                             "BPT_FLAG_SPARSE");
+        sparse_overflow = tot[2] != 0;
+        if (sparse_overflow) {  // fall back to the dense-store walks: undo the counts of this attempt
+            BPT_CUDA(cudaMemsetAsync(S.count0.p, 0, (size_t)S.n_pad * 4, st));
+            BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
+        }
+    }
+    if (lt_sparse && !sparse_overflow) {
         float ms = 0;
         BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         std::vector<uint32_t> sz(nlocal);

@@ -286,7 +286,8 @@ def test_level_loop_variants(bpt, monkeypatch, model):
         ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
         variants = [{"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "0"}, {"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "1"},
-                    {"BPT_LT_FUSED": "0"}]
+                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "0"},   # walks, sparse store (default)
+                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "1"}]   # walks, dense store
     infos = []
     for env in variants:
         for k, v in env.items():
@@ -299,14 +300,18 @@ def test_level_loop_variants(bpt, monkeypatch, model):
             assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
             info = s.info
             walker = model == "LT" and env.get("BPT_LT_FUSED") == "0"
+            if walker:
+                dense_bytes = (cfg.theta + 63) // 64 * cfg.n * 8
+                assert (info["store_bytes"] >= dense_bytes) == (env["BPT_LT_DENSE"] == "1")  # bitmap vs lists
             rows.append((info["e_phys"], info["e_logical"], info["members"]) if walker else
                         (colors, batch, info["e_phys"], info["e_logical"], info["members"], info["levels_total"]))
             s.close()
         infos.append(rows)
     assert infos[0] == infos[1]
     if model == "LT":  # walks: same work counters as the fused loop (E_phys = E_logical = sum |RR|)
-        assert [r[2:5] for r in infos[0]] == infos[2]
-        assert all(r[0] == r[1] == r[2] == int(ref["sizes"].sum()) for r in infos[2])
+        for walk in infos[2:]:
+            assert [r[2:5] for r in infos[0]] == walk
+            assert all(r[0] == r[1] == r[2] == int(ref["sizes"].sum()) for r in walk)
 
 
 @pytest.mark.parametrize("which", ["C1", "C2s"])
