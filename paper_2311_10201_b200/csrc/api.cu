@@ -197,6 +197,133 @@ bpt_status guarded(F&& f) {
 
 }  // namespace
 
+using clk_t = std::chrono::steady_clock;
+
+static bool env_is(const char* name, char c) {
+    const char* v = getenv(name);
+    return v && v[0] == c;
+}
+
+// timing of one walk launch (events released on every path)
+struct WalkTimer {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    explicit WalkTimer(cudaStream_t st) {
+        BPT_CUDA(cudaEventCreate(&e0));
+        BPT_CUDA(cudaEventCreate(&e1));
+        BPT_CUDA(cudaEventRecord(e0, st));
+    }
+    void stop(cudaStream_t st) { BPT_CUDA(cudaEventRecord(e1, st)); }
+    float ms() const {
+        float t = 0;
+        BPT_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        return t;
+    }
+    ~WalkTimer() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+// member lists of the local samples in walk order (a second walk of known length), offsets from
+// the sizes the first walk wrote
+static void lt_lists_by_rewalk(Samples& S, cudaStream_t st) {
+    const Graph& g = *S.g;
+    const uint64_t nlocal = S.s1 - S.s0;
+    std::vector<uint32_t> sz(nlocal);
+    BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> off(nlocal + 1, 0);
+    for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
+    S.list_off.alloc((nlocal + 1) * 8);
+    S.list_mem.alloc(off[nlocal] * 4 + 4);
+    BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
+    launch_walk_lt_lists(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, stream_key(S.seed, kTagStart),
+                         stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.list_off.as<uint64_t>(),
+                         S.list_mem.as<uint32_t>(), st);
+    S.lists_built = S.lists_ok = true;
+}
+
+static void lt_walk_info(Samples& S, const unsigned long long* tot, float ms, uint64_t launches0,
+                         clk_t::time_point t_begin, const char* label) {
+    bpt_samples_info& I = S.info;
+    I.members = I.frontier_entries = tot[0];
+    I.coins = tot[0];    // one coinLT draw per member vertex
+    I.atomics = tot[0];  // one visited-set insertion per member vertex
+    I.e_phys = I.e_logical = tot[0];  // (vertex, colour) expansions, SURVEY §8(d)
+    I.levels_total = I.levels_max = tot[1];
+    I.batch_groups = (uint32_t)S.blocks;
+    I.batches = 1;
+    I.store_bytes = S.sparse ? S.list_mem.bytes + S.list_off.bytes : S.store.bytes;
+    I.ms_expand = ms;
+    I.expand_launches = 1;
+    I.expand_bytes = 24.0 * (double)tot[0];  // row bounds 8 + chosen record 8 + visited RMW 8 per member
+    S.level_rows.clear();
+    I.kernel_launches = g_launches - launches0;
+    I.ms_total = std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count();
+    if (getenv("BPT_TRACE"))
+        fprintf(stderr, "[bpt] sample (%s): %llu members, longest %llu, walks %.2f ms, total %.2f ms\n", label, tot[0],
+                tot[1], ms, I.ms_total);
+}
+
+// LT, sparse store: walks with per-thread visited hash sets, sorted member lists as the store.
+// Returns false (counts undone) when a walk outgrew the visited set and the flag allows the dense
+// store instead.
+static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStream_t st, clk_t::time_point t_begin,
+                                uint64_t launches0) {
+    const Graph& g = *S.g;
+    const uint64_t nlocal = S.s1 - S.s0;
+    DevBuf totals(24), err(4);
+    BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
+    BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    WalkTimer tm(st);
+    launch_walk_lt_sparse(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, stream_key(S.seed, kTagStart),
+                          stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(),
+                          totals.as<unsigned long long>(), st);
+    tm.stop(st);
+    unsigned long long tot[3] = {0, 0, 0};
+    BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    if (tot[2]) {
+        if (opt.flags & BPT_FLAG_SPARSE)
+            fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
+                             "BPT_FLAG_SPARSE");
+        BPT_CUDA(cudaMemsetAsync(S.count0.p, 0, (size_t)S.n_pad * 4, st));  // undo this attempt
+        BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
+        return false;
+    }
+    lt_lists_by_rewalk(S, st);
+    launch_sort_lists(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal, err.as<uint32_t>(), st);
+    uint32_t h_err = 0;
+    BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    if (h_err) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's list sort; sample without "
+                                "BPT_FLAG_SPARSE");
+    S.sparse = true;
+    lt_walk_info(S, tot, tm.ms(), launches0, t_begin, "LT sparse walks");
+    return true;
+}
+
+// LT, dense store: sample s's bit in the RRR store is its visited set; member lists for the
+// selection's decrement by re-walking (cheaper than a pass over the dense store)
+static void run_lt_walks_dense(Samples& S, cudaStream_t st, clk_t::time_point t_begin, uint64_t launches0) {
+    const Graph& g = *S.g;
+    const uint64_t nlocal = S.s1 - S.s0;
+    S.store.alloc((size_t)S.blocks * g.n * 8);
+    BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
+    DevBuf totals(16);
+    BPT_CUDA(cudaMemsetAsync(totals.p, 0, 16, st));
+    WalkTimer tm(st);
+    launch_walk_lt(S.store.as<uint64_t>(), g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal,
+                   stream_key(S.seed, kTagStart), stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(),
+                   S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
+    tm.stop(st);
+    unsigned long long tot[2] = {0, 0};
+    BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 16, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    lt_lists_by_rewalk(S, st);
+    BPT_CUDA(cudaStreamSynchronize(st));
+    lt_walk_info(S, tot, tm.ms(), launches0, t_begin, "LT walks");
+}
+
 // ------------------------------------------------------------------ sampling driver
 static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st) {
     const Graph& g = *S.g;
@@ -218,149 +345,20 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     S.digests.alloc(nlocal * 8);
     BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
 
-    // ---- LT sparse store (BPT_FLAG_SPARSE): walks with per-thread visited sets, sorted member
-    //      lists as the store -- no n x blocks bitmap
-    // LT default: the sparse store (transparent to every consumer); a walk longer than the
-    // per-thread visited set falls back to the dense-store walks unless BPT_FLAG_SPARSE demands it.
-    // BPT_LT_DENSE=1 / BPT_LT_FUSED=1 select the dense forms.
-    const char* lt_dense = getenv("BPT_LT_DENSE");
-    const char* lt_fused = getenv("BPT_LT_FUSED");
-    const bool lt_sparse = S.model == BPT_LT && ((opt.flags & BPT_FLAG_SPARSE) ||
-                                                 (!(lt_dense && lt_dense[0] == '1') && !(lt_fused && lt_fused[0] == '1')));
-    bool sparse_overflow = false;
-    DevBuf totals, err;
-    unsigned long long tot[3] = {0, 0, 0};
-    const uint32_t ks = stream_key(S.seed, kTagStart), kl = stream_key(S.seed, kTagLT);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    struct EvPair {
-        cudaEvent_t* a; cudaEvent_t* b;
-        ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
-    } ev_guard{&e0, &e1};
-    if (lt_sparse) {
-        totals.alloc(24);
-        err.alloc(4);
-        BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
-        BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
-        BPT_CUDA(cudaEventCreate(&e0));
-        BPT_CUDA(cudaEventCreate(&e1));
-        BPT_CUDA(cudaEventRecord(e0, st));
-        launch_walk_lt_sparse(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, ks, kl,
-                              S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
-        BPT_CUDA(cudaEventRecord(e1, st));
-        BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
-        BPT_CUDA(cudaStreamSynchronize(st));
-        if (tot[2] && (opt.flags & BPT_FLAG_SPARSE))
-            fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
-                             "BPT_FLAG_SPARSE");
-        sparse_overflow = tot[2] != 0;
-        if (sparse_overflow) {  // fall back to the dense-store walks: undo the counts of this attempt
-            BPT_CUDA(cudaMemsetAsync(S.count0.p, 0, (size_t)S.n_pad * 4, st));
-            BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
-        }
-    }
-    if (lt_sparse && !sparse_overflow) {
-        float ms = 0;
-        BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        std::vector<uint32_t> sz(nlocal);
-        BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
-        std::vector<uint64_t> off(nlocal + 1, 0);
-        for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
-        S.list_off.alloc((nlocal + 1) * 8);
-        S.list_mem.alloc(off[nlocal] * 4 + 4);
-        BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
-        launch_walk_lt_lists(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, ks, kl,
-                             S.sizes.as<uint32_t>(), S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), st);
-        launch_sort_lists(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal, err.as<uint32_t>(), st);
-        uint32_t h_err = 0;
-        BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
-        BPT_CUDA(cudaStreamSynchronize(st));
-        if (h_err) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's list sort; sample without "
-                                    "BPT_FLAG_SPARSE");
-        S.sparse = true;
-        S.lists_built = S.lists_ok = true;
-        bpt_samples_info& I = S.info;
-        I.members = I.frontier_entries = I.coins = I.atomics = tot[0];
-        I.e_phys = I.e_logical = tot[0];
-        I.levels_total = I.levels_max = tot[1];
-        I.batch_groups = (uint32_t)S.blocks;
-        I.batches = 1;
-        I.store_bytes = S.list_mem.bytes + S.list_off.bytes;
-        I.ms_expand = ms;
-        I.expand_launches = 1;
-        I.expand_bytes = 24.0 * (double)tot[0];
-        S.level_rows.clear();
-        I.kernel_launches = g_launches - launches0;
-        I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
-        if (getenv("BPT_TRACE"))
-            fprintf(stderr, "[bpt] sample (LT sparse walks): %llu members, longest %llu, walks %.2f ms, total %.2f ms\n",
-                    tot[0], tot[1], ms, I.ms_total);
-        return;
-    }
-    S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
-
-    // ---- LT: one reverse walk per thread (k_sample.cu "LT reverse walks"); BPT_LT_FUSED=1 runs
-    //      the level-synchronous fused loop instead (same sets)
-    {
-        const char* ltf = getenv("BPT_LT_FUSED");
-        if (S.model == BPT_LT && !(ltf && ltf[0] == '1')) {
-            BPT_CUDA(cudaMemsetAsync(S.store.p, 0, S.store.bytes, st));
-            DevBuf totals(16);
-            BPT_CUDA(cudaMemsetAsync(totals.p, 0, 16, st));
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            struct EvPair {
-                cudaEvent_t* a; cudaEvent_t* b;
-                ~EvPair() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
-            } ev_guard{&e0, &e1};
-            BPT_CUDA(cudaEventCreate(&e0));
-            BPT_CUDA(cudaEventCreate(&e1));
-            BPT_CUDA(cudaEventRecord(e0, st));
-            launch_walk_lt(S.store.as<uint64_t>(), n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal,
-                           stream_key(S.seed, kTagStart), stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(),
-                           S.count0.as<uint32_t>(), totals.as<unsigned long long>(), st);
-            BPT_CUDA(cudaEventRecord(e1, st));
-            unsigned long long tot[2] = {0, 0};
-            BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 16, cudaMemcpyDeviceToHost, st));
-            BPT_CUDA(cudaStreamSynchronize(st));
-            float ms = 0;
-            BPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            // member lists for the selection's decrement, by re-walking (cheaper than a pass over the
-            // dense store); bpt_select_seeds finds them built
-            {
-                std::vector<uint32_t> sz(nlocal);
-                BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
-                std::vector<uint64_t> off(nlocal + 1, 0);
-                for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
-                S.list_off.alloc((nlocal + 1) * 8);
-                S.list_mem.alloc(off[nlocal] * 4 + 4);
-                BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
-                launch_walk_lt_lists(n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal,
-                                     stream_key(S.seed, kTagStart), stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(),
-                                     S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), st);
-                BPT_CUDA(cudaStreamSynchronize(st));
-                S.lists_built = S.lists_ok = true;
-            }
-            bpt_samples_info& I = S.info;
-            I.members = tot[0];
-            I.frontier_entries = tot[0];
-            I.coins = tot[0];    // one coinLT draw per member vertex
-            I.atomics = tot[0];  // one store atomicOr per member vertex (+ the stopping probe)
-            I.e_phys = I.e_logical = tot[0];  // (vertex, colour) expansions, SURVEY §8(d)
-            I.levels_total = I.levels_max = tot[1];
-            I.batch_groups = (uint32_t)S.blocks;
-            I.batches = 1;
-            I.store_bytes = S.store.bytes;
-            I.ms_expand = ms;
-            I.expand_launches = 1;
-            I.expand_bytes = 24.0 * (double)tot[0];  // row bounds 8 + chosen record 8 + store RMW 8 per member
-            S.level_rows.clear();
-            I.kernel_launches = g_launches - launches0;
-            I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
-            if (getenv("BPT_TRACE"))
-                fprintf(stderr, "[bpt] sample (LT walks): %llu members, longest %llu, walks %.2f ms, total %.2f ms\n",
-                        tot[0], tot[1], ms, I.ms_total);
+    // ---- LT: one reverse walk per thread (k_sample.cu "LT reverse walks"). Default: the sparse
+    //      member-list store, falling back to the dense store when a walk outgrows the per-thread
+    //      visited set (BPT_FLAG_SPARSE: fail instead); BPT_LT_DENSE=1 walks into the dense store;
+    //      BPT_LT_FUSED=1 runs the level-synchronous fused loop below (same sets).
+    if (S.model == BPT_LT) {
+        const bool fused = env_is("BPT_LT_FUSED", '1');
+        const bool want_sparse = (opt.flags & BPT_FLAG_SPARSE) || (!env_is("BPT_LT_DENSE", '1') && !fused);
+        if (want_sparse && run_lt_walks_sparse(S, opt, st, t_begin, launches0)) return;
+        if (!fused) {
+            run_lt_walks_dense(S, st, t_begin, launches0);
             return;
         }
     }
+    S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
 
     // ---- batch plan
     // IC: one block per batch keeps the working masks L2-resident; LT: as many as fit (fewer,
