@@ -17,6 +17,8 @@
 
 namespace bpt {
 
+size_t scan_temp_bytes(uint64_t count);
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp, cudaStream_t st);
 void comm_reduce_scatter_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint64_t recv_count, cudaStream_t st);
 void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st);
 
@@ -120,6 +122,11 @@ __global__ void k_lists_scatter(const uint64_t* __restrict__ store, uint32_t n, 
     }
 }
 
+__global__ void k_widen_u32(const uint32_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t count) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
 // sparse store: vertex -> local samples index (inv_off = exclusive scan of the occurrence counts)
 __global__ void k_inv_scatter(const uint64_t* __restrict__ off, const uint32_t* __restrict__ members, uint64_t nlists,
                               const uint64_t* __restrict__ inv_off, uint32_t* __restrict__ cursor,
@@ -204,15 +211,18 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     DevBuf covered(S.sparse ? (S.s1 - S.s0) * 4 + 4 : 4);
     if (S.sparse) {
         BPT_CUDA(cudaMemsetAsync(covered.p, 0, covered.bytes, st));
-        if (!S.inv_off.p) {  // vertex -> samples index, built once per handle
+        if (!S.inv_off.p) {  // vertex -> samples index, built once per handle (device scan)
             Samples& M = const_cast<Samples&>(S);
-            std::vector<uint32_t> cnt(n);
-            BPT_CUDA(cudaMemcpy(cnt.data(), S.count0.p, (uint64_t)n * 4, cudaMemcpyDeviceToHost));
-            std::vector<uint64_t> io(n + 1, 0);
-            for (uint32_t v = 0; v < n; ++v) io[v + 1] = io[v] + cnt[v];
             M.inv_off.alloc((uint64_t)(n + 1) * 8);
-            M.inv_s.alloc(io[n] * 4 + 4);
-            BPT_CUDA(cudaMemcpyAsync(M.inv_off.p, io.data(), (uint64_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));
+            DevBuf wide((uint64_t)(n + 1) * 8), temp(scan_temp_bytes(n + 1));
+            BPT_CUDA(cudaMemsetAsync(wide.p, 0, wide.bytes, st));
+            k_widen_u32<<<num_sms() * 4, 256, 0, st>>>(S.count0.as<uint32_t>(), wide.as<uint64_t>(), n);
+            exclusive_scan_u64(wide.as<uint64_t>(), M.inv_off.as<uint64_t>(), n + 1, temp.p, st);
+            count_launch();
+            uint64_t total = 0;
+            BPT_CUDA(cudaMemcpyAsync(&total, M.inv_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaStreamSynchronize(st));
+            M.inv_s.alloc(total * 4 + 4);
             DevBuf cursor((uint64_t)n * 4);
             BPT_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes, st));
             const uint64_t nl = S.s1 - S.s0;
