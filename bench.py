@@ -227,6 +227,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         step_no[0] += 1
         if host is None:
             g = bpt.Graph(d_row, d_col, w_q31=d_thr, model=model, comm=comm, n=cfg.n, m=cfg.m, stream=stream)
+        elif world > 1:  # end to end: rank 0 copies the input once, the reverse CSR goes over NVLink
+            g = bpt.Graph(host["row"] if rank == 0 else None, host["col"] if rank == 0 else None,
+                          w_q31=host["thr"] if rank == 0 else None, model=model, comm=comm, n=cfg.n, m=cfg.m,
+                          stream=stream, bcast_root=0)
         else:
             g = bpt.Graph(host["row"], host["col"], w_q31=host["thr"], model=model, comm=comm, n=cfg.n, m=cfg.m,
                           stream=stream)
@@ -301,7 +305,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         host = {"row": torch.from_numpy(row_ptr.view(np.int64).copy()).pin_memory(),
                 "col": torch.from_numpy(col.view(np.int32).copy()).pin_memory(),
                 "thr": torch.from_numpy(thr.view(np.int32).copy()).pin_memory()}
-        h2d = row_ptr.nbytes + col.nbytes + thr.nbytes
+        h2d = row_ptr.nbytes + col.nbytes + thr.nbytes  # copied once per step (rank 0 when world > 1)
         step(False, host)
         barrier()
         torch.cuda.synchronize()

@@ -94,6 +94,15 @@ BPT_API void bpt_comm_free(bpt_comm* comm);
 BPT_API bpt_status bpt_graph_load(bpt_comm* comm, const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
                           uint64_t m, const float* w_f32, const uint32_t* w_q31, bpt_model model,
                           void* stream, bpt_graph** out);
+/* Collective variant of bpt_graph_load for a communicator of world > 1 (every rank calls it):
+ * only the root's row_ptr / col / weights are read (others may pass NULL; n, m and model must
+ * be the same on every rank). The root validates and builds the reverse CSR; the result is
+ * broadcast over NCCL (NVLink), so the host-to-device copy of the input happens once instead
+ * of once per GPU (SURVEY §8(e) "rank 0 builds and ncclBroadcasts"). A validation error on the
+ * root fails the call on every rank. world == 1 (or comm NULL): same as bpt_graph_load. */
+BPT_API bpt_status bpt_graph_load_bcast(bpt_comm* comm, int root, const uint64_t* row_ptr, const uint32_t* col,
+                                        uint32_t n, uint64_t m, const float* w_f32, const uint32_t* w_q31,
+                                        bpt_model model, void* stream, bpt_graph** out);
 /* Export the reverse CSR (tests): roff[n+1], src[m], val[m] (IC: threshold; LT: cumulative
  * threshold). Any pointer may be NULL. Host or device buffers. */
 BPT_API bpt_status bpt_graph_reverse(const bpt_graph* g, uint32_t* roff, uint32_t* src, uint32_t* val);

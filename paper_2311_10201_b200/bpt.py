@@ -59,6 +59,7 @@ _SIGS = {
     "bpt_comm_init": ([_p, _i, _i, _i, ctypes.POINTER(_p)], _i),
     "bpt_comm_free": ([_p], None),
     "bpt_graph_load": ([_p, _p, _p, _u32, _u64, _p, _p, _i, _p, ctypes.POINTER(_p)], _i),
+    "bpt_graph_load_bcast": ([_p, _i, _p, _p, _u32, _u64, _p, _p, _i, _p, ctypes.POINTER(_p)], _i),
     "bpt_graph_reverse": ([_p, _p, _p, _p], _i),
     "bpt_graph_dims": ([_p, _p, _p, _p], _i),
     "bpt_graph_free": ([_p], None),
@@ -164,6 +165,14 @@ def bpt_graph_load(comm, row_ptr, col, n: int, m: int, w_f32=None, w_q31=None, m
     return h
 
 
+def bpt_graph_load_bcast(comm, root: int, row_ptr, col, n: int, m: int, w_f32=None, w_q31=None, model: int = IC,
+                         stream=None):
+    h = _p()
+    _check(_lib.bpt_graph_load_bcast(comm, root, _ptr(row_ptr), _ptr(col), n, m, _ptr(w_f32), _ptr(w_q31), model,
+                                     _stream(stream), ctypes.byref(h)))
+    return h
+
+
 def bpt_graph_free(h) -> None:
     _lib.bpt_graph_free(h)
 
@@ -266,11 +275,17 @@ class Graph:
     """bpt_graph_load: forward CSR + weights -> device reverse CSR."""
 
     def __init__(self, row_ptr, col, w_f32=None, w_q31=None, model: int = IC, comm: Comm | None = None,
-                 n: int | None = None, m: int | None = None, stream=None):
+                 n: int | None = None, m: int | None = None, stream=None, bcast_root: int | None = None):
+        """bcast_root: collective load (bpt_graph_load_bcast) -- only that rank's arrays are read
+        (others may pass None with n and m); the reverse CSR is broadcast over NCCL."""
         self.comm = comm
         self.n = int(n if n is not None else row_ptr.shape[0] - 1)
         self.m = int(m if m is not None else col.shape[0])
         self.model = model
+        if bcast_root is not None:
+            self._h = bpt_graph_load_bcast(comm._h if comm else None, bcast_root, row_ptr, col, self.n, self.m,
+                                           w_f32, w_q31, model, stream)
+            return
         if isinstance(row_ptr, np.ndarray):
             row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
             col = np.ascontiguousarray(col, dtype=np.uint32)

@@ -137,6 +137,7 @@ void compute_digests(const Samples& S, cudaStream_t st);
 void comm_unique_id(void* out);
 void comm_init(Comm* c, const void* uid);
 void comm_destroy(Comm* c);
+void comm_broadcast(Comm* c, const void* send, void* recv, uint64_t bytes, int root, cudaStream_t st);
 
 namespace {
 
@@ -641,6 +642,51 @@ bpt_status bpt_graph_load(bpt_comm* comm, const uint64_t* row_ptr, const uint32_
         DevIn dwq(w_q31, m * 4, st);
         build_reverse_csr(G->g, (const uint64_t*)drp.p, (const uint32_t*)dcol.p, (const float*)dwf.p,
                           (const uint32_t*)dwq.p, st);
+        *out = G.release();
+    });
+}
+
+bpt_status bpt_graph_load_bcast(bpt_comm* comm, int root, const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                                uint64_t m, const float* w_f32, const uint32_t* w_q31, bpt_model model, void* stream,
+                                bpt_graph** out) {
+    if (!comm || comm->c.world <= 1 || !comm->c.nccl)
+        return bpt_graph_load(comm, row_ptr, col, n, m, w_f32, w_q31, model, stream, out);
+    return guarded([&] {
+        if (!out) fail(BPT_EINVAL, "out is NULL");
+        if (root < 0 || root >= comm->c.world) fail(BPT_EINVAL, "root must be a rank of the communicator");
+        if (n == 0) fail(BPT_EINVAL, "n must be > 0");
+        if (m >= (1ull << 32)) fail(BPT_EINVAL, "m must be < 2^32");
+        if (model != BPT_IC && model != BPT_LT) fail(BPT_EINVAL, "model must be BPT_IC or BPT_LT");
+        use_device(comm->c.device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const bool is_root = comm->c.rank == root;
+        bpt_graph* built = nullptr;
+        std::string root_error;
+        if (is_root) {  // validate + build on the root; its outcome is broadcast before the data
+            const bpt_status r = bpt_graph_load(comm, row_ptr, col, n, m, w_f32, w_q31, model, stream, &built);
+            if (r != BPT_OK) root_error = g_last_error;
+        }
+        DevBuf status(4);
+        const uint32_t h_status = is_root ? (built ? 1u : 2u) : 0u;
+        BPT_CUDA(cudaMemcpyAsync(status.p, &h_status, 4, cudaMemcpyHostToDevice, st));
+        comm_broadcast(&comm->c, status.p, status.p, 4, root, st);
+        uint32_t got = 0;
+        BPT_CUDA(cudaMemcpyAsync(&got, status.p, 4, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
+        if (got != 1) fail(BPT_EINVAL, is_root ? root_error : "graph load failed on the root rank");
+        std::unique_ptr<bpt_graph> G(built ? built : new bpt_graph());
+        if (!is_root) {
+            G->g.comm = &comm->c;
+            G->g.device = comm->c.device;
+            G->g.n = n;
+            G->g.m = m;
+            G->g.model = model;
+            G->g.roff.alloc(((size_t)n + 1) * 4);
+            G->g.rec.alloc(m * 8 + 8);
+        }
+        comm_broadcast(&comm->c, G->g.roff.p, G->g.roff.p, ((uint64_t)n + 1) * 4, root, st);
+        if (m) comm_broadcast(&comm->c, G->g.rec.p, G->g.rec.p, m * 8, root, st);
+        BPT_CUDA(cudaStreamSynchronize(st));
         *out = G.release();
     });
 }

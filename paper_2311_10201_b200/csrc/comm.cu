@@ -39,6 +39,10 @@ void comm_reduce_scatter_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint
                "ncclReduceScatter");
 }
 
+void comm_broadcast(Comm* c, const void* send, void* recv, uint64_t bytes, int root, cudaStream_t st) {
+    check_nccl(ncclBroadcast(send, recv, bytes, ncclUint8, root, (ncclComm_t)c->nccl, st), "ncclBroadcast");
+}
+
 void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st) {
     check_nccl(ncclAllReduce(buf, buf, count, ncclUint64, ncclMax, (ncclComm_t)c->nccl, st), "ncclAllReduce");
 }

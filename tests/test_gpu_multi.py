@@ -45,8 +45,18 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
     uid = [bpt.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = bpt.Comm(world, rank, rank, uid[0])
-    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.IC if cfg.model == "IC" else bpt.LT, comm=comm)
-    s = g.sample(theta, colors=64, seed=cfg.seed, **(kw or {}))
+    kw = dict(kw or {})
+    model = bpt.IC if cfg.model == "IC" else bpt.LT
+    if kw.pop("bcast", False):  # collective load: only rank 0's arrays are read
+        g = bpt.Graph(row_ptr if rank == 0 else None, col if rank == 0 else None, w_q31=thr if rank == 0 else None,
+                      model=model, comm=comm, n=cfg.n, m=cfg.m, bcast_root=0)
+        ref = bpt.Graph(row_ptr, col, w_q31=thr, model=model, comm=comm)
+        a, b = g.reverse_csr(), ref.reverse_csr()
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+        ref.close()
+    else:
+        g = bpt.Graph(row_ptr, col, w_q31=thr, model=model, comm=comm)
+    s = g.sample(theta, colors=64, seed=cfg.seed, **kw)
     sizes = s.sizes(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint32)
     digests = s.digests(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint64)
     seeds, gains, sigma = s.select_seeds(cfg.k)
@@ -58,6 +68,7 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
 
 
 MODES = {"ic": ("C2", 1 << 14, {}), "ic_wide": ("C2", 1 << 14, {"wide": True}),
+         "ic_bcast": ("C2", 1 << 14, {"bcast": True}),
          "lt": ("C3", 1 << 13, {}), "lt_sparse": ("C3", 1 << 13, {"sparse": True})}
 
 
