@@ -1,16 +1,21 @@
 // k_sample.cu -- A2 start/colour assignment, A3/A3' fused frontier expansion (IC / LT),
-// A4 frontier compaction.  Listing 1 of the paper, level-synchronous
-// (reading C-7), mark-on-discovery.
+// A4 frontier compaction, and the device-resident loops that run them. Listing 1 of the
+// paper, level-synchronous (reading C-7), mark-on-discovery.
 //
-// Data layout per batch of `slots` 64-sample blocks (DESIGN.md §Layout):
-//   V[slot][n] u64   visited masks  = the fused RRR store (Listing 1 visited[])
-//   N[slot][n] u64   next-frontier accumulators (Listing 1 frontier[u] |= fr_u)
-//   raw[]      u64   discovered entries of the next level: v | slot << 32 | slice << 58
-//   q[]        uint4 compacted frontier entries {v, slot, mask lo, mask hi}
-//   qoff[]     u64   exclusive prefix of per-entry work (IC: in-degree, LT: popcount)
-//   tstart[]   u32   first entry of each expansion tile (written by the compaction)
-// Level L:  compact(L): raw(L) -> V |= N, q/qoff/tstart      (Listing 1 lines 7-8)
+// Data layout per batch of `slots` 64-sample blocks (DESIGN.md §5):
+//   VN[slot][n] {V, N}  visited masks (Listing 1 visited[]) and next-frontier
+//                       accumulators (frontier[u] |= fr_u), one 32-B sector per vertex
+//   raw[]      u64      discovered entries of the next level: v | slot << 32 | slice << 58
+//   q[]        uint4    compacted frontier entries {rowstart - off (IC) | v (LT), slot, mask}
+//   qoff[]     u64      exclusive prefix of per-entry work (LT)
+//   tstart[], umask[]   first entry / entry-start bitmap of each expansion unit (IC)
+// Level L:  compact(L): raw(L) -> V |= N, q/tstart/umask     (Listing 1 lines 7-8)
 //           expand(L):  q -> N atomicOr, raw(L+1)             (Listing 1 lines 9-15)
+//
+// Sections: helpers; A2 k_init; A4 compaction; level advance; IC expansion (the product's
+// dominant kernel); IC wide fusion (2 blocks per frontier entry, §8(f) NEXT #2); LT reverse
+// walks (dense and sparse store); LT fused expansion and its cooperative level loop; launchers
+// and the CUDA-graph builder.
 #include <algorithm>
 #include <cstdio>
 #include <type_traits>
