@@ -367,6 +367,29 @@ def test_lt_sparse_store(bpt):
     s.close()
 
 
+def test_lt_long_walks_fall_back_to_dense(bpt):
+    """A chain graph (i -> i+1, LT weight 1): the reverse walk from vertex v has v+1 members, so
+    walks outgrow the sparse store's per-thread visited set; by default the call falls back to
+    the dense store (same sets as the oracle), with BPT_FLAG_SPARSE it fails with ENOMEM."""
+    n = 3000
+    row_ptr = np.arange(n + 1, dtype=np.uint64)
+    row_ptr[n] = n - 1
+    col = np.arange(1, n, dtype=np.uint32)
+    thr = np.full(n - 1, Q31, np.uint32)
+    theta = 192
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    og = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT)
+    sizes, digests, _ = og.sample_many(7, np.arange(theta, dtype=np.uint64))
+    assert sizes.max() > 1536  # the case this test is about
+    s = g.sample(theta, colors=64, seed=7)
+    assert np.array_equal(s.sizes(0, theta), sizes) and np.array_equal(s.digests(0, theta), digests)
+    assert s.info["store_bytes"] >= (theta // 64) * n * 8  # the dense store
+    s.close()
+    with pytest.raises(bpt.BptError) as ei:
+        g.sample(theta, colors=64, seed=7, sparse=True)
+    assert ei.value.code == bpt.BPT_ENOMEM
+
+
 # ------------------------------------------------------------------ C2 / C5 shape, scaled
 
 @pytest.fixture(scope="module")
