@@ -214,9 +214,9 @@ def test_ragged_theta_and_ranges(bpt):
     cfg = graphgen.CONFIGS["C1"]
     row_ptr, col, thr = graphgen.make_graph(cfg)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
-    for theta in (1, 63, 65, 200):
+    for theta, wide in ((1, False), (63, False), (65, False), (200, False), (1, True), (65, True), (200, True)):
         ref = oracle_all(row_ptr, col, thr, oracle.IC, theta, 99)
-        s = g.sample(theta, colors=64, seed=99)
+        s = g.sample(theta, colors=64, seed=99, wide=wide)
         check_full(bpt, s, ref, theta)
         for first, count in [(0, 1), (theta - 1, 1), (theta // 3, theta - theta // 3)]:
             off, mem = s.extract(first, count)
@@ -225,10 +225,14 @@ def test_ragged_theta_and_ranges(bpt):
             assert np.array_equal(off, ref["offsets"][first:first + count + 1] - ref["offsets"][first])
 
 
-def test_graph_without_edges(bpt):
+@pytest.mark.parametrize("mode", ["ic", "ic_wide", "lt", "lt_dense"])
+def test_graph_without_edges(bpt, monkeypatch, mode):
     n = 10
-    g = bpt.Graph(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), w_q31=np.zeros(0, np.uint32))
-    s = g.sample(100, seed=4)
+    if mode == "lt_dense":
+        monkeypatch.setenv("BPT_LT_DENSE", "1")
+    model = bpt.LT if mode.startswith("lt") else bpt.IC
+    g = bpt.Graph(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), w_q31=np.zeros(0, np.uint32), model=model)
+    s = g.sample(100, seed=4, wide=mode == "ic_wide")
     off, mem = s.extract(0, 100)
     assert mem.tolist() == [oracle.start_vertex(i, n, 4) for i in range(100)]
     seeds, gains, sigma = s.select_seeds(n)
@@ -388,6 +392,22 @@ def test_lt_long_walks_fall_back_to_dense(bpt):
     with pytest.raises(bpt.BptError) as ei:
         g.sample(theta, colors=64, seed=7, sparse=True)
     assert ei.value.code == bpt.BPT_ENOMEM
+
+
+def test_lt_ragged_theta_and_ranges(bpt):
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 11, theta=64)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    for theta in (1, 63, 65, 200):
+        ref = oracle_all(row_ptr, col, thr, oracle.LT, theta, 5)
+        s = g.sample(theta, colors=64, seed=5)
+        check_full(bpt, s, ref, theta)
+        for first, count in [(0, 1), (theta - 1, 1), (theta // 3, theta - theta // 3)]:
+            off, mem = s.extract(first, count)
+            a, b = int(ref["offsets"][first]), int(ref["offsets"][first + count])
+            assert np.array_equal(mem, ref["members"][a:b])
+            assert np.array_equal(off, ref["offsets"][first:first + count + 1] - ref["offsets"][first])
+        s.close()
 
 
 # ------------------------------------------------------------------ C2 / C5 shape, scaled
