@@ -32,6 +32,13 @@ sys.path.insert(0, ROOT)
 import graphgen  # noqa: E402
 
 METRIC = "RRR sets/sec (64-color fused BPT, IC, LiveJournal-shaped R-MAT)"
+METRICS = {  # per config (the default C2 line keeps the name above)
+    "C1": "RRR sets/sec (64-color fused BPT, IC, R-MAT scale 10)",
+    "C2": METRIC,
+    "C3": "RRR sets/sec (64-color fused BPT, LT, Orkut-shaped R-MAT)",
+    "C4": "RRR sets/sec (64-color fused BPT, IC, Friendster-shaped R-MAT)",
+    "C5": METRIC,
+}
 UNIT = "RRR sets/s"
 CFG = graphgen.CONFIGS["C2"]
 EXTRACT_SAMPLES = 64
@@ -181,7 +188,7 @@ def run_reference(args, rank: int, world: int):
             times.append(time.perf_counter() - t0)
     ms = 1000.0 * sum(times) / len(times)
     value = per_step / (ms / 1000.0)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+    line = {"impl": "reference", "metric": METRICS.get(cfg.name, METRIC), "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "step": f"{per_step} samples of the workload (bounded)"},
@@ -376,7 +383,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, row_ptr, col, thr, args.cpu_samples or None)
     line = {
-        "metric": METRIC, "value": cfg.theta / (ms_max / 1000.0), "unit": UNIT, "n_gpus": world,
+        "metric": METRICS.get(cfg.name, METRIC), "value": cfg.theta / (ms_max / 1000.0), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "theta": cfg.theta, "colors": cfg.colors, "k": cfg.k,
