@@ -156,9 +156,10 @@ constexpr uint32_t kCompTile = kThreads * kCompItems;
 template <bool kCoh>
 __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __restrict__ tstart, uint64_t tstart_cap,
                                              uint32_t unit) {
-    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     LevelRec* L = &a.lv[LDX(&a.ctl->level)];
     const uint64_t nraw = umin64(LDX(&L->raw), a.raw_cap);
+    if (blockIdx.x > 0 && (uint64_t)blockIdx.x * kCompTile >= nraw) return;  // no tile of this level
+    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     __shared__ unsigned long long wsum[kWarps];
     __shared__ uint32_t wcnt[kWarps];
     __shared__ unsigned long long blk_base;
@@ -386,13 +387,15 @@ __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphCondi
 }
 
 // The last block of an expansion launch to finish advances the level (fused, no extra launch).
-__device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphConditionalHandle h_level, int use_cond) {
+// nblocks: blocks of this launch that take part (the others left without counting themselves)
+__device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphConditionalHandle h_level, int use_cond,
+                                              uint32_t nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
         atomicMax(&a.ctl->t_end, global_ns());
         __threadfence();
         const unsigned prev = atomicAdd(&a.ctl->blocks_done, 1u);
-        if (prev == gridDim.x - 1) {
+        if (prev == nblocks - 1) {
             __threadfence();
             a.ctl->blocks_done = 0;
             advance_level(a, h_level, use_cond);
@@ -618,12 +621,18 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     const uint64_t gblk0 = LDX(&ctl->gblk0);
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
-    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
     const unsigned long long packed = LDX(&L->packed);
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || LDX(&L->overflow)) {
-        finish_expand(a, h_level, use_cond);
+    const bool idle = nq == 0 || LDX(&L->overflow);
+    // blocks without a unit of this level leave at once (thin levels: a few blocks work); the
+    // active ones count themselves out, the last advances the level
+    const uint32_t active =
+        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kUnitIC * kWarps - 1) / ((uint64_t)kUnitIC * kWarps)));
+    if (blockIdx.x >= active) return;
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    if (idle) {
+        finish_expand(a, h_level, use_cond, active);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -637,7 +646,7 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     // 32-bit unit indices: total < 2^36 work items, so units < 2^30
     const uint32_t nunits = (uint32_t)((total + kUnitIC - 1) / kUnitIC);
     const uint32_t nfull = (uint32_t)(total / kUnitIC);
-    const uint32_t nwarps = gridDim.x * kWarps;
+    const uint32_t nwarps = active * kWarps;
     unsigned long long coins = 0, atoms = 0;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = LDX(&tstart[unit]);
@@ -652,7 +661,7 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    finish_expand(a, h_level, use_cond);
+    finish_expand(a, h_level, use_cond, active);
 }
 
 template <bool kC64>
@@ -1039,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
     if (nq == 0 || L->overflow) {
-        finish_expand(a, h_level, use_cond);
+        finish_expand(a, h_level, use_cond, gridDim.x);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1067,7 +1076,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    finish_expand(a, h_level, use_cond);
+    finish_expand(a, h_level, use_cond, gridDim.x);
 }
 
 // ------------------------------------------------------------------------ LT reverse walks
@@ -1266,7 +1275,7 @@ __device__ __forceinline__ void expand_lt_body(const BatchArgs& a, const uint32_
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
     if (nq == 0 || LDX(&L->overflow)) {
-        finish_expand(a, h_level, use_cond);
+        finish_expand(a, h_level, use_cond, gridDim.x);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1355,7 +1364,7 @@ __device__ __forceinline__ void expand_lt_body(const BatchArgs& a, const uint32_
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, sm.red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    finish_expand(a, h_level, use_cond);
+    finish_expand(a, h_level, use_cond, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart,
