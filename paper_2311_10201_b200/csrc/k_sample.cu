@@ -713,9 +713,10 @@ __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int us
 __global__ void __launch_bounds__(kThreads, 5) k_compact_w(BatchArgs a, uint32_t* __restrict__ tstart,
                                                         uint64_t tstart_cap) {
     if (!a.ctl->cont) return;
-    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     LevelRec* L = &a.lv[a.ctl->level];
     const uint64_t nraw = umin64(L->raw, a.raw_cap);
+    if (blockIdx.x > 0 && (uint64_t)blockIdx.x * kCompTile >= nraw) return;  // no tile of this level
+    if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     constexpr uint32_t unit = kUnitWide;
     __shared__ unsigned long long wsum[kWarps];
     __shared__ uint32_t wcnt[kWarps];
@@ -1043,12 +1044,17 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     const uint64_t gblk0 = ctl->gblk0;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
-    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
     const unsigned long long packed = L->packed;
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
-    if (nq == 0 || L->overflow) {
-        finish_expand(a, h_level, use_cond, gridDim.x);
+    const bool idle = nq == 0 || L->overflow;
+    const uint32_t active =  // blocks with work; the others leave at once
+        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kUnitWide * kWarps - 1) /
+                                                             ((uint64_t)kUnitWide * kWarps)));
+    if (blockIdx.x >= active) return;
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    if (idle) {
+        finish_expand(a, h_level, use_cond, active);
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1063,7 +1069,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     const uint32_t nfull = (uint32_t)(total / kUnitWide);
     const uint32_t sb0 = (uint32_t)(64ull * gblk0);
     unsigned long long coins = 0, atoms = 0;
-    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += gridDim.x * kWarps) {
+    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += active * kWarps) {
         const uint32_t jc0 = tstart[unit];
         if (unit < nfull)
             expand_unit_w<true>(a, Ln, W, lane, le_mask, unit, kUnitWide, jc0, sb0, coins, atoms);
@@ -1076,7 +1082,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArg
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    finish_expand(a, h_level, use_cond, gridDim.x);
+    finish_expand(a, h_level, use_cond, active);
 }
 
 // ------------------------------------------------------------------------ LT reverse walks
