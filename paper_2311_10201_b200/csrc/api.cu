@@ -272,17 +272,25 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
                                 uint64_t launches0) {
     const Graph& g = *S.g;
     const uint64_t nlocal = S.s1 - S.s0;
-    DevBuf totals(24), err(4);
+    DevBuf totals(24), err(4), rows;
     BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
     BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    {  // walk-order rows written during the walk when they fit a quarter of the free memory,
+       // else the lists come from a second walk
+        size_t fb = 0, tb = 0;
+        BPT_CUDA(cudaMemGetInfo(&fb, &tb));
+        const uint64_t bytes = nlocal * (uint64_t)walk_row_stride() * 4;
+        if (bytes < (fb + cached_bytes()) / 4 && !env_is("BPT_LT_REWALK", '1')) rows.alloc(bytes);
+    }
     WalkTimer tm(st);
     launch_walk_lt_sparse(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, stream_key(S.seed, kTagStart),
                           stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(),
-                          totals.as<unsigned long long>(), st);
+                          totals.as<unsigned long long>(), rows.p ? rows.as<uint32_t>() : nullptr, st);
     tm.stop(st);
     unsigned long long tot[3] = {0, 0, 0};
     BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
+    const double t_walk_ms = std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count();
     if (tot[2]) {
         if (opt.flags & BPT_FLAG_SPARSE)
             fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's visited set; sample without "
@@ -291,13 +299,28 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
         BPT_CUDA(cudaMemsetAsync(S.sizes.p, 0, nlocal * 4, st));
         return false;
     }
-    lt_lists_by_rewalk(S, st);
+    if (rows.p) {
+        std::vector<uint32_t> sz(nlocal);
+        BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> off(nlocal + 1, 0);
+        for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
+        S.list_off.alloc((nlocal + 1) * 8);
+        S.list_mem.alloc(off[nlocal] * 4 + 4);
+        BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
+        launch_rows_to_lists(rows.as<uint32_t>(), S.list_off.as<uint64_t>(), nlocal, S.list_mem.as<uint32_t>(), st);
+        S.lists_built = S.lists_ok = true;
+    } else {
+        lt_lists_by_rewalk(S, st);
+    }
     launch_sort_lists(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal, err.as<uint32_t>(), st);
     uint32_t h_err = 0;
     BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
     if (h_err) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's list sort; sample without "
                                 "BPT_FLAG_SPARSE");
+    if (getenv("BPT_TRACE"))
+        fprintf(stderr, "[bpt] LT sparse: rows %s, walk ends %.2f ms, lists+sort end %.2f ms after call start\n",
+                rows.p ? "yes" : "no", t_walk_ms, std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count());
     S.sparse = true;
     lt_walk_info(S, tot, tm.ms(), launches0, t_begin, "LT sparse walks");
     return true;

@@ -223,7 +223,10 @@ void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uin
 // totals[0..1] as launch_walk_lt, totals[2] = 1 if a walk outgrew the hash set
 void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
-                           unsigned long long* totals, cudaStream_t st);
+                           unsigned long long* totals, uint32_t* rows, cudaStream_t st);
+// walk-order member rows (optional output of the sparse walk: stride walk_row_stride()) -> lists
+uint32_t walk_row_stride();
+void launch_rows_to_lists(const uint32_t* rows, const uint64_t* off, uint64_t nlists, uint32_t* members, cudaStream_t st);
 // sort every list ascending in place (one block per list of <= 4096 members; longer lists set *err)
 void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, uint32_t* err, cudaStream_t st);
 // LT: re-walk every local sample and write its members at off[i] (unsorted; for the selection)

@@ -3,8 +3,8 @@
 // The BPTs traverse the transpose (Def. 2; Listing 1's mate(e,v)).
 // Canonical order (reading C-4): rows by destination v, entries in forward-CSR position
 // order inside a row. That is a STABLE sort of the forward edge list by destination,
-// done here as an LSD radix sort (8-bit digits; per-warp __match_any_sync ranking keeps
-// it stable), then:
+// done here as an LSD radix sort (8-bit digits; per-warp ballot ranking keeps
+// it stable; the {src, thr} payload travels with the key), then:
 //   roff[v]  = lower_bound(sorted destinations, v)
 //   rec[i]   = {src(e_fwd), thr(e_fwd)}, thr = Q1.31 (reading C-5: floor(p * 2^31))
 //   LT       : rec[i].y = inclusive prefix of thr within the row, row sum <= 2^31 (C-6)
@@ -61,9 +61,18 @@ __global__ void k_expand_rows(const uint64_t* __restrict__ row_ptr, uint32_t n, 
     }
 }
 
-__global__ void k_iota(uint32_t* __restrict__ v, uint64_t m) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        v[i] = (uint32_t)i;
+// lanes of the warp holding the same digit d in [0, kRadix] (kRadix = past the end): nine
+// ballots, a constant cost; __match_any_sync costs grow with the number of distinct values
+// per warp (measured 3.6x slower on the low digits of R-MAT destinations)
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+    uint32_t p = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+        const bool on = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        p &= on ? bal : ~bal;
+    }
+    return p;
 }
 
 // per-warp digit counts of one tile into smem cnt[warp][digit]
@@ -71,10 +80,17 @@ __device__ __forceinline__ void tile_warp_counts(const uint32_t* __restrict__ ke
                                                  uint32_t (*cnt)[kRadix]) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile + (uint64_t)w * (32 * kRsRounds);
+    uint32_t key[kRsRounds];
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r) {  // all loads in flight before the first ballot
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        key[r] = i < m ? keys[i] : 0u;
+    }
+#pragma unroll
     for (int r = 0; r < kRsRounds; ++r) {
         uint64_t i = base + (uint64_t)r * 32 + lane;
-        uint32_t d = i < m ? (keys[i] >> shift) & (kRadix - 1) : kRadix;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t d = i < m ? (key[r] >> shift) & (kRadix - 1) : kRadix;
+        uint32_t peers = digit_peers(d);
         if (d < kRadix && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
     }
 }
@@ -91,36 +107,105 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t* __res
     hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = s;  // digit-major
 }
 
-__global__ void __launch_bounds__(kRsThreads) k_radix_scatter(const uint32_t* __restrict__ keys,
-                                                              const uint32_t* __restrict__ vals, uint64_t m,
-                                                              int shift, const uint32_t* __restrict__ hist_scan,
-                                                              uint64_t ntiles, uint32_t* __restrict__ keys_out,
-                                                              uint32_t* __restrict__ vals_out) {
-    __shared__ uint32_t cnt[kRsWarps][kRadix];
+// One stable LSD pass over a 4096-item tile, the (src, thr) payload carried with the key so
+// the sorted records need no gather through a permutation afterwards. The tile is ranked in
+// registers (per-warp ballot rounds), reordered by digit in shared memory, and
+// written out in that order: the items of one digit leave as one contiguous run (16 items on
+// average at 8-bit digits) instead of 32 scattered 4-byte stores per warp round.
+// kFirst: payload read from (srcof, weights); kLast: records written as uint2 {src, thr}.
+constexpr size_t kPassSmem = (size_t)kRsTile * 12 + (size_t)kRsWarps * kRadix * 4 + kRadix * 8;
+
+template <bool kFirst, bool kLast>
+__global__ void __launch_bounds__(kRsThreads, 2) k_radix_pass(const uint32_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ src,
+                                                           const float* __restrict__ wf,
+                                                           const uint32_t* __restrict__ wq, uint64_t m, int shift,
+                                                           const uint32_t* __restrict__ hist_scan, uint64_t ntiles,
+                                                           uint32_t* __restrict__ keys_out,
+                                                           uint32_t* __restrict__ src_out,
+                                                           uint32_t* __restrict__ w_out, uint2* __restrict__ rec_out) {
+    extern __shared__ uint4 smem_raw[];
+    uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* ss = sk + kRsTile;
+    uint32_t* sw = ss + kRsTile;
+    uint32_t (*cnt)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(sw + kRsTile);
+    uint32_t* toff = &cnt[kRsWarps][0];  // [kRadix] tile-local digit offsets
+    uint32_t* gdel = toff + kRadix;      // [kRadix] global position - local position (mod 2^32)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kRsWarps * kRadix; i += kRsThreads) (&cnt[0][0])[i] = 0;
     __syncthreads();
-    tile_warp_counts(keys, m, shift, cnt);
-    __syncthreads();
-    {   // cnt[w][d] <- global position of warp w's first item with digit d
-        const int d = threadIdx.x;
-        uint32_t run = hist_scan[(uint64_t)d * ntiles + blockIdx.x];
-        for (int w = 0; w < kRsWarps; ++w) { uint32_t c = cnt[w][d]; cnt[w][d] = run; run += c; }
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t)blockIdx.x * kRsTile + (uint64_t)w * (32 * kRsRounds);
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kRsTile;
+    const uint64_t base = tile0 + (uint64_t)w * (32 * kRsRounds);
     const uint32_t lt = (1u << lane) - 1u;
+    uint32_t key[kRsRounds], sv[kRsRounds], wv[kRsRounds], rank[kRsRounds];
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r) {  // the whole tile in flight before the ranking
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        key[r] = sv[r] = wv[r] = 0u;
+        if (i < m) {
+            key[r] = keys[i];
+            sv[r] = src[i];
+            wv[r] = kFirst && wf ? (uint32_t)floor((double)wf[i] * 2147483648.0) : wq[i];  // reading C-5
+        }
+    }
+#pragma unroll
     for (int r = 0; r < kRsRounds; ++r) {
-        uint64_t i = base + (uint64_t)r * 32 + lane;
-        uint32_t key = 0, val = 0, d = kRadix;
-        if (i < m) { key = keys[i]; val = vals[i]; d = (key >> shift) & (kRadix - 1); }
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t pos = 0;
-        if (d < kRadix) pos = cnt[w][d] + __popc(peers & lt);
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        const uint32_t d = i < m ? (key[r] >> shift) & (kRadix - 1) : kRadix;
+        const uint32_t peers = digit_peers(d);
+        rank[r] = 0;
+        if (d < kRadix) rank[r] = cnt[w][d] + __popc(peers & lt);
         __syncwarp();
         if (d < kRadix && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
         __syncwarp();
-        if (d < kRadix) { keys_out[pos] = key; vals_out[pos] = val; }
+    }
+    __syncthreads();
+    {   // thread d: tile total of digit d, exclusive scan over digits, per-warp bases
+        const int d = threadIdx.x;
+        uint32_t tot = 0;
+        for (int q = 0; q < kRsWarps; ++q) tot += cnt[q][d];
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        toff[d] = x;  // inclusive within the warp, fixed up below
+        __syncthreads();
+        uint32_t carry = 0;
+        for (int q = 0; q < w; ++q) carry += toff[q * 32 + 31];
+        __syncthreads();
+        const uint32_t off = carry + x - tot;
+        toff[d] = off;
+        gdel[d] = hist_scan[(uint64_t)d * ntiles + blockIdx.x] - off;
+        uint32_t run = off;
+        for (int q = 0; q < kRsWarps; ++q) { const uint32_t c = cnt[q][d]; cnt[q][d] = run; run += c; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r) {
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        if (i < m) {
+            const uint32_t d = (key[r] >> shift) & (kRadix - 1);
+            const uint32_t lp = cnt[w][d] + rank[r];
+            sk[lp] = key[r];
+            ss[lp] = sv[r];
+            sw[lp] = wv[r];
+        }
+    }
+    __syncthreads();
+    const uint32_t count = (uint32_t)(m - tile0 < kRsTile ? m - tile0 : kRsTile);
+    for (uint32_t j = threadIdx.x; j < count; j += kRsThreads) {
+        const uint32_t k = sk[j];
+        const uint32_t pos = gdel[(k >> shift) & (kRadix - 1)] + j;
+        if (kLast) {
+            rec_out[pos] = make_uint2(ss[j], sw[j]);
+            keys_out[pos] = k;
+        } else {
+            keys_out[pos] = k;
+            src_out[pos] = ss[j];
+            w_out[pos] = sw[j];
+        }
     }
 }
 
@@ -136,41 +221,87 @@ __global__ void k_row_offsets(const uint32_t* __restrict__ sorted_dst, uint64_t 
     }
 }
 
-__device__ __forceinline__ uint32_t q31_of(const float* wf, const uint32_t* wq, uint32_t ef) {
-    if (wf) return (uint32_t)floor((double)wf[ef] * 2147483648.0);  // reading C-5, exact in f64
-    return wq[ef];
-}
+// LT: rec[i].y <- inclusive prefix of thr over the row, row sum must be <= 2^31 (reading C-6).
+// A flat segmented scan over the sorted records (segments = equal destination keys), so
+// the work is coalesced and independent of the degree distribution:
+//   k_lt_scan_tiles : per 4096-item tile, in-tile segmented scan (the tile start counts as a
+//                     segment head); tail[t] = local sum of the tile's last segment; checks
+//                     the row sums of the segments that start inside the tile
+//   k_lt_fix_tiles  : per tile, the carry of its first segment from the tiles before it
+//                     (walking back while the key continues), added to that segment; checks
+//                     its row sum where it ends
+constexpr int kLtThreads = 256;
+constexpr int kLtRounds = 16;
+constexpr uint64_t kLtTile = (uint64_t)kLtThreads * kLtRounds;
 
-__global__ void k_gather_records(const uint32_t* __restrict__ order, const uint32_t* __restrict__ srcof,
-                                 const float* __restrict__ wf, const uint32_t* __restrict__ wq, uint64_t m,
-                                 uint2* __restrict__ rec) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t ef = order[i];
-        rec[i] = make_uint2(srcof[ef], q31_of(wf, wq, ef));
-    }
-}
+__device__ __forceinline__ uint32_t sat32(unsigned long long x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
 
-// LT: rec[i].y <- inclusive prefix of thr over the row (warp per row); row sum must be <= 2^31
-__global__ void k_lt_prefix(const uint32_t* __restrict__ roff, uint32_t n, uint2* __restrict__ rec, BuildErr* err) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t v = warp; v < n; v += nwarps) {
-        uint32_t a = roff[v], b = roff[v + 1];
-        unsigned long long carry = 0;
-        for (uint32_t base = a; base < b; base += 32) {
-            uint32_t i = base + lane;
-            unsigned long long x = i < b ? rec[i].y : 0ull;
+__global__ void __launch_bounds__(kLtThreads) k_lt_scan_tiles(const uint32_t* __restrict__ keys, uint64_t m,
+                                                              uint2* __restrict__ rec,
+                                                              unsigned long long* __restrict__ tail, BuildErr* err) {
+    __shared__ unsigned long long wsum[kLtThreads / 32];
+    __shared__ uint32_t wflag[kLtThreads / 32];
+    __shared__ unsigned long long carry_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kLtTile;
+    const uint32_t key0 = keys[tile0];
+    unsigned long long carry = 0;
+    for (int r = 0; r < kLtRounds; ++r) {
+        const uint64_t i = tile0 + (uint64_t)r * kLtThreads + threadIdx.x;
+        const bool in = i < m;
+        const uint32_t k = in ? keys[i] : 0xFFFFFFFFu;
+        uint32_t f = in && (i == tile0 || k != keys[i - 1]);  // segment head (past-the-end items add 0)
+        unsigned long long x = in ? rec[i].y : 0ull;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
-                if (lane >= d) x += y;
-            }
-            unsigned long long c = carry + x;
-            if (i < b) rec[i].y = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
-            carry += __shfl_sync(0xffffffffu, x, 31);
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t fy = __shfl_up_sync(0xffffffffu, f, o);
+            if (lane >= o) { if (!f) x += y; f |= fy; }
         }
-        if (lane == 0 && carry > 0x80000000ull) atomicMin(&err->bad_lt, (unsigned long long)v);
+        if (lane == 31) { wsum[w] = x; wflag[w] = f; }
+        __syncthreads();
+        // prefix of the earlier warps of this round plus the previous round's carry
+        unsigned long long pre = carry;
+        for (int q = 0; q < w; ++q) pre = wflag[q] ? wsum[q] : pre + wsum[q];
+        if (!f) x += pre;
+        if (in) {
+            rec[i].y = sat32(x);
+            const bool end = i + 1 == m || keys[i + 1] != k;
+            if (end && k != key0 && x > 0x80000000ull) atomicMin(&err->bad_lt, (unsigned long long)k);
+        }
+        if (threadIdx.x == kLtThreads - 1) carry_s = x;
+        __syncthreads();
+        carry = carry_s;
+        if (tile0 + (uint64_t)(r + 1) * kLtThreads >= m) break;
+    }
+    if (threadIdx.x == 0) tail[blockIdx.x] = carry;  // the tile's last item: local sum of its last segment
+}
+
+__global__ void __launch_bounds__(kLtThreads) k_lt_fix_tiles(const uint32_t* __restrict__ keys, uint64_t m,
+                                                             uint2* __restrict__ rec,
+                                                             const unsigned long long* __restrict__ tail,
+                                                             BuildErr* err) {
+    __shared__ unsigned long long carry_s;
+    const uint64_t t = blockIdx.x, tile0 = t * kLtTile;
+    const uint64_t tile1 = m - tile0 < kLtTile ? m : tile0 + kLtTile;
+    const uint32_t key0 = keys[tile0];
+    if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        for (uint64_t q = t; q > 0; --q) {  // tile q-1 ends with key0?
+            if (keys[q * kLtTile - 1] != key0) break;
+            c += tail[q - 1];
+            if (keys[(q - 1) * kLtTile] != key0) break;  // its last segment starts inside it
+        }
+        carry_s = c;
+    }
+    __syncthreads();
+    const unsigned long long c = carry_s;
+    for (uint64_t i = tile0 + threadIdx.x; i < tile1; i += kLtThreads) {
+        if (keys[i] != key0) break;  // keys are sorted: the first segment is a prefix of the tile
+        unsigned long long x = rec[i].y;
+        if (c) { x += c; rec[i].y = sat32(x); }
+        const bool end = i + 1 == m || keys[i + 1] != key0;
+        if (end && x > 0x80000000ull) atomicMin(&err->bad_lt, (unsigned long long)key0);
     }
 }
 
@@ -208,39 +339,58 @@ void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_co
     g.roff.alloc(((size_t)n + 1) * sizeof(uint32_t));
     g.rec.alloc((m ? m : 1) * sizeof(uint2));
 
-    // stable LSD radix sort of (dst, forward position) by dst
-    DevBuf k0(m * 4 + 4), k1(m * 4 + 4), v0(m * 4 + 4), v1(m * 4 + 4), srcof(m * 4 + 4);
-    uint32_t *ka = k0.as<uint32_t>(), *kb = k1.as<uint32_t>(), *va = v0.as<uint32_t>(), *vb = v1.as<uint32_t>();
+    // stable LSD radix sort of the forward edges by dst, carrying {src, thr}
+    DevBuf k1(m * 4 + 4), s0(m * 4 + 4), s1(m * 4 + 4), w0(m * 4 + 4), w1(m * 4 + 4), k2(m * 4 + 4);
+    const uint32_t* sorted_keys = d_col;
     if (m) {
-        BPT_CUDA(cudaMemcpyAsync(ka, d_col, m * 4, cudaMemcpyDeviceToDevice, st));
-        k_iota<<<grid_for(m, 256), 256, 0, st>>>(va, m);
-        k_expand_rows<<<grid_for((uint64_t)n * 32, 256), 256, 0, st>>>(d_row_ptr, n, srcof.as<uint32_t>());
-        count_launch(2);
+        k_expand_rows<<<grid_for((uint64_t)n * 32, 256), 256, 0, st>>>(d_row_ptr, n, s0.as<uint32_t>());
+        count_launch();
         int bits = 0;
         while (bits < 32 && (1ull << bits) < (uint64_t)n) ++bits;
+        const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
         const uint64_t ntiles = (m + kRsTile - 1) / kRsTile;
         DevBuf hist(ntiles * kRadix * 4), tmp(scan_temp_bytes(ntiles * kRadix));
-        for (int shift = 0; shift < bits; shift += 8) {
-            k_radix_hist<<<(unsigned)ntiles, kRsThreads, 0, st>>>(ka, m, shift, hist.as<uint32_t>(), ntiles);
+        for (auto fn : {k_radix_pass<true, false>, k_radix_pass<false, false>, k_radix_pass<true, true>,
+                        k_radix_pass<false, true>})
+            BPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
+        const uint32_t* kin = d_col;
+        const uint32_t* sin = s0.as<uint32_t>();
+        const uint32_t* win = d_wq;
+        uint32_t* kbuf[2] = {k1.as<uint32_t>(), k2.as<uint32_t>()};
+        uint32_t* sbuf[2] = {s1.as<uint32_t>(), s0.as<uint32_t>()};
+        uint32_t* wbuf[2] = {w1.as<uint32_t>(), w0.as<uint32_t>()};
+        for (int p = 0; p < passes; ++p) {
+            const int shift = 8 * p;
+            const bool first = p == 0, last = p == passes - 1;
+            k_radix_hist<<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, m, shift, hist.as<uint32_t>(), ntiles);
             count_launch();
             exclusive_scan_u32(hist.as<uint32_t>(), hist.as<uint32_t>(), ntiles * kRadix, tmp.p, st);
-            k_radix_scatter<<<(unsigned)ntiles, kRsThreads, 0, st>>>(ka, va, m, shift, hist.as<uint32_t>(), ntiles,
-                                                                     kb, vb);
+            uint32_t *ko = kbuf[p & 1], *so = sbuf[p & 1], *wo = wbuf[p & 1];
+            const float* wfi = first ? d_wf : nullptr;
+            auto* fn = first ? (last ? k_radix_pass<true, true> : k_radix_pass<true, false>)
+                             : (last ? k_radix_pass<false, true> : k_radix_pass<false, false>);
+            fn<<<(unsigned)ntiles, kRsThreads, kPassSmem, st>>>(kin, sin, wfi, win, m, shift, hist.as<uint32_t>(),
+                                                               ntiles, ko, so, wo, g.rec.as<uint2>());
             count_launch();
-            std::swap(ka, kb);
-            std::swap(va, vb);
+            ::bpt::check_cuda(cudaGetLastError(), "launch k_radix_pass");
+            kin = ko;
+            sin = so;
+            win = wo;
         }
-        k_gather_records<<<grid_for(m, 256), 256, 0, st>>>(va, srcof.as<uint32_t>(), d_wf, d_wq, m,
-                                                            g.rec.as<uint2>());
-        count_launch();
+        sorted_keys = kin;
     }
-    k_row_offsets<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(ka, m, n, g.roff.as<uint32_t>());
+    k_row_offsets<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(sorted_keys, m, n, g.roff.as<uint32_t>());
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_row_offsets");
     if (g.model == BPT_LT && m) {
-        k_lt_prefix<<<grid_for((uint64_t)n * 32, 256), 256, 0, st>>>(g.roff.as<uint32_t>(), n, g.rec.as<uint2>(), err);
-        count_launch();
-        ::bpt::check_cuda(cudaGetLastError(), "launch k_lt_prefix");
+        const uint64_t nt = (m + kLtTile - 1) / kLtTile;
+        DevBuf tail(nt * 8);
+        k_lt_scan_tiles<<<(unsigned)nt, kLtThreads, 0, st>>>(sorted_keys, m, g.rec.as<uint2>(),
+                                                            tail.as<unsigned long long>(), err);
+        k_lt_fix_tiles<<<(unsigned)nt, kLtThreads, 0, st>>>(sorted_keys, m, g.rec.as<uint2>(),
+                                                           tail.as<unsigned long long>(), err);
+        count_launch(2);
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_lt_fix_tiles");
         BPT_CUDA(cudaMemcpyAsync(&h, err, sizeof(BuildErr), cudaMemcpyDeviceToHost, st));
         BPT_CUDA(cudaStreamSynchronize(st));
         if (h.bad_lt != ~0ull)

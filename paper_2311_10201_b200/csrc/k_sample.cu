@@ -1186,7 +1186,9 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
                                                         const uint2* __restrict__ rec, uint64_t s0, uint64_t nlocal,
                                                         uint32_t k_start, uint32_t k_lt,
                                                         uint32_t* __restrict__ sizes, uint32_t* __restrict__ count0,
-                                                        unsigned long long* __restrict__ totals) {
+                                                        unsigned long long* __restrict__ totals,
+                                                        uint32_t* __restrict__ rows) {
+    // rows (optional): member i of local sample l at rows[l * kWalkMax + i], in walk order
     uint32_t ht[kWalkHash];
     unsigned long long members = 0;
     uint32_t longest = 0, too_long = 0;
@@ -1207,13 +1209,16 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
         uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
         insert(v);
         atomicAdd(&count0[v], 1u);
+        uint32_t* row = rows ? rows + i * kWalkMax : nullptr;
+        if (row) row[0] = v;
         uint32_t size = 1, u = 0;
         while (lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
             if (!insert(u)) break;  // already in RR_s
             atomicAdd(&count0[u], 1u);
+            if (size >= kWalkMax) { too_long = 1; break; }
+            if (row) row[size] = u;
             ++size;
             v = u;
-            if (size >= kWalkMax) { too_long = 1; break; }
         }
         sizes[i] = size;
         members += size;
@@ -1229,6 +1234,17 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
         if (members) atomicAdd(&totals[0], members);
         if (longest) atomicMax(&totals[1], (unsigned long long)longest);
         if (too_long) atomicMax(&totals[2], 1ull);
+    }
+}
+
+// rows (walk order, kWalkMax-strided) -> contiguous member lists at off[l]
+__global__ void k_rows_to_lists(const uint32_t* __restrict__ rows, const uint64_t* __restrict__ off, uint64_t nlists,
+                                uint32_t* __restrict__ members) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t l = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; l < nlists;
+         l += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint64_t b = off[l], len = off[l + 1] - b;
+        for (uint64_t j = lane; j < len; j += 32) members[b + j] = rows[l * kWalkMax + j];
     }
 }
 
@@ -1468,11 +1484,22 @@ void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uin
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt");
 }
 
+uint32_t walk_row_stride() { return kWalkMax; }
+
+void launch_rows_to_lists(const uint32_t* rows, const uint64_t* off, uint64_t nlists, uint32_t* members, cudaStream_t st) {
+    const unsigned grid = (unsigned)umin64((nlists * 32 + 255) / 256, (uint64_t)num_sms() * 16);
+    if (!grid) return;
+    k_rows_to_lists<<<grid, 256, 0, st>>>(rows, off, nlists, members);
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_rows_to_lists");
+}
+
 void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
-                           unsigned long long* totals, cudaStream_t st) {
+                           unsigned long long* totals, uint32_t* rows, cudaStream_t st) {
     const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
-    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals);
+    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals,
+                                                      rows);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_sparse");
 }

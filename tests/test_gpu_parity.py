@@ -84,6 +84,50 @@ def test_reverse_csr_multigraph_and_lt_prefix(bpt):
     assert np.array_equal(cum.astype(np.uint64), want)
 
 
+def _hub_graph(n, hubs, others, seed):
+    """Forward CSR with `hubs` = {v: in-degree} heavy rows (spanning several 4096-item builder
+    tiles) plus `others` random edges; rows by source, duplicates kept."""
+    rng = np.random.default_rng(seed)
+    v = np.concatenate([np.full(d, h, np.int64) for h, d in hubs.items()] + [rng.integers(0, n, others)])
+    u = rng.integers(0, n, v.shape[0])
+    order = np.argsort(u, kind="stable")
+    u, v = u[order], v[order]
+    row_ptr = np.zeros(n + 1, np.uint64)
+    np.add.at(row_ptr, u + 1, 1)
+    return np.cumsum(row_ptr).astype(np.uint64), v.astype(np.uint32)
+
+
+def test_reverse_csr_hub_rows_across_tiles(bpt):
+    """Three 8-bit radix passes (n > 2^16) and in-degree hubs spanning many builder tiles:
+    the payload-carrying sort keeps the stable order (C-4) and the LT segmented scan carries
+    row prefixes across tiles (C-6)."""
+    n = 70000
+    row_ptr, col = _hub_graph(n, {5: 30000, n - 1: 9000, 4097: 4097}, 20000, seed=3)
+    rng = np.random.default_rng(4)
+    indeg = np.bincount(col, minlength=n)
+    thr = (rng.random(col.shape[0]) * (Q31 // np.maximum(indeg[col], 1))).astype(np.uint32)
+    for model, omodel in ((bpt.IC, oracle.IC), (bpt.LT, oracle.LT)):
+        g = bpt.Graph(row_ptr, col, w_q31=thr, model=model)
+        roff, src, got = g.reverse_csr()
+        o_roff, o_src, o_thr = oracle.Graph(row_ptr, col, w_q31=thr, model=omodel).reverse_csr()
+        assert np.array_equal(roff.astype(np.uint64), o_roff)
+        assert np.array_equal(src, o_src)
+        if model == bpt.IC:
+            assert np.array_equal(got, o_thr)
+        else:
+            seg = np.repeat(np.arange(n), np.diff(o_roff.astype(np.int64)))
+            c = np.cumsum(o_thr.astype(np.uint64))
+            start = np.concatenate([[0], c])[o_roff[:-1].astype(np.int64)]
+            assert np.array_equal(got.astype(np.uint64), c - start[seg])
+        g.close()
+    # an LT row whose sum passes 2^31 only in its last tile is rejected with its vertex id
+    bad = thr.copy()
+    bad[col == 5] = Q31 // 30000 + 1
+    with pytest.raises(bpt.BptError) as ei:
+        bpt.Graph(row_ptr, col, w_q31=bad, model=bpt.LT)
+    assert "vertex 5 " in str(ei.value)
+
+
 def test_invalid_inputs_rejected(bpt):
     rp = np.array([0, 2, 3], np.uint64)
     col = np.array([1, 0, 1], np.uint32)
@@ -291,6 +335,7 @@ def test_level_loop_variants(bpt, monkeypatch, model):
         g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
         variants = [{"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "0"}, {"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "1"},
                     {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "0"},   # walks, sparse store (default)
+                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "0", "BPT_LT_REWALK": "1"},  # lists by a 2nd walk
                     {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "1"}]   # walks, dense store
     infos = []
     for env in variants:
@@ -306,7 +351,8 @@ def test_level_loop_variants(bpt, monkeypatch, model):
             walker = model == "LT" and env.get("BPT_LT_FUSED") == "0"
             if walker:
                 dense_bytes = (cfg.theta + 63) // 64 * cfg.n * 8
-                assert (info["store_bytes"] >= dense_bytes) == (env["BPT_LT_DENSE"] == "1")  # bitmap vs lists
+                assert (info["store_bytes"] >= dense_bytes) == (env["BPT_LT_DENSE"] == "1")
+                monkeypatch.delenv("BPT_LT_REWALK", raising=False)  # bitmap vs lists
             rows.append((info["e_phys"], info["e_logical"], info["members"]) if walker else
                         (colors, batch, info["e_phys"], info["e_logical"], info["members"], info["levels_total"]))
             s.close()
