@@ -140,7 +140,7 @@ typedef struct {
  * frontier, so each reverse edge of a frontier vertex is read once for 128 samples. Same RRR
  * sets (coins are keyed by the global sample id); E_phys counts the 128-sample groups. */
 #define BPT_FLAG_WIDE 2u
-/* LT only: REQUIRE the sparse store -- the RRR sets kept as sorted member lists instead of the
+/* LT only: REQUIRE the sparse store -- the RRR sets kept as member lists instead of the
  * dense n x blocks bitmap (SURVEY A5 "compressed rows": C3 ~0.1 GB instead of 100 GB). LT uses
  * it by default too, falling back to the dense store when a walk outgrows the per-thread
  * visited set (1,536 vertices); with this flag that case fails with ENOMEM instead. Sizes,

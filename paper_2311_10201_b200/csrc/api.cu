@@ -272,9 +272,8 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
                                 uint64_t launches0) {
     const Graph& g = *S.g;
     const uint64_t nlocal = S.s1 - S.s0;
-    DevBuf totals(24), err(4), rows;
+    DevBuf totals(24), rows;
     BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
-    BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
     {  // walk-order rows written during the walk when they fit a quarter of the free memory,
        // else the lists come from a second walk
         size_t fb = 0, tb = 0;
@@ -312,12 +311,9 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
     } else {
         lt_lists_by_rewalk(S, st);
     }
-    launch_sort_lists(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nlocal, err.as<uint32_t>(), st);
-    uint32_t h_err = 0;
-    BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+    // lists stay in walk order: sizes, digests and the selection do not depend on the order;
+    // bpt_rrr_extract sorts the range it returns
     BPT_CUDA(cudaStreamSynchronize(st));
-    if (h_err) fail(BPT_ENOMEM, "an LT walk is longer than the sparse store's list sort; sample without "
-                                "BPT_FLAG_SPARSE");
     if (getenv("BPT_TRACE"))
         fprintf(stderr, "[bpt] LT sparse: rows %s, walk ends %.2f ms, lists+sort end %.2f ms after call start\n",
                 rows.p ? "yes" : "no", t_walk_ms, std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count());
@@ -872,7 +868,14 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         if (capacity < total)
             fail(BPT_ENOMEM, "members capacity " + std::to_string(capacity) + " < required " + std::to_string(total));
         if (total && !members) fail(BPT_EINVAL, "members is NULL");
-        if (total && S.sparse) {  // the store is the sorted lists: one contiguous slice
+        if (total && S.sparse) {  // the store is the member lists: sort the range, one contiguous slice
+            DevBuf err(4);
+            BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, 0));
+            launch_sort_lists(S.list_off.as<uint64_t>() + (first - S.s0), const_cast<uint32_t*>(S.list_mem.as<uint32_t>()),
+                              count, err.as<uint32_t>(), 0);
+            uint32_t h_err = 0;
+            BPT_CUDA(cudaMemcpy(&h_err, err.p, 4, cudaMemcpyDeviceToHost));
+            if (h_err) fail(BPT_ESTATE, "member list longer than the list sort");
             uint64_t b = 0;
             BPT_CUDA(cudaMemcpy(&b, S.list_off.as<uint64_t>() + (first - S.s0), 8, cudaMemcpyDeviceToHost));
             BPT_CUDA(cudaMemcpy(members, S.list_mem.as<uint32_t>() + b, total * 4, cudaMemcpyDefault));

@@ -32,11 +32,21 @@ __global__ void __launch_bounds__(kSelThreads) k_argmax(const uint32_t* __restri
                                                         uint32_t* __restrict__ nlist) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *nlist = 0;
     unsigned long long best = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = vbase + i;
-        if (v >= n || selected[v]) continue;
-        const unsigned long long k = ((unsigned long long)count[i] << 32) | (unsigned long long)(~(uint32_t)v);
-        best = k > best ? k : best;
+    // four vertices per thread: one 16-B load of counts, one 4-B load of selected flags
+    // (vbase is a multiple of 64; count and selected are padded to a multiple of 4)
+    const uint4* c4 = reinterpret_cast<const uint4*>(count);
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(selected + vbase);
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; 4 * q < len; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 c = c4[q];
+        const uint32_t sl = s4[q];
+        const uint32_t cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint64_t v = vbase + 4 * q + e;
+            if (v >= n || 4 * q + e >= len || ((sl >> (8 * e)) & 0xffu)) continue;
+            const unsigned long long k = ((unsigned long long)cv[e] << 32) | (unsigned long long)(~(uint32_t)v);
+            best = k > best ? k : best;
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -131,8 +141,10 @@ __global__ void k_widen_u32(const uint32_t* __restrict__ in, uint64_t* __restric
 __global__ void k_inv_scatter(const uint64_t* __restrict__ off, const uint32_t* __restrict__ members, uint64_t nlists,
                               const uint64_t* __restrict__ inv_off, uint32_t* __restrict__ cursor,
                               uint32_t* __restrict__ inv_s) {
-    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < nlists; l += (uint64_t)gridDim.x * blockDim.x)
-        for (uint64_t j = off[l]; j < off[l + 1]; ++j) {
+    const int lane = threadIdx.x & 31;  // one warp per list, lanes over its members
+    for (uint64_t l = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; l < nlists;
+         l += ((uint64_t)gridDim.x * blockDim.x) >> 5)
+        for (uint64_t j = off[l] + lane; j < off[l + 1]; j += 32) {
             const uint32_t w = members[j];
             inv_s[inv_off[w] + atomicAdd(&cursor[w], 1u)] = (uint32_t)l;
         }
@@ -148,10 +160,14 @@ __global__ void k_cover_sparse(const unsigned long long* __restrict__ key, const
     if (blockIdx.x == 0 && threadIdx.x == 0) selected[vstar] = 1;
     if (*key == 0) return;  // no gain left on any rank's shard: nothing to cover
     const uint64_t b = inv_off[vstar], e = inv_off[vstar + 1];
-    for (uint64_t j = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e; j += (uint64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;  // one warp per sample containing v*, lanes over its members
+    for (uint64_t j = b + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); j < e;
+         j += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t l = inv_s[j];
-        if (atomicExch(&covered[l], 1u)) continue;
-        for (uint64_t t = off[l]; t < off[l + 1]; ++t) atomicSub(&count[members[t]], 1u);
+        uint32_t was = 0;
+        if (lane == 0) was = atomicExch(&covered[l], 1u);
+        if (__shfl_sync(0xffffffffu, was, 0)) continue;
+        for (uint64_t t = off[l] + lane; t < off[l + 1]; t += 32) atomicSub(&count[members[t]], 1u);
     }
 }
 
@@ -195,13 +211,13 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     Comm* comm = S.comm;
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
     const uint64_t blocks = S.blocks;
-    DevBuf count((uint64_t)S.n_pad * 4), shard(world > 1 ? (uint64_t)S.n_pad / world * 4 : 4), sel(n),
+    DevBuf count((uint64_t)S.n_pad * 4), shard(world > 1 ? (uint64_t)S.n_pad / world * 4 : 4), sel(S.n_pad),
         cov(blocks * 8 + 8), list(blocks * 4 + 4), newm(blocks * 8 + 8), nlist(4), keys((uint64_t)k * 8);
     BPT_CUDA(cudaMemcpyAsync(count.p, S.count0.p, (uint64_t)S.n_pad * 4, cudaMemcpyDeviceToDevice, st));
-    BPT_CUDA(cudaMemsetAsync(sel.p, 0, n, st));
+    BPT_CUDA(cudaMemsetAsync(sel.p, 0, S.n_pad, st));
     BPT_CUDA(cudaMemsetAsync(cov.p, 0, blocks * 8 + 8, st));
     BPT_CUDA(cudaMemsetAsync(keys.p, 0, (uint64_t)k * 8, st));
-    const unsigned vgrid = (unsigned)umin64(((uint64_t)n + kSelThreads - 1) / kSelThreads, (uint64_t)num_sms() * 4);
+    const unsigned vgrid = (unsigned)umin64(((uint64_t)n + 4 * kSelThreads - 1) / (4 * kSelThreads), (uint64_t)num_sms() * 4);
     const unsigned ggrid = (unsigned)umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4);
     const unsigned dgrid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
     const uint64_t shard_len = (uint64_t)S.n_pad / world;
@@ -226,7 +242,7 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
             DevBuf cursor((uint64_t)n * 4);
             BPT_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes, st));
             const uint64_t nl = S.s1 - S.s0;
-            const unsigned g = (unsigned)umin64((nl + 255) / 256, (uint64_t)num_sms() * 8);
+            const unsigned g = (unsigned)umin64((nl * 32 + 255) / 256, (uint64_t)num_sms() * 16);
             if (g) k_inv_scatter<<<g, 256, 0, st>>>(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nl,
                                                     M.inv_off.as<uint64_t>(), cursor.as<uint32_t>(),
                                                     M.inv_s.as<uint32_t>());
