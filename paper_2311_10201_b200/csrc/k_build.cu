@@ -75,35 +75,27 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
     return p;
 }
 
-// per-warp digit counts of one tile into smem cnt[warp][digit]
-__device__ __forceinline__ void tile_warp_counts(const uint32_t* __restrict__ keys, uint64_t m, int shift,
-                                                 uint32_t (*cnt)[kRadix]) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t)blockIdx.x * kRsTile + (uint64_t)w * (32 * kRsRounds);
-    uint32_t key[kRsRounds];
-#pragma unroll
-    for (int r = 0; r < kRsRounds; ++r) {  // all loads in flight before the first ballot
-        const uint64_t i = base + (uint64_t)r * 32 + lane;
-        key[r] = i < m ? keys[i] : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < kRsRounds; ++r) {
-        uint64_t i = base + (uint64_t)r * 32 + lane;
-        uint32_t d = i < m ? (key[r] >> shift) & (kRadix - 1) : kRadix;
-        uint32_t peers = digit_peers(d);
-        if (d < kRadix && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
-    }
-}
-
+// Per-tile digit counts need no stable ranks: one shared-memory atomic per item into the
+// warp's own histogram (the ballot ranking costs ~30 instructions per 32 items)
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t* __restrict__ keys, uint64_t m, int shift,
                                                            uint32_t* __restrict__ hist, uint64_t ntiles) {
     __shared__ uint32_t cnt[kRsWarps][kRadix];
     for (int i = threadIdx.x; i < kRsWarps * kRadix; i += kRsThreads) (&cnt[0][0])[i] = 0;
     __syncthreads();
-    tile_warp_counts(keys, m, shift, cnt);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t base = (uint64_t)blockIdx.x * kRsTile + (uint64_t)w * (32 * kRsRounds);
+    uint32_t key[kRsRounds];
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r) {
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        key[r] = i < m ? keys[i] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r)
+        if (base + (uint64_t)r * 32 + lane < m) atomicAdd(&cnt[w][(key[r] >> shift) & (kRadix - 1)], 1u);
     __syncthreads();
     uint32_t s = 0;
-    for (int w = 0; w < kRsWarps; ++w) s += cnt[w][threadIdx.x];
+    for (int q = 0; q < kRsWarps; ++q) s += cnt[q][threadIdx.x];
     hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = s;  // digit-major
 }
 
@@ -239,42 +231,90 @@ __device__ __forceinline__ uint32_t sat32(unsigned long long x) { return x > 0xF
 __global__ void __launch_bounds__(kLtThreads) k_lt_scan_tiles(const uint32_t* __restrict__ keys, uint64_t m,
                                                               uint2* __restrict__ rec,
                                                               unsigned long long* __restrict__ tail, BuildErr* err) {
+    // thread t owns the kLtRounds consecutive items i0 .. i0 + 15 (vector loads), a sequential
+    // segmented scan over them, then one block-wide segmented scan of the thread aggregates
     __shared__ unsigned long long wsum[kLtThreads / 32];
     __shared__ uint32_t wflag[kLtThreads / 32];
-    __shared__ unsigned long long carry_s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t tile0 = (uint64_t)blockIdx.x * kLtTile;
+    const uint64_t i0 = tile0 + (uint64_t)threadIdx.x * kLtRounds;
     const uint32_t key0 = keys[tile0];
-    unsigned long long carry = 0;
-    for (int r = 0; r < kLtRounds; ++r) {
-        const uint64_t i = tile0 + (uint64_t)r * kLtThreads + threadIdx.x;
-        const bool in = i < m;
-        const uint32_t k = in ? keys[i] : 0xFFFFFFFFu;
-        uint32_t f = in && (i == tile0 || k != keys[i - 1]);  // segment head (past-the-end items add 0)
-        unsigned long long x = in ? rec[i].y : 0ull;
+    uint32_t k[kLtRounds + 1];
+    uint2 r2[kLtRounds];
+    if (i0 + kLtRounds <= m) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            const uint32_t fy = __shfl_up_sync(0xffffffffu, f, o);
-            if (lane >= o) { if (!f) x += y; f |= fy; }
+        for (int j = 0; j < kLtRounds; j += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(keys + i0 + j);
+            k[j] = q.x; k[j + 1] = q.y; k[j + 2] = q.z; k[j + 3] = q.w;
         }
-        if (lane == 31) { wsum[w] = x; wflag[w] = f; }
-        __syncthreads();
-        // prefix of the earlier warps of this round plus the previous round's carry
-        unsigned long long pre = carry;
-        for (int q = 0; q < w; ++q) pre = wflag[q] ? wsum[q] : pre + wsum[q];
-        if (!f) x += pre;
-        if (in) {
-            rec[i].y = sat32(x);
-            const bool end = i + 1 == m || keys[i + 1] != k;
-            if (end && k != key0 && x > 0x80000000ull) atomicMin(&err->bad_lt, (unsigned long long)k);
+#pragma unroll
+        for (int j = 0; j < kLtRounds; j += 2) {
+            const uint4 q = *reinterpret_cast<const uint4*>(rec + i0 + j);
+            r2[j] = make_uint2(q.x, q.y); r2[j + 1] = make_uint2(q.z, q.w);
         }
-        if (threadIdx.x == kLtThreads - 1) carry_s = x;
-        __syncthreads();
-        carry = carry_s;
-        if (tile0 + (uint64_t)(r + 1) * kLtThreads >= m) break;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kLtRounds; ++j) {
+            const bool in = i0 + j < m;
+            k[j] = in ? keys[i0 + j] : 0xFFFFFFFFu;
+            r2[j] = in ? rec[i0 + j] : make_uint2(0u, 0u);
+        }
     }
-    if (threadIdx.x == 0) tail[blockIdx.x] = carry;  // the tile's last item: local sum of its last segment
+    k[kLtRounds] = i0 + kLtRounds < m ? keys[i0 + kLtRounds] : 0xFFFFFFFFu;  // for the segment-end test
+    const uint32_t kprev = i0 > tile0 && i0 <= m ? keys[i0 - 1] : 0u;
+    unsigned long long x[kLtRounds];
+    unsigned long long run = 0;
+    int first_head = kLtRounds;  // index of the first segment head among the thread's items
+#pragma unroll
+    for (int j = kLtRounds - 1; j >= 0; --j) {
+        const uint64_t i = i0 + j;
+        const bool head = i < m && (i == tile0 || k[j] != (j ? k[j - 1] : kprev));
+        if (head) first_head = j;
+    }
+#pragma unroll
+    for (int j = 0; j < kLtRounds; ++j) {
+        const uint64_t i = i0 + j;
+        const bool head = i < m && (i == tile0 || k[j] != (j ? k[j - 1] : kprev));
+        if (head) run = 0;
+        run += i < m ? r2[j].y : 0u;
+        x[j] = run;
+    }
+    // block-wide exclusive segmented scan of (has head, run)
+    uint32_t f = first_head < kLtRounds;
+    unsigned long long agg = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, agg, o);
+        const uint32_t fy = __shfl_up_sync(0xffffffffu, f, o);
+        if (lane >= o) { if (!f) agg += y; f |= fy; }
+    }
+    if (lane == 31) { wsum[w] = agg; wflag[w] = f; }
+    const unsigned long long ex = __shfl_up_sync(0xffffffffu, agg, 1);
+    const uint32_t exf = __shfl_up_sync(0xffffffffu, f, 1);
+    __syncthreads();
+    unsigned long long pre = 0;  // exclusive prefix of the earlier warps
+    for (int q = 0; q < w; ++q) pre = wflag[q] ? wsum[q] : pre + wsum[q];
+    const unsigned long long carry = lane == 0 ? pre : (exf ? ex : pre + ex);
+    const uint64_t last = (m - tile0 < kLtTile ? m : tile0 + kLtTile) - 1;
+#pragma unroll
+    for (int j = 0; j < kLtRounds; ++j) {
+        const uint64_t i = i0 + j;
+        if (j < first_head) x[j] += carry;
+        if (i < m) {
+            const bool end = i + 1 == m || k[j + 1] != k[j];
+            if (end && k[j] != key0 && x[j] > 0x80000000ull) atomicMin(&err->bad_lt, (unsigned long long)k[j]);
+            if (i == last) tail[blockIdx.x] = x[j];  // local sum of the tile's last segment
+            r2[j].y = sat32(x[j]);
+        }
+    }
+    if (i0 + kLtRounds <= m) {
+#pragma unroll
+        for (int j = 0; j < kLtRounds; j += 2)
+            *reinterpret_cast<uint4*>(rec + i0 + j) = make_uint4(r2[j].x, r2[j].y, r2[j + 1].x, r2[j + 1].y);
+    } else {
+        for (int j = 0; j < kLtRounds; ++j)
+            if (i0 + j < m) rec[i0 + j] = r2[j];
+    }
 }
 
 __global__ void __launch_bounds__(kLtThreads) k_lt_fix_tiles(const uint32_t* __restrict__ keys, uint64_t m,
