@@ -205,6 +205,19 @@ static bool env_is(const char* name, char c) {
     return v && v[0] == c;
 }
 
+static uint64_t device_total_bytes() {  // cached per device
+    static uint64_t total[64] = {};
+    int d = 0;
+    BPT_CUDA(cudaGetDevice(&d));
+    if (d < 0 || d >= 64) d = 0;
+    if (!total[d]) {
+        cudaDeviceProp p{};
+        BPT_CUDA(cudaGetDeviceProperties(&p, d));
+        total[d] = p.totalGlobalMem;
+    }
+    return total[d];
+}
+
 // timing of one walk launch (events released on every path)
 struct WalkTimer {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -274,18 +287,28 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
     const uint64_t nlocal = S.s1 - S.s0;
     DevBuf totals(24), rows;
     BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
-    {  // walk-order rows written during the walk when they fit a quarter of the free memory,
-       // else the lists come from a second walk
-        size_t fb = 0, tb = 0;
-        BPT_CUDA(cudaMemGetInfo(&fb, &tb));
+    auto since = [&]() { return std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count(); };
+    const double t_pre = since();
+    if (!env_is("BPT_LT_REWALK", '1')) {
+        // walk-order rows written during the walk (6 KB per sample) when they fit a quarter of
+        // the device memory and the allocation succeeds, else the lists come from a second walk
+        // (no cudaMemGetInfo here: it stalled the call for 10-40 ms at times)
         const uint64_t bytes = nlocal * (uint64_t)walk_row_stride() * 4;
-        if (bytes < (fb + cached_bytes()) / 4 && !env_is("BPT_LT_REWALK", '1')) rows.alloc(bytes);
+        if (bytes < device_total_bytes() / 4) {
+            try {
+                rows.alloc(bytes);
+            } catch (const Error& e) {
+                if (e.code != BPT_ENOMEM) throw;
+            }
+        }
     }
+    const double t_alloc = since();
     WalkTimer tm(st);
     launch_walk_lt_sparse(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, stream_key(S.seed, kTagStart),
                           stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(),
                           totals.as<unsigned long long>(), rows.p ? rows.as<uint32_t>() : nullptr, st);
     tm.stop(st);
+    const double t_launch = since();
     unsigned long long tot[3] = {0, 0, 0};
     BPT_CUDA(cudaMemcpyAsync(tot, totals.p, 24, cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
@@ -315,8 +338,8 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
     // bpt_rrr_extract sorts the range it returns
     BPT_CUDA(cudaStreamSynchronize(st));
     if (getenv("BPT_TRACE"))
-        fprintf(stderr, "[bpt] LT sparse: rows %s, walk ends %.2f ms, lists+sort end %.2f ms after call start\n",
-                rows.p ? "yes" : "no", t_walk_ms, std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count());
+        fprintf(stderr, "[bpt] LT sparse: rows %s, set-up %.2f, rows alloc %.2f, launched %.2f, walk ends %.2f, "
+                "lists end %.2f ms after call start\n", rows.p ? "yes" : "no", t_pre, t_alloc, t_launch, t_walk_ms, since());
     S.sparse = true;
     lt_walk_info(S, tot, tm.ms(), launches0, t_begin, "LT sparse walks");
     return true;
