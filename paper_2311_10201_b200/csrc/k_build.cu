@@ -20,10 +20,10 @@ namespace {
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 #ifndef BPT_RS_ROUNDS
-#define BPT_RS_ROUNDS 8
+#define BPT_RS_ROUNDS 12
 #endif
 #ifndef BPT_RS_MINB
-#define BPT_RS_MINB 4
+#define BPT_RS_MINB 3
 #endif
 constexpr int kRsRounds = BPT_RS_ROUNDS;                       // 32-item rounds per warp
 constexpr uint64_t kRsTile = (uint64_t)kRsThreads * kRsRounds; // 4096 items per tile
@@ -105,10 +105,10 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t* __res
     hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = s;  // digit-major
 }
 
-// One stable LSD pass over a 2048-item tile, the (src, thr) payload carried with the key so
+// One stable LSD pass over a 3072-item tile, the (src, thr) payload carried with the key so
 // the sorted records need no gather through a permutation afterwards. The tile is ranked in
 // registers (per-warp ballot rounds), reordered by digit in shared memory, and
-// written out in that order: the items of one digit leave as one contiguous run (8 items on
+// written out in that order: the items of one digit leave as one contiguous run (12 items on
 // average at 8-bit digits) instead of 32 scattered 4-byte stores per warp round.
 // kFirst: payload read from (srcof, weights); kLast: records written as uint2 {src, thr}.
 constexpr size_t kPassSmem = (size_t)kRsTile * 12 + (size_t)kRsWarps * kRadix * 4 + kRadix * 8;
