@@ -42,6 +42,7 @@ METRICS = {  # per config (the default C2 line keeps the name above)
 UNIT = "RRR sets/s"
 CFG = graphgen.CONFIGS["C2"]
 EXTRACT_SAMPLES = 64
+PER_MEMBER_BYTES_LT = "24 B per RRR member (8 B row bounds + 8 B chosen in-edge record + 8 B visited-set insertion)"
 PER_EDGE_BYTES = "16 B per reverse-edge read (8 B {src,thr} record + 8 B V[u] gather) + 8 B per atomicOr + 24 B per frontier entry + 8 B per enqueued entry"
 
 
@@ -79,7 +80,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -89,6 +90,16 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi has produced its first sample (so short timed regions are covered)."""
+        t_end = time.time() + timeout
+        while self.proc and not self.lines and time.time() < t_end:
+            time.sleep(0.01)
+
+    def mark(self):
+        """Start of the timed region: samples before it are dropped."""
+        self.first = len(self.lines)
 
     def stop(self) -> dict:
         if not self.proc:
@@ -100,7 +111,10 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        first = getattr(self, "first", 0)
+        if len(self.lines) <= first:  # region shorter than one sampling period: keep the sample after it
+            first = max(0, first - 1)
+        for line in self.lines[first:]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -126,9 +140,9 @@ def measured_peak_hbm() -> tuple[float, str]:
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def ncu_traffic_per_launch():
-    """dram read+write bytes per expansion launch from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "expand_traffic.json")
+def ncu_traffic_per_launch(name: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", name)
     try:
         with open(p) as f:
             d = json.load(f)
@@ -267,10 +281,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         step(False)
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
+    clocks.start()
+    clocks.wait_first()
     launches0 = bpt.kernel_launch_count()
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -366,8 +382,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return
     peak, peak_src = measured_peak_hbm()
     achieved = expand_bytes / (ms_expand / 1000.0) / 1e9 if ms_expand > 0 else None
-    traffic, alg_ncu, traffic_src = ncu_traffic_per_launch()
-    roofline = {"bound": "hbm", "kernel": "k_expand_ic (A3 fused frontier expansion)",
+    if cfg.model == "IC":
+        traffic, alg_ncu, traffic_src = ncu_traffic_per_launch("expand_traffic.json")
+        kernel, per_unit = "k_expand_ic (A3 fused frontier expansion)", PER_EDGE_BYTES
+    else:  # LT: one reverse walk per sample into the sparse member-list store
+        traffic, alg_ncu, traffic_src = ncu_traffic_per_launch("walk_lt_traffic.json")
+        kernel, per_unit = "k_walk_lt_sparse (A3' LT reverse walks, sparse store)", PER_MEMBER_BYTES_LT
+    roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_launch": expand_bytes / expand_launches if expand_launches else None,
@@ -378,7 +399,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "timing": "CUDA events around every expansion launch of one extra step run right after the "
                           "timed region (host-driven loop); the timed steps themselves run the graph loop and "
                           "report the device %globaltimer span of every launch (achieved_timed_region)",
-                "peak_source": peak_src, "per_unit": PER_EDGE_BYTES, "traffic_source": traffic_src}
+                "peak_source": peak_src, "per_unit": per_unit, "traffic_source": traffic_src}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, row_ptr, col, thr, args.cpu_samples or None)
