@@ -221,7 +221,7 @@ void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uin
                     cudaStream_t st);
 // LT sparse store: walks with a per-thread visited hash set (no dense store); sizes, count0,
 // totals[0..1] as launch_walk_lt, totals[2] = 1 if a walk outgrew the hash set
-void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
                            unsigned long long* totals, uint32_t* rows, cudaStream_t st);
 // walk-order member rows (optional output of the sparse walk: stride walk_row_stride()) -> lists

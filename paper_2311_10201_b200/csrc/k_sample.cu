@@ -1117,6 +1117,65 @@ __device__ __forceinline__ bool lt_pick(const uint32_t* __restrict__ roff, const
     return true;
 }
 
+// The same pick with fewer dependent loads (the walk kernel's time is the critical path of its
+// longest walks, a chain of dependent DRAM round trips per step): the first guess assumes the
+// row sum is ~2^31 (normalised LT weights; any guess gives the same answer, only the number of
+// round trips depends on it) and one 64-B window of 8 records around it is loaded at once. The
+// answer is the first j in [lo, hi) with cum[j] > r (none if r >= cum[hi - 1]) exactly as in
+// lt_pick; when it is not inside the window the search continues on the side it lies.
+__device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, const uint2* __restrict__ rec,
+                                            uint32_t m, uint32_t v, uint32_t r, uint32_t* u_out) {
+    uint32_t lo = __ldg(&roff[v]), hi = __ldg(&roff[v + 1]);
+    if (lo >= hi) return false;
+    uint32_t g = lo + (uint32_t)(((uint64_t)r * (hi - lo)) >> 31);
+    g = min(g, hi - 1);
+    const uint32_t w0 = (g >= 3 ? g - 3 : 0u) & ~1u;  // 16-B aligned
+    if (w0 + 8 > m) return lt_pick(roff, rec, v, r, u_out);
+    const uint4* wp = reinterpret_cast<const uint4*>(rec + w0);
+    const uint4 q0 = __ldg(wp), q1 = __ldg(wp + 1), q2 = __ldg(wp + 2), q3 = __ldg(wp + 3);
+    const uint32_t xs[8] = {q0.x, q0.z, q1.x, q1.z, q2.x, q2.z, q3.x, q3.z};
+    const uint32_t ys[8] = {q0.y, q0.w, q1.y, q1.w, q2.y, q2.w, q3.y, q3.w};
+    const uint32_t a = max(lo, w0), b = min(hi, w0 + 8);  // window part inside the row (a < b)
+    uint32_t k = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) k += (w0 + j >= a && w0 + j < b && ys[j] <= r) ? 1u : 0u;
+    const uint32_t j = a + k;  // first index of [a, b) with cum > r, b if none
+    uint32_t clo, chi;
+    uint2 hit;
+    if (j < b) {
+        if (j > a || a == lo) {  // cum[j - 1] <= r < cum[j] (or j == lo)
+            *u_out = xs[j - w0];
+            return true;
+        }
+        // cum[a] > r, a > lo: the answer is in [lo, a]
+        hi = a + 1;
+        chi = ys[a - w0];
+        hit = make_uint2(xs[a - w0], chi);
+        clo = 0;
+    } else {
+        if (b == hi) return false;  // r >= cum[hi - 1]: no in-edge chosen
+        clo = ys[b - 1 - w0];     // cum[b - 1] <= r: the answer is in [b, hi)
+        lo = b;
+        hit = __ldg(&rec[hi - 1]);
+        if (r >= hit.y) return false;
+        chi = hit.y;
+    }
+    for (int step = 0; hi - lo > 1; ++step) {
+        uint32_t gg;
+        if (step < 4) {
+            gg = lo + (uint32_t)((uint64_t)(r - clo) * (hi - lo) / (uint64_t)(chi - clo));
+            gg = min(gg, hi - 2);
+        } else {
+            gg = (lo + hi - 1) >> 1;
+        }
+        const uint2 x = __ldg(&rec[gg]);
+        if (x.y > r) { hi = gg + 1; chi = x.y; hit = x; }
+        else { lo = gg + 1; clo = x.y; }
+    }
+    *u_out = hit.x;
+    return true;
+}
+
 __global__ void __launch_bounds__(256) k_walk_lt(uint64_t* __restrict__ store, uint32_t n,
                                                  const uint32_t* __restrict__ roff, const uint2* __restrict__ rec,
                                                  uint64_t s0, uint64_t nlocal, uint32_t k_start, uint32_t k_lt,
@@ -1183,7 +1242,8 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
 constexpr uint32_t kWalkHash = 2048, kWalkMax = 1536;
 
 __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32_t* __restrict__ roff,
-                                                        const uint2* __restrict__ rec, uint64_t s0, uint64_t nlocal,
+                                                        const uint2* __restrict__ rec, uint32_t m, uint64_t s0,
+                                                        uint64_t nlocal,
                                                         uint32_t k_start, uint32_t k_lt,
                                                         uint32_t* __restrict__ sizes, uint32_t* __restrict__ count0,
                                                         unsigned long long* __restrict__ totals,
@@ -1212,7 +1272,7 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
         uint32_t* row = rows ? rows + i * kWalkMax : nullptr;
         if (row) row[0] = v;
         uint32_t size = 1, u = 0;
-        while (lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
+        while (lt_pick_win(roff, rec, m, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
             if (!insert(u)) break;  // already in RR_s
             atomicAdd(&count0[u], 1u);
             if (size >= kWalkMax) { too_long = 1; break; }
@@ -1494,11 +1554,11 @@ void launch_rows_to_lists(const uint32_t* rows, const uint64_t* off, uint64_t nl
     ::bpt::check_cuda(cudaGetLastError(), "launch k_rows_to_lists");
 }
 
-void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
                            unsigned long long* totals, uint32_t* rows, cudaStream_t st) {
     const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
-    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, count0, totals,
+    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, m, s0, nlocal, k_start, k_lt, sizes, count0, totals,
                                                       rows);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_sparse");

@@ -417,6 +417,34 @@ def test_lt_sparse_store(bpt):
     s.close()
 
 
+@pytest.mark.parametrize("shape", ["scaled", "skewed"])
+def test_lt_sparse_store_row_sums_off_one(bpt, shape):
+    """The sparse walks' in-edge pick guesses the position from r / 2^31 and loads one window of
+    8 records; row sums well below 2^31 ("scaled": thresholds x 0.37, so ~63% of picks choose no
+    edge and the guess lands left of the answer) or weights piled on the last in-edge
+    ("skewed": most of each row's mass on its first in-edge, so the guess lands right of the answer) exercise both continuations of the search. Sizes,
+    digests and seeds stay identical to the oracle."""
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 13, theta=2048 + 17)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    thr = thr.astype(np.uint64)
+    if shape == "scaled":
+        thr = (thr * 37) // 100
+    else:  # reverse rows keep forward-position order: the first forward edge into v heads v's row
+        dst, first = np.unique(col.astype(np.int64), return_index=True)
+        thr = thr // 8
+        sums = np.bincount(col.astype(np.int64), weights=thr.astype(np.float64), minlength=cfg.n)
+        room = np.floor(Q31 - sums[dst]).astype(np.int64) - 64
+        thr[first] += np.maximum(room, 0).astype(np.uint64)
+    thr = thr.astype(np.uint32)
+    ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, sparse=True)
+    check_full(bpt, s, ref, cfg.theta)
+    seeds, gains, _ = s.select_seeds(cfg.k)
+    assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+    s.close()
+
+
 def test_lt_long_walks_fall_back_to_dense(bpt):
     """A chain graph (i -> i+1, LT weight 1): the reverse walk from vertex v has v+1 members, so
     walks outgrow the sparse store's per-thread visited set; by default the call falls back to
