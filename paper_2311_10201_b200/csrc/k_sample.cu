@@ -1123,9 +1123,22 @@ __device__ __forceinline__ bool lt_pick(const uint32_t* __restrict__ roff, const
 // round trips depends on it) and one 64-B window of 8 records around it is loaded at once. The
 // answer is the first j in [lo, hi) with cum[j] > r (none if r >= cum[hi - 1]) exactly as in
 // lt_pick; when it is not inside the window the search continues on the side it lies.
+// The visited-set probe *slot (local memory) and the row bounds roff[u], roff[u + 1] in ONE asm
+// statement: the probe decides a branch, and without this the compiler sank the bound loads
+// below it (the probe and the bounds then ran as two DRAM round trips in series).
+__device__ __forceinline__ void ld_probe_and_bounds(const uint32_t* slot, const uint32_t* p, uint32_t& x,
+                                                    uint32_t& lo, uint32_t& hi) {
+    const uint32_t ls = (uint32_t)__cvta_generic_to_local(slot);
+    asm volatile("ld.local.u32 %0, [%3];\n\tld.global.nc.u32 %1, [%4];\n\tld.global.nc.u32 %2, [%4+4];"
+                 : "=r"(x), "=r"(lo), "=r"(hi)
+                 : "r"(ls), "l"(p)
+                 : "memory");
+}
+
+// lo, hi: the row bounds roff[v], roff[v + 1], loaded by the caller (ahead of time).
 __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, const uint2* __restrict__ rec,
-                                            uint32_t m, uint32_t v, uint32_t r, uint32_t* u_out) {
-    uint32_t lo = __ldg(&roff[v]), hi = __ldg(&roff[v + 1]);
+                                            uint32_t m, uint32_t v, uint32_t lo, uint32_t hi, uint32_t r,
+                                            uint32_t* u_out) {
     if (lo >= hi) return false;
     uint32_t g = lo + (uint32_t)(((uint64_t)r * (hi - lo)) >> 31);
     g = min(g, hi - 1);
@@ -1140,21 +1153,30 @@ __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, c
 #pragma unroll
     for (int j = 0; j < 8; ++j) k += (w0 + j >= a && w0 + j < b && ys[j] <= r) ? 1u : 0u;
     const uint32_t j = a + k;  // first index of [a, b) with cum > r, b if none
+    // register selects (no dynamic indexing: that would put the window in local memory)
+    uint32_t xj = 0, xa = 0, ya = 0, yb = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        xj = (w0 + t == j) ? xs[t] : xj;
+        xa = (w0 + t == a) ? xs[t] : xa;
+        ya = (w0 + t == a) ? ys[t] : ya;
+        yb = (w0 + t + 1 == b) ? ys[t] : yb;
+    }
     uint32_t clo, chi;
     uint2 hit;
     if (j < b) {
         if (j > a || a == lo) {  // cum[j - 1] <= r < cum[j] (or j == lo)
-            *u_out = xs[j - w0];
+            *u_out = xj;
             return true;
         }
         // cum[a] > r, a > lo: the answer is in [lo, a]
         hi = a + 1;
-        chi = ys[a - w0];
-        hit = make_uint2(xs[a - w0], chi);
+        chi = ya;
+        hit = make_uint2(xa, chi);
         clo = 0;
     } else {
         if (b == hi) return false;  // r >= cum[hi - 1]: no in-edge chosen
-        clo = ys[b - 1 - w0];     // cum[b - 1] <= r: the answer is in [b, hi)
+        clo = yb;                 // cum[b - 1] <= r: the answer is in [b, hi)
         lo = b;
         hit = __ldg(&rec[hi - 1]);
         if (r >= hit.y) return false;
@@ -1256,24 +1278,38 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
         const uint64_t s = s0 + i;
 #pragma unroll 8
         for (uint32_t h = 0; h < kWalkHash; ++h) ht[h] = ~0u;
-        auto insert = [&](uint32_t u) -> bool {  // false if u was already in the set
-            uint32_t h = (u * 0x9E3779B1u) >> 21;
+        // insert u, whose home slot h was already read (x); false if u was already in the set
+        auto insert_at = [&](uint32_t u, uint32_t h, uint32_t x) -> bool {
             while (true) {
-                const uint32_t x = ht[h];
                 if (x == u) return false;
                 if (x == ~0u) { ht[h] = u; return true; }
                 h = (h + 1) & (kWalkHash - 1);
+                x = ht[h];
             }
         };
+        auto home = [](uint32_t u) -> uint32_t { return (u * 0x9E3779B1u) >> 21; };
+        auto insert = [&](uint32_t u) -> bool { const uint32_t h = home(u); return insert_at(u, h, ht[h]); };
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), k_start);
         uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
         insert(v);
         atomicAdd(&count0[v], 1u);
         uint32_t* row = rows ? rows + i * kWalkMax : nullptr;
         if (row) row[0] = v;
-        uint32_t size = 1, u = 0;
-        while (lt_pick_win(roff, rec, m, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u)) {
-            if (!insert(u)) break;  // already in RR_s
+        uint32_t size = 1, u = 0, bad_bounds = 0;
+        uint32_t lo = __ldg(&roff[v]), hi = __ldg(&roff[v + 1]);
+        uint32_t r = philox2x32_10(v, (uint32_t)s, k_lt).x >> 1;
+        while (lt_pick_win(roff, rec, m, v, lo, hi, r, &u)) {
+            // u's visited-set probe, its row bounds and its coin do not depend on each other: all
+            // three are in flight together (one DRAM round trip per step instead of two in a row;
+            // the bounds and coin are wasted only on the step that ends the walk)
+            const uint32_t h = home(u);
+            uint32_t x;
+            ld_probe_and_bounds(&ht[h], roff + u, x, lo, hi);
+            // consumed on both sides of the branch below (never true for a validated CSR, where
+            // roff[u] <= m): keeps the bound loads above the branch
+            bad_bounds |= (lo > m) | (hi > m);
+            r = philox2x32_10(u, (uint32_t)s, k_lt).x >> 1;
+            if (!insert_at(u, h, x)) break;  // already in RR_s
             atomicAdd(&count0[u], 1u);
             if (size >= kWalkMax) { too_long = 1; break; }
             if (row) row[size] = u;
@@ -1283,6 +1319,7 @@ __global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32
         sizes[i] = size;
         members += size;
         longest = max(longest, size);
+        too_long |= bad_bounds;
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
