@@ -1263,7 +1263,14 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
 // those), so no dense n x blocks bitmap exists at all.
 constexpr uint32_t kWalkHash = 2048, kWalkMax = 1536;
 
-__global__ void __launch_bounds__(256) k_walk_lt_sparse(uint32_t n, const uint32_t* __restrict__ roff,
+// Register cap for the sparse walks: at 7 blocks per SM ptxas fits the walk in 32 registers, so
+// 8 blocks x 256 threads are resident per SM and C3's 262,144 walks (1,024 blocks) start in ONE
+// wave (at 64 registers, 592 resident blocks: the second wave waited for the first wave's
+// longest walks). C3 walk 6.6 -> 4.8 ms (warm, CUDA events; 3, 5, 6 blocks/SM: 6.6, 5.4, 5.7).
+#ifndef BPT_WALK_MINB
+#define BPT_WALK_MINB 7
+#endif
+__global__ void __launch_bounds__(256, BPT_WALK_MINB) k_walk_lt_sparse(uint32_t n, const uint32_t* __restrict__ roff,
                                                         const uint2* __restrict__ rec, uint32_t m, uint64_t s0,
                                                         uint64_t nlocal,
                                                         uint32_t k_start, uint32_t k_lt,

@@ -17,6 +17,7 @@ import paper_2311_10201_b200 as bpt  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--reps", type=int, default=1)
     args = ap.parse_args()
     cfg = graphgen.CONFIGS[args.config]
     row_ptr, col, thr = graphgen.make_graph(cfg)
@@ -26,10 +27,12 @@ def main():
     d_thr = torch.from_numpy(thr.view(np.int32).copy()).to(dev)
     stream = torch.cuda.current_stream()
     g = bpt.Graph(d_row, d_col, w_q31=d_thr, model=bpt.LT, n=cfg.n, m=cfg.m, stream=stream)
-    s = g.sample(cfg.theta, colors=cfg.colors, seed=cfg.seed, stream=stream)
-    torch.cuda.synchronize()
     keep = ("members", "e_phys", "ms_expand", "expand_bytes", "expand_launches", "store_bytes")
-    print(json.dumps({k: s.info[k] for k in keep}))
+    for _ in range(args.reps):
+        s = g.sample(cfg.theta, colors=cfg.colors, seed=cfg.seed, stream=stream)
+        torch.cuda.synchronize()
+        print(json.dumps({k: s.info[k] for k in keep}))
+        s.close()
 
 
 if __name__ == "__main__":
