@@ -250,7 +250,7 @@ static void lt_lists_by_rewalk(Samples& S, cudaStream_t st) {
     S.list_off.alloc((nlocal + 1) * 8);
     S.list_mem.alloc(off[nlocal] * 4 + 4);
     BPT_CUDA(cudaMemcpyAsync(S.list_off.p, off.data(), (nlocal + 1) * 8, cudaMemcpyHostToDevice, st));
-    launch_walk_lt_lists(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), S.s0, nlocal, stream_key(S.seed, kTagStart),
+    launch_walk_lt_lists(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), (uint32_t)g.m, S.s0, nlocal, stream_key(S.seed, kTagStart),
                          stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.list_off.as<uint64_t>(),
                          S.list_mem.as<uint32_t>(), st);
     S.lists_built = S.lists_ok = true;

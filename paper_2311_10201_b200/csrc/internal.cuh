@@ -230,7 +230,7 @@ void launch_rows_to_lists(const uint32_t* rows, const uint64_t* off, uint64_t nl
 // sort every list ascending in place (one block per list of <= 4096 members; longer lists set *err)
 void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, uint32_t* err, cudaStream_t st);
 // LT: re-walk every local sample and write its members at off[i] (unsorted; for the selection)
-void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
                           uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,
                           uint32_t* members, cudaStream_t st);
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);

@@ -1238,7 +1238,8 @@ __global__ void __launch_bounds__(256) k_walk_lt(uint64_t* __restrict__ store, u
 // Second pass for the selection: re-walk each sample (same coins, same path; the walk length is
 // known from pass 1) and write its members to its slot of the member-list buffer.
 __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_t* __restrict__ roff,
-                                                       const uint2* __restrict__ rec, uint64_t s0, uint64_t nlocal,
+                                                       const uint2* __restrict__ rec, uint32_t m, uint64_t s0,
+                                                       uint64_t nlocal,
                                                        uint32_t k_start, uint32_t k_lt,
                                                        const uint32_t* __restrict__ sizes,
                                                        const uint64_t* __restrict__ off, uint32_t* __restrict__ members) {
@@ -1251,7 +1252,8 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
         out[0] = v;
         for (uint32_t j = 1; j < size; ++j) {
             uint32_t u = 0;
-            lt_pick(roff, rec, v, philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u);
+            lt_pick_win(roff, rec, m, v, __ldg(&roff[v]), __ldg(&roff[v + 1]),
+                        philox2x32_10(v, (uint32_t)s, k_lt).x >> 1, &u);
             out[j] = u;
             v = u;
         }
@@ -1616,11 +1618,11 @@ void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, 
     ::bpt::check_cuda(cudaGetLastError(), "launch k_sort_lists");
 }
 
-void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint64_t s0, uint64_t nlocal,
+void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
                           uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,
                           uint32_t* members, cudaStream_t st) {
     const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
-    k_walk_lt_lists<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, s0, nlocal, k_start, k_lt, sizes, off, members);
+    k_walk_lt_lists<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, m, s0, nlocal, k_start, k_lt, sizes, off, members);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_lists");
 }
