@@ -229,7 +229,10 @@ __global__ void k_row_offsets(const uint32_t* __restrict__ sorted_dst, uint64_t 
 //                     (walking back while the key continues), added to that segment; checks
 //                     its row sum where it ends
 constexpr int kLtThreads = 256;
-constexpr int kLtRounds = 16;
+#ifndef BPT_LT_ROUNDS
+#define BPT_LT_ROUNDS 8
+#endif
+constexpr int kLtRounds = BPT_LT_ROUNDS;  // consecutive items per thread (multiple of 4)
 constexpr uint64_t kLtTile = (uint64_t)kLtThreads * kLtRounds;
 
 __device__ __forceinline__ uint32_t sat32(unsigned long long x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
