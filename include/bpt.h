@@ -146,9 +146,18 @@ typedef struct {
  * visited set (1,536 vertices); with this flag that case fails with ENOMEM instead. Sizes,
  * digests, extraction and selection read whichever form the handle holds. */
 #define BPT_FLAG_SPARSE 4u
-/* LT samples are drawn as one reverse walk per thread (the RRR store is each sample's visited
- * set; same coins and sets as the fused level-synchronous form, which the environment variable
- * BPT_LT_FUSED=1 selects); batch_groups and BPT_FLAG_PROFILE do not apply to the walks. */
+/* LT samples are drawn as one reverse walk per thread by default (the RRR store is each
+ * sample's visited set); batch_groups and BPT_FLAG_PROFILE do not apply to the walks. The
+ * flags below select the other execution forms; every form gives the same RRR sets, sizes,
+ * digests, seeds and exact work counters (coins are keyed by (sample, edge / vertex) only). */
+#define BPT_FLAG_LT_FUSED 8u    /* LT: the fused level-synchronous loop of Listing 1
+                                   over 64-colour groups instead of per-sample walks */
+#define BPT_FLAG_LT_DENSE 16u   /* LT walks: dense n x blocks store instead of member lists */
+#define BPT_FLAG_LT_REWALK 32u  /* LT sparse store: member lists from a second walk */
+#define BPT_FLAG_LT_LEVELS 64u  /* LT fused: one launch pair per level instead of one cooperative
+                                   launch per batch */
+#define BPT_FLAG_QUEUE 128u     /* IC, 64 colours: discovered vertices through a first-setter
+                                   queue (atomicOr with return) instead of the touched bitmap */
 
 BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
                       void* stream, bpt_samples** out);
@@ -182,8 +191,8 @@ BPT_API bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* 
  * for v in [0, n). counts[n] u32, host or device. */
 BPT_API bpt_status bpt_occurrences(const bpt_samples* s, uint32_t* counts);
 
-/* Per level of every batch: {batch, level, raw_entries, kept_entries, edges_or_tasks, vc_pairs}
- * as 6 u64 per row, host buffer. *rows = number of rows available (written if rows_out != NULL). */
+/* Per level of every batch: {batch, level, raw_entries, kept_entries, edges_or_tasks, vc_pairs,
+ * coins, atomics} as 8 u64 per row, host buffer (coins / atomics are schedule-dependent). *rows = number of rows available (written if rows_out != NULL). */
 BPT_API bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_rows, uint64_t* rows_out);
 
 /* ---------------------------------------------------------------------------------
@@ -217,11 +226,23 @@ BPT_API bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* 
 
 BPT_API void bpt_samples_free(bpt_samples* s);
 
+/* Device self-test of reading C-1: out[2i], out[2i+1] = Philox2x32-10(ctr = {ctr_key[3i],
+ * ctr_key[3i+1]}, key = ctr_key[3i+2]) evaluated by the same device function the coins and start
+ * vertices use (checked against the Random123 known-answer vectors). Host or device buffers. */
+BPT_API bpt_status bpt_selftest_philox(const uint32_t* ctr_key, uint32_t* out, uint64_t count);
+/* Integer-ALU roof of the coin: times `iters` rounds of Philox2x32-10 coin evaluations on every
+ * resident thread (CUDA events); *calls = evaluations made, *ms = their device time. */
+BPT_API bpt_status bpt_bench_philox(uint64_t iters, uint64_t* calls, double* ms);
+
 /* Release the device blocks the library caches between calls (its memory pool). */
 BPT_API bpt_status bpt_release_cache(void);
 
-/* Library-wide count of kernels launched by this process (evidence for gpu_launches). */
+/* Launch evidence (process-wide counters). bpt_kernel_launch_count: launches the host issued --
+ * kernels launched directly plus one per CUDA-graph launch. bpt_graph_kernel_count: kernel
+ * executions inside the sampling graphs (its conditional level / batch loops), counted on the
+ * device by the kernels themselves. Their sum is every kernel execution of the library. */
 BPT_API uint64_t bpt_kernel_launch_count(void);
+BPT_API uint64_t bpt_graph_kernel_count(void);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,11 @@ IC, LT = 0, 1
 FLAG_PROFILE = 1
 FLAG_WIDE = 2  # 128 colours per frontier entry (IC, colors=64, batch_groups=0)
 FLAG_SPARSE = 4  # LT: sorted member lists instead of the dense store
+FLAG_LT_FUSED = 8  # LT: fused level-synchronous loop instead of per-sample walks
+FLAG_LT_DENSE = 16  # LT walks: dense store
+FLAG_LT_REWALK = 32  # LT sparse store: member lists by a second walk
+FLAG_LT_LEVELS = 64  # LT fused: per-level launches instead of one cooperative launch per batch
+FLAG_QUEUE = 128  # IC 64 colours: first-setter queue instead of the touched bitmap
 _STATUS = {0: "BPT_OK", -1: "BPT_EINVAL", -2: "BPT_ENOMEM", -3: "BPT_ECUDA", -4: "BPT_ENCCL", -5: "BPT_ESTATE"}
 
 _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
@@ -55,6 +60,7 @@ _SIGS = {
     "bpt_last_error": ([], ctypes.c_char_p),
     "bpt_abi_version": ([], _i),
     "bpt_kernel_launch_count": ([], _u64),
+    "bpt_graph_kernel_count": ([], _u64),
     "bpt_comm_unique_id": ([_p], _i),
     "bpt_comm_init": ([_p, _i, _i, _i, ctypes.POINTER(_p)], _i),
     "bpt_comm_free": ([_p], None),
@@ -74,6 +80,8 @@ _SIGS = {
     "bpt_select_seeds": ([_p, _u32, _p, _p, _p], _i),
     "bpt_samples_free": ([_p], None),
     "bpt_release_cache": ([], _i),
+    "bpt_selftest_philox": ([_p, _p, _u64], _i),
+    "bpt_bench_philox": ([_u64, ctypes.POINTER(_u64), ctypes.POINTER(ctypes.c_double)], _i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -134,11 +142,38 @@ def bpt_abi_version() -> int:
     return _lib.bpt_abi_version()
 
 
+def selftest_philox(ctr_key) -> np.ndarray:
+    """Device Philox2x32-10 of rows (ctr0, ctr1, key) -> rows (out0, out1) (reading C-1)."""
+    a = np.ascontiguousarray(ctr_key, dtype=np.uint32).reshape(-1, 3)
+    out = np.zeros((a.shape[0], 2), dtype=np.uint32)
+    _check(_lib.bpt_selftest_philox(_ptr(a), _ptr(out), a.shape[0]))
+    return out
+
+
+def bench_philox(iters: int = 64) -> tuple[int, float]:
+    """(coin evaluations, device ms) of the Philox throughput kernel."""
+    calls, ms = _u64(), ctypes.c_double()
+    _check(_lib.bpt_bench_philox(iters, ctypes.byref(calls), ctypes.byref(ms)))
+    return int(calls.value), float(ms.value)
+
+
 def kernel_launch_count() -> int:
+    """Kernel launches the host issued (direct launches + one per CUDA-graph launch)."""
     return int(_lib.bpt_kernel_launch_count())
 
 
+def graph_kernel_count() -> int:
+    """Kernel executions inside the sampling graphs, counted on the device by the kernels."""
+    return int(_lib.bpt_graph_kernel_count())
+
+
+def kernels_executed() -> int:
+    """Every kernel execution of the library so far (host launches + graph-node executions)."""
+    return kernel_launch_count() + graph_kernel_count()
+
+
 bpt_kernel_launch_count = kernel_launch_count
+bpt_graph_kernel_count = graph_kernel_count
 
 
 def bpt_comm_unique_id() -> bytes:
@@ -196,7 +231,7 @@ def bpt_samples_get_info(h) -> dict:
 def bpt_level_stats(h) -> np.ndarray:
     rows = _u64()
     _check(_lib.bpt_level_stats(h, None, 0, ctypes.byref(rows)))
-    out = np.zeros((rows.value, 6), dtype=np.uint64)
+    out = np.zeros((rows.value, 8), dtype=np.uint64)  # batch, level, raw, kept, work, vc, coins, atomics
     if rows.value:
         _check(_lib.bpt_level_stats(h, _ptr(out), rows.value, None))
     return out
@@ -305,8 +340,8 @@ class Graph:
 
     def sample(self, theta: int, colors: int = 64, seed: int = 0, stream=None, batch_groups: int = 0,
                poll_levels: int = 0, profile: bool = False, shard: tuple[int, int] | None = None,
-               wide: bool = False, sparse: bool = False) -> "Samples":
-        flags = (FLAG_PROFILE if profile else 0) | (FLAG_WIDE if wide else 0) | (FLAG_SPARSE if sparse else 0)
+               wide: bool = False, sparse: bool = False, flags: int = 0) -> "Samples":
+        flags |= (FLAG_PROFILE if profile else 0) | (FLAG_WIDE if wide else 0) | (FLAG_SPARSE if sparse else 0)
         h = bpt_sample(self._h, self.model, theta, colors, seed, stream, batch_groups, poll_levels, flags, shard)
         return Samples(self, h)
 

@@ -18,6 +18,7 @@ namespace bpt {
 // ------------------------------------------------------------------ errors
 thread_local std::string g_last_error;
 uint64_t g_launches = 0;
+uint64_t g_graph_kernels = 0;
 
 void fail(bpt_status code, const std::string& msg) { throw Error{code, msg}; }
 
@@ -31,13 +32,26 @@ void check_cuda(cudaError_t e, const char* what) {
 // ------------------------------------------------------------------ device memory pool
 // Freed device blocks are cached per device and reused for later requests of a similar size
 // (best fit within +25%), so repeated bpt_graph_load / bpt_sample calls do not pay
-// cudaMalloc/cudaFree of multi-GB stores each time. Every API call synchronises its stream
-// before returning, so a block is never recycled while a kernel may still use it.
-// On allocation failure the cache is released and the allocation retried.
+// cudaMalloc/cudaFree of multi-GB stores each time. Recycling is stream-ordered: a block
+// remembers the stream of the API call that used it (StreamScope); when it is released an
+// event is recorded on that stream, and the next call that takes the block makes its own
+// stream wait on that event, so a block is never handed out while a kernel queued before
+// its release may still touch it (no host synchronisation needed).
+// On allocation failure the cache is released (after its events complete) and the
+// allocation retried.
+thread_local cudaStream_t g_cur_stream = nullptr;
+
+StreamScope::StreamScope(cudaStream_t st) : prev_(g_cur_stream) { g_cur_stream = st; }
+StreamScope::~StreamScope() { g_cur_stream = prev_; }
+
 namespace {
+struct Cached {
+    void* p;
+    cudaEvent_t ev;  // recorded on the releasing stream (nullptr: nothing pending)
+};
 struct Pool {
     std::mutex mu;
-    std::multimap<size_t, void*> free_blocks[64];  // per device: size -> block
+    std::multimap<size_t, Cached> free_blocks[64];  // per device: size -> block
     size_t cached[64] = {};
 };
 Pool& pool() {
@@ -69,7 +83,13 @@ void release_cached_blocks() {
     for (int d = 0; d < 64; ++d) {
         if (P.free_blocks[d].empty()) continue;
         cudaSetDevice(d);
-        for (auto& kv : P.free_blocks[d]) cudaFree(kv.second);
+        for (auto& kv : P.free_blocks[d]) {
+            if (kv.second.ev) {
+                cudaEventSynchronize(kv.second.ev);
+                cudaEventDestroy(kv.second.ev);
+            }
+            cudaFree(kv.second.p);
+        }
         P.free_blocks[d].clear();
         P.cached[d] = 0;
     }
@@ -85,11 +105,16 @@ void DevBuf::alloc(size_t b) {
         std::lock_guard<std::mutex> lk(P.mu);
         auto it = P.free_blocks[dev].lower_bound(b);
         if (it != P.free_blocks[dev].end() && it->first <= b + b / 4) {
-            p = it->second;
+            p = it->second.p;
             bytes = it->first;
+            if (it->second.ev) {  // work queued before the release must finish first
+                cudaStreamWaitEvent(g_cur_stream, it->second.ev, 0);
+                cudaEventDestroy(it->second.ev);
+            }
             P.cached[dev] -= bytes;
             P.free_blocks[dev].erase(it);
             device = dev;
+            stream = g_cur_stream;
             return;
         }
     }
@@ -108,12 +133,29 @@ void DevBuf::alloc(size_t b) {
     }
     bytes = b;
     device = dev;
+    stream = g_cur_stream;
 }
 void DevBuf::reset() {
     if (p) {
+        cudaEvent_t ev = nullptr;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != device) cudaSetDevice(device);
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+            if (cudaEventRecord(ev, stream) != cudaSuccess) {  // cannot order: wait for the device
+                cudaEventDestroy(ev);
+                ev = nullptr;
+                cudaDeviceSynchronize();
+            }
+        } else {
+            ev = nullptr;
+            cudaDeviceSynchronize();
+        }
+        cudaGetLastError();
+        if (cur != device && cur >= 0) cudaSetDevice(cur);
         Pool& P = pool();
         std::lock_guard<std::mutex> lk(P.mu);
-        P.free_blocks[device].emplace(bytes, p);
+        P.free_blocks[device].emplace(bytes, Cached{p, ev});
         P.cached[device] += bytes;
     }
     p = nullptr;
@@ -135,9 +177,12 @@ void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint6
                    cudaStream_t st);
 void compute_digests(const Samples& S, cudaStream_t st);
 void comm_unique_id(void* out);
+void selftest_philox(const uint32_t* d_in, uint32_t* d_out, uint64_t count, cudaStream_t st);
+double bench_philox(uint64_t iters, uint64_t* calls_out, cudaStream_t st);
 void comm_init(Comm* c, const void* uid);
 void comm_destroy(Comm* c);
 void comm_broadcast(Comm* c, const void* send, void* recv, uint64_t bytes, int root, cudaStream_t st);
+void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st);
 
 namespace {
 
@@ -173,11 +218,20 @@ void use_device(int dev) {
     if (cur != dev) BPT_CUDA(cudaSetDevice(dev));
 }
 
+// Restores the caller's current device when an API call returns (calls switch to the
+// device of the handle they operate on).
+struct DeviceGuard {
+    int dev = -1;
+    DeviceGuard() { if (cudaGetDevice(&dev) != cudaSuccess) { dev = -1; cudaGetLastError(); } }
+    ~DeviceGuard() { if (dev >= 0) cudaSetDevice(dev); }
+};
+
 template <class F>
 bpt_status guarded(F&& f) {
     // a pending error recorded by an earlier (unchecked) runtime call must not be
     // attributed to this call's first launch check; keep it for the message
     const cudaError_t stale = cudaGetLastError();
+    DeviceGuard restore_device;
     try {
         f();
         return BPT_OK;
@@ -199,11 +253,6 @@ bpt_status guarded(F&& f) {
 }  // namespace
 
 using clk_t = std::chrono::steady_clock;
-
-static bool env_is(const char* name, char c) {
-    const char* v = getenv(name);
-    return v && v[0] == c;
-}
 
 static uint64_t device_total_bytes() {  // cached per device
     static uint64_t total[64] = {};
@@ -289,7 +338,7 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
     BPT_CUDA(cudaMemsetAsync(totals.p, 0, 24, st));
     auto since = [&]() { return std::chrono::duration<double, std::milli>(clk_t::now() - t_begin).count(); };
     const double t_pre = since();
-    if (!env_is("BPT_LT_REWALK", '1')) {
+    if (!(opt.flags & BPT_FLAG_LT_REWALK)) {
         // walk-order rows written during the walk (6 KB per sample) when they fit a quarter of
         // the device memory and the allocation succeeds, else the lists come from a second walk
         // (no cudaMemGetInfo here: it stalled the call for 10-40 ms at times)
@@ -393,8 +442,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     //      visited set (BPT_FLAG_SPARSE: fail instead); BPT_LT_DENSE=1 walks into the dense store;
     //      BPT_LT_FUSED=1 runs the level-synchronous fused loop below (same sets).
     if (S.model == BPT_LT) {
-        const bool fused = env_is("BPT_LT_FUSED", '1');
-        const bool want_sparse = (opt.flags & BPT_FLAG_SPARSE) || (!env_is("BPT_LT_DENSE", '1') && !fused);
+        const bool fused = (opt.flags & BPT_FLAG_LT_FUSED) != 0;
+        const bool want_sparse = (opt.flags & BPT_FLAG_SPARSE) || (!(opt.flags & BPT_FLAG_LT_DENSE) && !fused);
         if (want_sparse && run_lt_walks_sparse(S, opt, st, t_begin, launches0)) return;
         if (!fused) {
             run_lt_walks_dense(S, st, t_begin, launches0);
@@ -408,19 +457,21 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     // longer levels: LT frontiers are thin, per-level overhead dominates)
     uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 2048);
     // wide fusion (IC, 64 colours): kWide blocks share one frontier (k_sample.cu "wide fusion")
-    const char* wide_env = getenv("BPT_WIDE");
-    const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups &&
-                      ((opt.flags & BPT_FLAG_WIDE) || (wide_env && wide_env[0] == '1'));
+    const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups && (opt.flags & BPT_FLAG_WIDE);
+    // touched-bitmap frontier (IC, 64 colours; k_sample.cu "A4: compaction")
+    const bool bitmap = S.model == BPT_IC && C == 64 && !wide && !(opt.flags & BPT_FLAG_QUEUE);
     if (wide) want = kWide;
     uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
     const uint32_t tile = wide ? kUnitWide : expand_unit(S.model);
+    const uint64_t tiles = (n + 1023) / 1024;  // bitmap: 1,024-vertex tiles per slot
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
         raw_cap = umin64(wide ? n : sl * slices * n, (1ull << 28) - 1);  // wide: one entry per vertex
         q_cap = raw_cap;
+        if (bitmap) raw_cap = 1;  // no queue
         const uint64_t work = S.model == BPT_IC ? umin64((wide ? 1 : sl * slices) * g.m, kEdgeMask)
                                                 : umin64(sl * 64 * n, kEdgeMask);
         ts_cap = work / tile + 2;
-        return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 20;
+        return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 20 + (bitmap ? sl * tiles * 128 : 0);
     };
     size_t free_b = 0, total_b = 0;
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -438,7 +489,11 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
         elog(8);
     BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
-    DevBuf vflag, qd, qmask;
+    DevBuf vflag, qd, qmask, touched;
+    if (bitmap) {
+        touched.alloc(slots * tiles * 128);
+        BPT_CUDA(cudaMemsetAsync(touched.p, 0, touched.bytes, st));  // the compaction clears what it reads
+    }
     if (wide) {
         vflag.alloc((uint64_t)n * 4 + 4);
         qd.alloc(q_cap * 4 + 4);
@@ -488,6 +543,10 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.vflag = wide ? vflag.as<uint32_t>() : nullptr;
     a.qd = wide ? qd.as<uint32_t>() : nullptr;
     a.qmask = wide ? qmask.as<unsigned long long>() : nullptr;
+    a.touched = bitmap ? touched.as<uint32_t>() : nullptr;
+    a.tiles = (uint32_t)tiles;
+    a.lt_persist = (opt.flags & BPT_FLAG_LT_LEVELS) ? 0 : 1;
+    a.lt_blocks_per_sm = 1;
 
     const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
     double ev_ms = 0;
@@ -586,18 +645,20 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         const uint64_t kept = r.packed >> kPackShift, work = r.packed & kEdgeMask;
         const uint64_t raw_next = (i + 1 < rows && (R[i + 1].pad >> 32) == (r.pad >> 32)) ? R[i + 1].raw : 0;
         bytes += (S.model == BPT_IC ? 16.0 : 24.0) * work + 8.0 * r.atomics + 24.0 * kept + 8.0 * raw_next;
-        const uint64_t row[6] = {r.pad >> 32, r.pad & 0xffffffffull, r.raw, kept, work, r.vc};
-        S.level_rows.insert(S.level_rows.end(), row, row + 6);
+        const uint64_t row[kLevelCols] = {r.pad >> 32, r.pad & 0xffffffffull, r.raw, kept, work, r.vc, r.coins, r.atomics};
+        S.level_rows.insert(S.level_rows.end(), row, row + kLevelCols);
     }
     I.expand_bytes = bytes;
     // expansion time: CUDA events around every launch (profile mode) or the device-side
     // %globaltimer span of every launch (graph mode)
     I.ms_expand = profile ? ev_ms : cf.expand_ns * 1e-6;
     I.expand_launches = profile ? ev_launches : cf.levels_total;
-    // kernels executed: per batch init + finalize + next_batch, per level compact + expand (LT: one
-    // cooperative level-loop launch per batch)
-    if (!profile) g_launches += level_loop_persistent(a) ? 4 * nbatches : 3 * nbatches + 2 * cf.levels_total;
-    I.kernel_launches = g_launches - launches0;
+    // graph mode: one host launch (the graph); the kernels it ran counted themselves on the device
+    if (!profile) {
+        g_launches += 1;
+        g_graph_kernels += cf.kernels_run;
+    }
+    I.kernel_launches = g_launches - launches0 + (profile ? 0 : cf.kernels_run);
     I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     if (getenv("BPT_TRACE")) {
         auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
@@ -623,6 +684,7 @@ extern "C" {
 const char* bpt_last_error(void) { return g_last_error.c_str(); }
 int bpt_abi_version(void) { return BPT_ABI_VERSION; }
 uint64_t bpt_kernel_launch_count(void) { return g_launches; }
+uint64_t bpt_graph_kernel_count(void) { return g_graph_kernels; }
 
 bpt_status bpt_release_cache(void) {
     return guarded([&] { release_cached_blocks(); });
@@ -672,6 +734,7 @@ bpt_status bpt_graph_load(bpt_comm* comm, const uint64_t* row_ptr, const uint32_
         if (comm) { use_device(comm->c.device); dev = comm->c.device; }
         else BPT_CUDA(cudaGetDevice(&dev));
         cudaStream_t st = (cudaStream_t)stream;
+        StreamScope scope(st);
         auto G = std::make_unique<bpt_graph>();
         G->g.comm = comm ? &comm->c : nullptr;
         G->g.device = dev;
@@ -694,28 +757,42 @@ bpt_status bpt_graph_load_bcast(bpt_comm* comm, int root, const uint64_t* row_pt
     if (!comm || comm->c.world <= 1 || !comm->c.nccl)
         return bpt_graph_load(comm, row_ptr, col, n, m, w_f32, w_q31, model, stream, out);
     return guarded([&] {
-        if (!out) fail(BPT_EINVAL, "out is NULL");
-        if (root < 0 || root >= comm->c.world) fail(BPT_EINVAL, "root must be a rank of the communicator");
-        if (n == 0) fail(BPT_EINVAL, "n must be > 0");
-        if (m >= (1ull << 32)) fail(BPT_EINVAL, "m must be < 2^32");
-        if (model != BPT_IC && model != BPT_LT) fail(BPT_EINVAL, "model must be BPT_IC or BPT_LT");
         use_device(comm->c.device);
         cudaStream_t st = (cudaStream_t)stream;
+        StreamScope scope(st);
+        // Every rank takes part in the status exchange whatever its own checks found, so a
+        // failure on one rank (its arguments, or the root's validation / build) fails the call
+        // on every rank with the same code instead of leaving the others in a broadcast.
+        bpt_status local = BPT_OK;
+        std::string local_msg;
+        auto local_fail = [&](bpt_status c, const char* msg) { if (local == BPT_OK) { local = c; local_msg = msg; } };
+        if (!out) local_fail(BPT_EINVAL, "out is NULL");
+        if (root < 0 || root >= comm->c.world) local_fail(BPT_EINVAL, "root must be a rank of the communicator");
+        if (n == 0) local_fail(BPT_EINVAL, "n must be > 0");
+        if (m >= (1ull << 32)) local_fail(BPT_EINVAL, "m must be < 2^32");
+        if (model != BPT_IC && model != BPT_LT) local_fail(BPT_EINVAL, "model must be BPT_IC or BPT_LT");
         const bool is_root = comm->c.rank == root;
         bpt_graph* built = nullptr;
-        std::string root_error;
-        if (is_root) {  // validate + build on the root; its outcome is broadcast before the data
-            const bpt_status r = bpt_graph_load(comm, row_ptr, col, n, m, w_f32, w_q31, model, stream, &built);
-            if (r != BPT_OK) root_error = g_last_error;
+        if (is_root && local == BPT_OK) {  // validate + build on the root
+            local = bpt_graph_load(comm, row_ptr, col, n, m, w_f32, w_q31, model, stream, &built);
+            if (local != BPT_OK) local_msg = g_last_error;
         }
-        DevBuf status(4);
-        const uint32_t h_status = is_root ? (built ? 1u : 2u) : 0u;
-        BPT_CUDA(cudaMemcpyAsync(status.p, &h_status, 4, cudaMemcpyHostToDevice, st));
-        comm_broadcast(&comm->c, status.p, status.p, 4, root, st);
-        uint32_t got = 0;
-        BPT_CUDA(cudaMemcpyAsync(&got, status.p, 4, cudaMemcpyDeviceToHost, st));
+        // status word: (rank-local failure code as a positive number) << 8 | failing rank
+        DevBuf status(8);
+        const unsigned long long mine =
+            local == BPT_OK ? 0ull : ((unsigned long long)(-(int)local) << 8) | (unsigned long long)comm->c.rank;
+        BPT_CUDA(cudaMemcpyAsync(status.p, &mine, 8, cudaMemcpyHostToDevice, st));
+        comm_allreduce_max_u64(&comm->c, status.as<unsigned long long>(), 1, st);
+        unsigned long long got = 0;
+        BPT_CUDA(cudaMemcpyAsync(&got, status.p, 8, cudaMemcpyDeviceToHost, st));
         BPT_CUDA(cudaStreamSynchronize(st));
-        if (got != 1) fail(BPT_EINVAL, is_root ? root_error : "graph load failed on the root rank");
+        if (got) {
+            if (built) bpt_graph_free(built);
+            const bpt_status code = (bpt_status)(-(int)(got >> 8));
+            fail(code, local != BPT_OK ? local_msg
+                                       : "graph load failed on rank " + std::to_string(got & 0xff) + " (" +
+                                             std::to_string((int)code) + ")");
+        }
         std::unique_ptr<bpt_graph> G(built ? built : new bpt_graph());
         if (!is_root) {
             G->g.comm = &comm->c;
@@ -737,6 +814,7 @@ bpt_status bpt_graph_reverse(const bpt_graph* g, uint32_t* roff, uint32_t* src, 
     return guarded([&] {
         if (!g) fail(BPT_EINVAL, "graph is NULL");
         use_device(g->g.device);
+        StreamScope scope(nullptr);
         const Graph& G = g->g;
         copy_out(roff, G.roff.p, ((size_t)G.n + 1) * 4, 0);
         if (src || val) {
@@ -776,6 +854,7 @@ bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, ui
         if (theta == 0 || theta >= (1ull << 32)) fail(BPT_EINVAL, "theta must be in [1, 2^32)");
         if (colors < 1 || colors > 64 || (64 % colors) != 0) fail(BPT_EINVAL, "colors must divide 64 (1,2,4,...,64)");
         use_device(g->g.device);
+        StreamScope scope((cudaStream_t)stream);
         bpt_sample_opts o{};
         if (opts) o = *opts;
         auto S = std::make_unique<bpt_samples>();
@@ -788,6 +867,7 @@ bpt_status bpt_sample_ex(const bpt_graph* g, bpt_model model, uint64_t theta, ui
         s.theta = theta;
         s.seed = seed;
         s.colors = colors;
+        s.stream = (cudaStream_t)stream;
         const Comm* c = g->g.comm;
         uint64_t W = c ? c->world : 1, r = c ? c->rank : 0;
         if (o.shard_world) {  // test hook: one shard of a W-way split, without communication
@@ -829,17 +909,18 @@ bpt_status bpt_occurrences(const bpt_samples* s, uint32_t* counts) {
     return guarded([&] {
         if (!s || !counts) fail(BPT_EINVAL, "NULL argument");
         use_device(s->s.device);
-        copy_out(counts, s->s.count0.p, (size_t)s->s.n * 4, 0);
-        BPT_CUDA(cudaStreamSynchronize(0));
+        StreamScope scope(s->s.stream);
+        copy_out(counts, s->s.count0.p, (size_t)s->s.n * 4, s->s.stream);
+        BPT_CUDA(cudaStreamSynchronize(s->s.stream));
     });
 }
 
 bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_rows, uint64_t* rows_out) {
     return guarded([&] {
         if (!s) fail(BPT_EINVAL, "samples is NULL");
-        const uint64_t rows = s->s.level_rows.size() / 6;
+        const uint64_t rows = s->s.level_rows.size() / kLevelCols;
         if (rows_out) *rows_out = rows;
-        if (out) memcpy(out, s->s.level_rows.data(), std::min(rows, cap_rows) * 6 * 8);
+        if (out) memcpy(out, s->s.level_rows.data(), std::min(rows, cap_rows) * kLevelCols * 8);
     });
 }
 
@@ -856,8 +937,9 @@ bpt_status bpt_rrr_sizes(const bpt_samples* s, uint64_t first, uint64_t count, u
         if (!s || !sizes) fail(BPT_EINVAL, "NULL argument");
         check_range(s->s, first, count);
         use_device(s->s.device);
-        copy_out(sizes, s->s.sizes.as<uint32_t>() + (first - s->s.s0), count * 4, 0);
-        BPT_CUDA(cudaStreamSynchronize(0));
+        StreamScope scope(s->s.stream);
+        copy_out(sizes, s->s.sizes.as<uint32_t>() + (first - s->s.s0), count * 4, s->s.stream);
+        BPT_CUDA(cudaStreamSynchronize(s->s.stream));
     });
 }
 
@@ -866,13 +948,14 @@ bpt_status bpt_rrr_digests(const bpt_samples* s, uint64_t first, uint64_t count,
         if (!s || !digests) fail(BPT_EINVAL, "NULL argument");
         check_range(s->s, first, count);
         use_device(s->s.device);
+        StreamScope scope(s->s.stream);
         Samples& M = const_cast<Samples&>(s->s);
         if (!M.digests_ready) {  // verification checksums: computed on first use
-            compute_digests(M, 0);
+            compute_digests(M, M.stream);
             M.digests_ready = true;
         }
-        copy_out(digests, s->s.digests.as<uint64_t>() + (first - s->s.s0), count * 8, 0);
-        BPT_CUDA(cudaStreamSynchronize(0));
+        copy_out(digests, s->s.digests.as<uint64_t>() + (first - s->s.s0), count * 8, M.stream);
+        BPT_CUDA(cudaStreamSynchronize(M.stream));
     });
 }
 
@@ -883,8 +966,11 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         const Samples& S = s->s;
         check_range(S, first, count);
         use_device(S.device);
+        const cudaStream_t st = S.stream;
+        StreamScope scope(st);
         std::vector<uint32_t> sz(count);
-        BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.as<uint32_t>() + (first - S.s0), count * 4, cudaMemcpyDeviceToHost));
+        BPT_CUDA(cudaMemcpyAsync(sz.data(), S.sizes.as<uint32_t>() + (first - S.s0), count * 4, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
         std::vector<uint64_t> off(count + 1, 0);
         for (uint64_t i = 0; i < count; ++i) off[i + 1] = off[i] + sz[i];
         const uint64_t total = off[count];
@@ -893,24 +979,27 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         if (total && !members) fail(BPT_EINVAL, "members is NULL");
         if (total && S.sparse) {  // the store is the member lists: sort the range, one contiguous slice
             DevBuf err(4);
-            BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, 0));
+            BPT_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
             launch_sort_lists(S.list_off.as<uint64_t>() + (first - S.s0), const_cast<uint32_t*>(S.list_mem.as<uint32_t>()),
-                              count, err.as<uint32_t>(), 0);
+                              count, err.as<uint32_t>(), st);
             uint32_t h_err = 0;
-            BPT_CUDA(cudaMemcpy(&h_err, err.p, 4, cudaMemcpyDeviceToHost));
-            if (h_err) fail(BPT_ESTATE, "member list longer than the list sort");
             uint64_t b = 0;
-            BPT_CUDA(cudaMemcpy(&b, S.list_off.as<uint64_t>() + (first - S.s0), 8, cudaMemcpyDeviceToHost));
-            BPT_CUDA(cudaMemcpy(members, S.list_mem.as<uint32_t>() + b, total * 4, cudaMemcpyDefault));
+            BPT_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaMemcpyAsync(&b, S.list_off.as<uint64_t>() + (first - S.s0), 8, cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaStreamSynchronize(st));
+            if (h_err) fail(BPT_ESTATE, "member list longer than the list sort");
+            BPT_CUDA(cudaMemcpyAsync(members, S.list_mem.as<uint32_t>() + b, total * 4, cudaMemcpyDefault, st));
+            BPT_CUDA(cudaStreamSynchronize(st));
         } else if (total) {
             DevBuf tmp;
             uint32_t* dm = members;
             if (!is_device_ptr(members)) { tmp.alloc(total * 4); dm = tmp.as<uint32_t>(); }
-            extract_range(S, first, count, off.data(), dm, 0);
-            if (dm != members) BPT_CUDA(cudaMemcpyAsync(members, dm, total * 4, cudaMemcpyDeviceToHost, 0));
-            BPT_CUDA(cudaStreamSynchronize(0));
+            extract_range(S, first, count, off.data(), dm, st);
+            if (dm != members) BPT_CUDA(cudaMemcpyAsync(members, dm, total * 4, cudaMemcpyDeviceToHost, st));
+            BPT_CUDA(cudaStreamSynchronize(st));
         }
-        BPT_CUDA(cudaMemcpy(offsets, off.data(), (count + 1) * 8, cudaMemcpyDefault));
+        BPT_CUDA(cudaMemcpyAsync(offsets, off.data(), (count + 1) * 8, cudaMemcpyDefault, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -920,9 +1009,10 @@ bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* seeds, u
         const Samples& S = s->s;
         if (k == 0 || k > S.n) fail(BPT_EINVAL, "k must be in [1, n]");
         use_device(S.device);
+        StreamScope scope(S.stream);
         std::vector<uint32_t> hs(k);
         std::vector<uint64_t> hg(k);
-        select_seeds(S, k, hs.data(), hg.data(), 0);
+        select_seeds(S, k, hs.data(), hg.data(), S.stream);
         uint64_t covered = 0;
         for (uint32_t i = 0; i < k; ++i) covered += hg[i];
         const double sig = (double)S.n * (double)covered / (double)S.theta;  // reading C-12
@@ -932,6 +1022,26 @@ bpt_status bpt_select_seeds(const bpt_samples* s, uint32_t k, uint32_t* seeds, u
             if (is_device_ptr(sigma_hat)) BPT_CUDA(cudaMemcpy(sigma_hat, &sig, 8, cudaMemcpyHostToDevice));
             else *sigma_hat = sig;
         }
+    });
+}
+
+bpt_status bpt_selftest_philox(const uint32_t* ctr_key, uint32_t* out, uint64_t count) {
+    return guarded([&] {
+        if (count && (!ctr_key || !out)) fail(BPT_EINVAL, "NULL argument");
+        StreamScope scope(nullptr);
+        DevIn din(ctr_key, count * 12, nullptr);
+        DevBuf dout(count * 8 + 8);
+        selftest_philox((const uint32_t*)din.p, dout.as<uint32_t>(), count, nullptr);
+        copy_out(out, dout.p, count * 8, nullptr);
+        BPT_CUDA(cudaStreamSynchronize(nullptr));
+    });
+}
+
+bpt_status bpt_bench_philox(uint64_t iters, uint64_t* calls, double* ms) {
+    return guarded([&] {
+        if (!calls || !ms || iters == 0) fail(BPT_EINVAL, "calls / ms NULL or iters == 0");
+        StreamScope scope(nullptr);
+        *ms = bench_philox(iters, calls, nullptr);
     });
 }
 

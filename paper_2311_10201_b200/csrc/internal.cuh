@@ -23,7 +23,8 @@ void check_cuda(cudaError_t e, const char* what);
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
-extern uint64_t g_launches;  // kernels launched by this process (host counter)
+extern uint64_t g_launches;        // kernel launches issued by the host (<<<>>> and cudaGraphLaunch)
+extern uint64_t g_graph_kernels;   // kernel executions inside CUDA graphs, counted on the device
 inline void count_launch(uint64_t k = 1) { g_launches += k; }
 
 // ------------------------------------------------------------------ Philox2x32-10
@@ -56,17 +57,29 @@ struct Comm {
     void* nccl = nullptr;  // ncclComm_t
 };
 
-struct DevBuf {  // RAII device allocation
+// The stream the current API call runs on (set by StreamScope at the entry of every call
+// that queues work): device blocks are allocated and released in that stream's order.
+struct StreamScope {
+    explicit StreamScope(cudaStream_t st);
+    ~StreamScope();
+    StreamScope(const StreamScope&) = delete;
+    StreamScope& operator=(const StreamScope&) = delete;
+private:
+    cudaStream_t prev_;
+};
+
+struct DevBuf {  // RAII device allocation from the stream-ordered pool (api.cu)
     void* p = nullptr;
     size_t bytes = 0;
     int device = 0;
+    cudaStream_t stream = nullptr;  // last stream that may use the block (release is ordered after it)
     DevBuf() = default;
     explicit DevBuf(size_t b) { alloc(b); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), device(o.device) { o.p = nullptr; o.bytes = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), device(o.device), stream(o.stream) { o.p = nullptr; o.bytes = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        reset(); p = o.p; bytes = o.bytes; device = o.device; o.p = nullptr; o.bytes = 0; return *this;
+        reset(); p = o.p; bytes = o.bytes; device = o.device; stream = o.stream; o.p = nullptr; o.bytes = 0; return *this;
     }
     ~DevBuf() { reset(); }
     void alloc(size_t b);
@@ -90,18 +103,24 @@ struct LevelRec {
     unsigned long long vc;       // sum popc(mask) over raw entries (vertex-colour pairs)
     unsigned long long coins;    // coin evaluations by the expansion of this level
     unsigned long long atomics;  // atomicOr merges issued by the expansion of this level
-    unsigned int raw;            // raw (discovered) entries appended for THIS level
+    unsigned int raw;            // raw (discovered) entries of THIS level (queue appends, or the
+                                 // touched vertices the bitmap compaction found)
     unsigned int overflow;       // set if a queue overflowed
-    unsigned long long pad;
+    unsigned long long pad;      // stats copy: batch << 32 | level
+    unsigned int any;            // touched-bitmap mode: some colour reached this level
+    unsigned int pad2;
+    unsigned long long pad3;
 };
-static_assert(sizeof(LevelRec) == 48, "LevelRec layout");
+static_assert(sizeof(LevelRec) == 64, "LevelRec layout");
 constexpr int kPackShift = 36;
+constexpr int kLevelCols = 8;  // bpt_level_stats row width
 constexpr unsigned long long kEdgeMask = (1ull << kPackShift) - 1;
 
 struct Samples {
     const Graph* g = nullptr;   // valid only inside bpt_sample; the samples outlive the graph
     uint32_t n = 0;
     int device = 0;
+    cudaStream_t stream = nullptr;  // stream of bpt_sample: every later call on the handle runs on it
     Comm* comm = nullptr;       // must outlive the samples (selection collectives)
     int model = 0;
     uint64_t theta = 0, seed = 0, s0 = 0, s1 = 0;
@@ -114,7 +133,7 @@ struct Samples {
     DevBuf count0;              // u32[n_pad]  occurrences: sum_s 1[v in RR_s] (local)
     uint32_t n_pad = 0;
     bpt_samples_info info{};
-    std::vector<uint64_t> level_rows;  // 6 per row
+    std::vector<uint64_t> level_rows;  // kLevelCols per row (bpt_level_stats)
     // member lists of all local samples (selection on sparse stores), built on demand
     bool lists_built = false, lists_ok = false;
     bool digests_ready = false;
@@ -152,6 +171,9 @@ struct Ctl {
     uint32_t bar_count;      // grid barrier of the cooperative LT level loop: arrivals ...
     uint32_t bar_gen;        // ... and generation
     uint32_t pad_;
+    unsigned long long kernels_run;  // kernel executions inside the sampling graph, counted by the
+                                     // kernels themselves (block 0, thread 0 of every launch)
+    unsigned long long pad2_;
 };
 static_assert(sizeof(Ctl) % 16 == 0, "Ctl is read with 16-B vector loads");
 constexpr int kMaxLevels = 8192;
@@ -186,6 +208,13 @@ struct BatchArgs {
     uint32_t* vflag;
     uint32_t* qd;             // entry: rowstart - work offset (edge id = item + qd)
     unsigned long long* qmask;  // entry masks [j * kWide + b]
+    // touched-bitmap mode (IC, 64 colours, slot-major): the expansion merges with fire-and-forget
+    // ORs and marks every vertex whose N it makes non-empty in touched[slot * tile_words + v / 32];
+    // the compaction scans the bitmap (1,024-vertex tiles) instead of a queue of first setters
+    uint32_t* touched;        // nullptr: queue mode
+    uint32_t tiles;           // 1,024-vertex tiles per slot (tile_words = 32 * tiles)
+    int lt_persist;           // LT fused loop: one cooperative launch per batch
+    int lt_blocks_per_sm;     // ... with this many blocks per SM
 };
 #ifndef BPT_WIDE_BLOCKS
 #define BPT_WIDE_BLOCKS 2

@@ -98,6 +98,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
+// every kernel of the sampling graph counts its own execution (launch evidence)
+__device__ __forceinline__ void count_self(Ctl* c) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&c->kernels_run, 1ull);
+}
+
 __device__ __forceinline__ unsigned long long block_sum_ull(unsigned long long x, unsigned long long* sh) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(kFull, x, d);
@@ -116,6 +121,7 @@ __device__ __forceinline__ unsigned long long block_sum_ull(unsigned long long x
 // Listing 1 lines 1-3: frontier[start].c = 1 -> here VN[slot][start].N |= bit,
 // first setter of the (slot, slice) enqueues the raw entry of level 0.
 __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
     const uint64_t total = (uint64_t)a.ctl->slots * 64;
     const uint64_t gblk0 = a.ctl->gblk0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -130,6 +136,12 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), a.k_start);
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
+        if (a.touched) {  // bitmap mode: mark the start, the compaction of level 0 finds it
+            atomicOr(&a.VN[(size_t)slot * a.n + start].y, 1ull << bit);
+            atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (start >> 5)], 1u << (start & 31));
+            a.lv[0].any = 1;
+            continue;
+        }
         const uint32_t slice = bit / a.colors;
         const uint64_t smask = slice_mask_of(a.colors, slice);
         const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + start].y, 1ull << bit);
@@ -153,11 +165,15 @@ constexpr uint32_t kCompTile = kThreads * kCompItems;
 // kCoh: loads of data written earlier in the same launch bypass L1 (the persistent LT level
 // loop below runs several levels per launch; separate launches see fresh L1s anyway)
 #define LDX(ptr) (kCoh ? __ldcg(ptr) : *(ptr))
+// Touched-bitmap mode (IC, 64 colours): the items are the vertices of 1,024-vertex tiles of each
+// slot; item i of a tile is discovered iff its bit in the bitmap the expansion set is on (bits
+// are cleared as they are read). Same per-item work as a queue entry from then on.
 template <bool kCoh>
 __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __restrict__ tstart, uint64_t tstart_cap,
                                              uint32_t unit) {
     LevelRec* L = &a.lv[LDX(&a.ctl->level)];
-    const uint64_t nraw = umin64(LDX(&L->raw), a.raw_cap);
+    const bool bitmap = a.touched != nullptr;
+    const uint64_t nraw = bitmap ? (uint64_t)LDX(&a.ctl->slots) * a.tiles * kCompTile : umin64(LDX(&L->raw), a.raw_cap);
     if (blockIdx.x > 0 && (uint64_t)blockIdx.x * kCompTile >= nraw) return;  // no tile of this level
     if (threadIdx.x == 0) atomicMin(&a.ctl->c_start, global_ns());
     __shared__ unsigned long long wsum[kWarps];
@@ -172,12 +188,38 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long vc_local = 0;
+    uint32_t touched_local = 0;
     for (uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kCompTile) {
         uint64_t r[kCompItems];
+        if (bitmap) {
+            // tile t of slot t / tiles covers vertices 1024 (t % tiles) + [0, 1024); item it of
+            // thread x is vertex it * 256 + x of the tile: bit `lane` of word 8 it + warp
+            const uint64_t t = tile0 / kCompTile;
+            const uint32_t slot = (uint32_t)(t / a.tiles);
+            const uint32_t vbase = (uint32_t)(t % a.tiles) * kCompTile;
+            uint32_t* wp = a.touched + t * 32 + wid;
+            uint32_t wv[kCompItems];
 #pragma unroll
-        for (int it = 0; it < kCompItems; ++it) {
-            const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
-            r[it] = i < nraw ? LDX(&a.raw[i]) : ~0ull;
+            for (int it = 0; it < kCompItems; ++it) wv[it] = LDX(wp + 8 * it);
+            bool anyb = false;
+#pragma unroll
+            for (int it = 0; it < kCompItems; ++it) {
+                const bool on = (wv[it] >> lane) & 1u;
+                r[it] = on ? raw_pack(vbase + it * kThreads + threadIdx.x, slot, 0) : ~0ull;
+                anyb |= on;
+                touched_local += on;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < kCompItems; ++it)  // cleared for the next level
+                if (lane == it && wv[it]) wp[8 * it] = 0;
+            if (!__syncthreads_or(anyb)) continue;
+        } else {
+#pragma unroll
+            for (int it = 0; it < kCompItems; ++it) {
+                const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
+                r[it] = i < nraw ? LDX(&a.raw[i]) : ~0ull;
+            }
         }
         uint64_t mask[kCompItems];
         uint32_t rs[kCompItems], re[kCompItems];
@@ -295,12 +337,17 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
     // level statistics
     unsigned long long vc_tot = block_sum_ull(vc_local, vc_acc);
     if (threadIdx.x == 0 && vc_tot) atomicAdd(&L->vc, vc_tot);
+    if (bitmap) {
+        const unsigned long long tt = block_sum_ull(touched_local, vc_acc);
+        if (threadIdx.x == 0 && tt) atomicAdd(&L->raw, (unsigned)tt);
+    }
     if (threadIdx.x == 0) atomicMax(&a.ctl->c_end, global_ns());
 }
 
 
 __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
                                                       uint64_t tstart_cap, uint32_t unit) {
+    count_self(a.ctl);
     if (!a.ctl->cont) return;
     compact_body<false>(a, tstart, tstart_cap, unit);
 }
@@ -353,7 +400,7 @@ __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphCondi
     }
     const uint2 nx = __ldcg(reinterpret_cast<const uint2*>(&a.lv[Lv + 1].raw));  // {raw, overflow}
     R.pad = 0;
-    const uint32_t next_raw = nx.x, next_ovf = nx.y;
+    const uint32_t next_raw = a.touched ? __ldcg(&a.lv[Lv + 1].any) : nx.x, next_ovf = nx.y;
     c->work = C.work + (R.packed & kEdgeMask);
     c->entries = C.entries + (R.packed >> kPackShift);
     c->vc = C.vc + R.vc;
@@ -408,11 +455,11 @@ __device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphCondi
 // of (sample c, e) passes (reading C-2); surviving bits are OR-merged into N[u] (line 14,
 // the fusing step); the first setter of N[u] (per slice) enqueues u for level L+1.
 //
-// Warp-centric and barrier-free: a warp owns units of 128 consecutive work items (reverse
-// edge reads) as 4 windows of 32 lanes. The entry of every item comes from one coalesced
-// load of the next 128 entry offsets + a REDUX.OR of the entry starts per window (no
-// per-edge search). The 4 windows' loads are issued together (4x memory-level
-// parallelism). The live colours of all 128 edges are flattened into one list of
+// Warp-centric and barrier-free: a warp owns units of kUnitIC = 32 * kWinIC (96) consecutive
+// work items (reverse edge reads) as kWinIC windows of 32 lanes. The entry of every item comes
+// from the unit's first entry (tstart) + a popcount of the entry-start bitmap (no per-edge
+// search). The windows' loads are issued together (kWinIC x memory-level parallelism). The
+// live colours of all the unit's edges are flattened into one list of
 // (edge, colour) coin tasks evaluated 32 at a time (full lanes, no divergence to the
 // warp's maximum colour count). Discovered vertices go through a per-warp shared buffer,
 // so the global queue counter sees one atomic per >= 32 entries.
@@ -420,6 +467,7 @@ __device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphCondi
 #define BPT_WIN_IC 3
 #endif
 constexpr int kWinIC = BPT_WIN_IC;       // 32-lane windows per warp work unit
+static_assert(kWinIC >= 1 && kWinIC <= 4, "the window search packs <= 3 window prefixes into 8-bit fields");
 constexpr int kUnitIC = 32 * kWinIC;
 constexpr int kEbuf = 32 + kUnitIC;  // <= 31 pending + one unit's new entries
 
@@ -466,16 +514,16 @@ __device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, ui
         atomicOr(reinterpret_cast<uint32_t*>(&W.pass[w][o]) + (bit >> 5), 1u << (bit & 31));
 }
 
-// One 128-item unit. kWhole: all 128 items valid (every unit but the last of a level), so no
+// One kUnitIC-item unit. kWhole: all items valid (every unit but the last of a level), so no
 // per-lane predication is needed on the loads.
-template <bool kWhole, bool kC64, bool kCoh>
+template <bool kWhole, bool kC64, bool kBm, bool kCoh>
 __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane,
                                                uint32_t le_mask, uint32_t unit, uint32_t rem,
                                                uint32_t jc0, uint64_t gblk0, unsigned long long& coins,
-                                               unsigned long long& atoms) {
+                                               unsigned long long& atoms, bool& any_pass) {
     const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
     // ---- entry of every item: jc0 contains item 0; the compaction marked every entry start in
-    //      the unit's 128-bit mask (the unit's own mask is cleared here for the next level)
+    //      the unit's kUnitIC-bit mask (the unit's own mask is cleared here for the next level)
     uint32_t mw[kWinIC];
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) mw[w] = LDX(&a.umask[(size_t)unit * kWinIC + w]);
@@ -495,6 +543,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     uint2 rc[kWinIC];
     uint32_t vidx[kWinIC];
     uint64_t live[kWinIC];
+    bool nzero[kWinIC];  // N[u] was still empty when gathered (bitmap mode: this edge marks u)
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) ent[w] = LDX(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
 #pragma unroll
@@ -510,6 +559,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         vidx[w] = ent[w].y * a.n + rc[w].x;
         const ulonglong2 vn = kCoh ? ld_keep_cg(&a.VN[vidx[w]]) : ld_keep(&a.VN[vidx[w]]);
         live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
+        nzero[w] = vn.y == 0;
         if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
     }
     // ---- coin tasks of the whole unit, flattened into one list
@@ -568,7 +618,24 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         __syncwarp();
         if (lane == 0) coins += ntask;
     }
-    // ---- merges (Listing 1 line 14) of the 4 windows issued together
+    if constexpr (kBm) {
+        // ---- merges (Listing 1 line 14) without a return value: fire-and-forget ORs into N[u].
+        //      An edge that found N[u] empty also marks u in the touched bitmap: the first OR to
+        //      land on N[u] in this level came from such an edge (N is empty at level start), so
+        //      every vertex with a non-empty N is marked; the compaction scans the bitmap.
+#pragma unroll
+        for (int w = 0; w < kWinIC; ++w) {
+            if (pass[w]) {
+                ++atoms;
+                atomicOr(&a.VN[vidx[w]].y, pass[w]);
+                if (nzero[w])
+                    atomicOr(&a.touched[(size_t)ent[w].y * a.tiles * 32 + (rc[w].x >> 5)], 1u << (rc[w].x & 31));
+                any_pass = true;
+            }
+        }
+        return;
+    }
+    // ---- merges (Listing 1 line 14) of the windows issued together
     unsigned long long old[kWinIC];
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
@@ -613,7 +680,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
 #ifndef BPT_EXPAND_MINB
 #define BPT_EXPAND_MINB 5
 #endif
-template <bool kC64, bool kCoh>
+template <bool kC64, bool kBm, bool kCoh>
 __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_t* __restrict__ tstart,
                                                cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
@@ -648,15 +715,20 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     const uint32_t nfull = (uint32_t)(total / kUnitIC);
     const uint32_t nwarps = active * kWarps;
     unsigned long long coins = 0, atoms = 0;
+    bool any_pass = false;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = LDX(&tstart[unit]);
         if (unit < nfull)
-            expand_unit_ic<true, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms);
+            expand_unit_ic<true, kC64, kBm, kCoh>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
         else
-            expand_unit_ic<false, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
-                                        jc0, gblk0, coins, atoms);
+            expand_unit_ic<false, kC64, kBm, kCoh>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
+                                        jc0, gblk0, coins, atoms, any_pass);
     }
-    warp_flush(a, Ln, W, lane);
+    if constexpr (kBm) {
+        if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
+    } else {
+        warp_flush(a, Ln, W, lane);
+    }
     unsigned long long ct = block_sum_ull(coins, red);
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
@@ -664,11 +736,178 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     finish_expand(a, h_level, use_cond, active);
 }
 
-template <bool kC64>
+// kBm: touched-bitmap mode (64 colours; a.touched != nullptr), else the first-setter queue
+template <bool kC64, bool kBm>
 __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                               cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
     if (!a.ctl->cont) return;
-    expand_ic_body<kC64, false>(a, tstart, h_level, use_cond);
+    static_assert(kC64 || !kBm, "the touched bitmap needs 64-colour groups");
+    expand_ic_body<kC64, kBm, false>(a, tstart, h_level, use_cond);
+}
+
+// ------------------------------------------------------------------------ IC expansion, task lists
+// The product's IC expansion (64 colours, touched-bitmap frontier). Same units, entry lookup and
+// loads as expand_unit_ic; the coins differ in how the live (edge, colour) pairs reach the lanes:
+// every lane writes its own pairs, lowest colour first, as 16-bit task words (item << 6 | colour)
+// into a per-warp list at its exclusive prefix, and the warp then evaluates the list 32 tasks at
+// a time -- one shared-memory read decodes a task (no owner search, no rank select). A lane's
+// write loop runs once per live colour of its items (0 for most edges; ~1.4 for a live edge at
+// the heavy levels). Passing colours are OR-merged per item in shared memory, then into N[u]
+// with one fire-and-forget OR per item (Listing 1 line 14), and u is marked in the touched
+// bitmap when its N was empty at the gather (see expand_unit_ic).
+constexpr uint32_t kTaskCap = 256;  // task words per warp per pass (a unit with more runs several passes)
+
+struct TaskScratch {
+    uint2 et[kUnitIC];                     // per item: {edge id, threshold}
+    uint32_t sb[kUnitIC];                  // per item: global id of colour 0 of its block
+    uint32_t pass[kUnitIC][2];             // per item: passing colours (ATOMS.OR on 32-bit halves)
+    unsigned short task[kTaskCap];         // item << 6 | colour
+};
+
+template <bool kWhole>
+__device__ __forceinline__ void expand_unit_tasks(const BatchArgs& a, TaskScratch& W, int lane, uint32_t le_mask,
+                                                  uint32_t unit, uint32_t rem, uint32_t jc0, uint64_t gblk0,
+                                                  unsigned long long& coins, unsigned long long& atoms,
+                                                  bool& any_pass) {
+    const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
+    // ---- entry of every item (jc0 holds item 0; the compaction marked every entry start)
+    uint32_t mw[kWinIC];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[(size_t)unit * kWinIC + w];
+    __syncwarp();
+    if (lane < kWinIC) a.umask[(size_t)unit * kWinIC + lane] = 0;
+    mw[0] &= ~1u;
+    uint32_t jl[kWinIC];
+    uint32_t before = jc0;
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        jl[w] = before + __popc(mw[w] & le_mask);
+        before += __popc(mw[w]);
+    }
+    // ---- loads of the windows issued together
+    uint4 ent[kWinIC];
+    uint2 rc[kWinIC];
+    uint32_t vidx[kWinIC];  // working-mask index slot * n + u of the item's source vertex
+    uint32_t tword[kWinIC]; // its touched-bitmap word, ~0 if N[u] was not empty at the gather
+    uint32_t tbits = 0;     // 5-bit positions of u in those words
+    uint64_t left[kWinIC];  // live colours whose coins are not evaluated yet
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) ent[w] = a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0];
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
+    }
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        vidx[w] = ent[w].y * a.n + rc[w].x;
+        const ulonglong2 vn = ld_keep(&a.VN[vidx[w]]);
+        left[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
+        tword[w] = vn.y == 0 ? ent[w].y * a.tiles * 32 + (rc[w].x >> 5) : ~0u;
+        tbits |= (rc[w].x & 31u) << (5 * w);
+        if (!kWhole && 32u * w + lane >= rem) left[w] = 0;
+    }
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) tot += __popcll(left[w]);
+    if (!__any_sync(kFull, tot != 0)) return;
+    // ---- coin tasks: per-item data, then the lanes' task words, evaluated 32 at a time
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        const uint32_t it = 32u * w + lane;
+        W.et[it] = make_uint2(t0l + it + ent[w].x, rc[w].y);
+        W.sb[it] = (uint32_t)(64ull * (gblk0 + ent[w].y));
+        W.pass[it][0] = 0;
+        W.pass[it][1] = 0;
+    }
+    while (true) {  // one pass per kTaskCap tasks (one pass for nearly every unit)
+        const uint32_t incl = warp_incl_scan_u32(tot, lane);
+        const uint32_t ntask = __shfl_sync(kFull, incl, 31);
+        uint32_t pos = incl - tot;
+#pragma unroll
+        for (int w = 0; w < kWinIC; ++w) {
+            while (left[w] && pos < kTaskCap) {
+                const uint32_t b = __ffsll((long long)left[w]) - 1;
+                W.task[pos++] = (unsigned short)(((32u * w + lane) << 6) | b);
+                left[w] &= left[w] - 1;
+            }
+        }
+        __syncwarp();
+        const uint32_t nt = min(ntask, kTaskCap);
+        for (uint32_t k = lane; k < nt; k += 32) {
+            const uint32_t t = W.task[k];
+            const uint32_t it = t >> 6, b = t & 63u;
+            const uint2 x = W.et[it];
+            const uint32_t r = philox2x32_10(x.x, W.sb[it] + b, a.k_ic).x;
+            if ((r >> 1) < x.y) atomicOr(&W.pass[it][b >> 5], 1u << (b & 31));
+        }
+        if (lane == 0) coins += nt;
+        __syncwarp();
+        if (ntask <= kTaskCap) break;
+        tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWinIC; ++w) tot += __popcll(left[w]);
+    }
+    // ---- merges: fire-and-forget ORs into N[u]; u marked in the touched bitmap when its N was empty
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        const uint32_t it = 32u * w + lane;
+        const uint64_t pass = ((uint64_t)W.pass[it][1] << 32) | W.pass[it][0];
+        if (pass) {
+            ++atoms;
+            atomicOr(&a.VN[vidx[w]].y, pass);
+            if (tword[w] != ~0u) atomicOr(&a.touched[tword[w]], 1u << ((tbits >> (5 * w)) & 31u));
+            any_pass = true;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_tasks(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                                 cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
+    if (!a.ctl->cont) return;
+    Ctl* ctl = a.ctl;
+    const uint32_t level = ctl->level;
+    const uint64_t gblk0 = ctl->gblk0;
+    const LevelRec* L = &a.lv[level];
+    LevelRec* Ln = &a.lv[level + 1];
+    const unsigned long long packed = L->packed;
+    const uint64_t nq = packed >> kPackShift;
+    const uint64_t total = packed & kEdgeMask;
+    const bool idle = nq == 0 || L->overflow;
+    const uint32_t active =
+        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kUnitIC * kWarps - 1) / ((uint64_t)kUnitIC * kWarps)));
+    if (blockIdx.x >= active) return;
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    if (idle) {
+        finish_expand(a, h_level, use_cond, active);
+        return;
+    }
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TaskScratch& W = reinterpret_cast<TaskScratch*>(smem_raw)[threadIdx.x >> 5];
+    __shared__ unsigned long long red[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
+    const uint32_t nunits = (uint32_t)((total + kUnitIC - 1) / kUnitIC);
+    const uint32_t nfull = (uint32_t)(total / kUnitIC);
+    const uint32_t nwarps = active * kWarps;
+    unsigned long long coins = 0, atoms = 0;
+    bool any_pass = false;
+    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
+        const uint32_t jc0 = tstart[unit];
+        if (unit < nfull)
+            expand_unit_tasks<true>(a, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
+        else
+            expand_unit_tasks<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC), jc0, gblk0,
+                                     coins, atoms, any_pass);
+    }
+    if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
+    unsigned long long ct = block_sum_ull(coins, red);
+    if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
+    unsigned long long at = block_sum_ull(atoms, red);
+    if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
+    finish_expand(a, h_level, use_cond, active);
 }
 
 // ------------------------------------------------------------------------ wide fusion (IC)
@@ -686,6 +925,7 @@ using CumW = std::conditional_t<(kVW <= 4), uint32_t, unsigned long long>;
 constexpr int kCumBits = kVW <= 4 ? 8 : 9;
 
 __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
     const uint64_t total = (uint64_t)a.ctl->slots * 64;
     const uint64_t gblk0 = a.ctl->gblk0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -712,6 +952,7 @@ __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int us
 // A4 for wide entries: for each queued vertex v: masks m_b = N_b; V_b |= N_b; N_b = 0; vflag = 0.
 __global__ void __launch_bounds__(kThreads, 5) k_compact_w(BatchArgs a, uint32_t* __restrict__ tstart,
                                                         uint64_t tstart_cap) {
+    count_self(a.ctl);
     if (!a.ctl->cont) return;
     LevelRec* L = &a.lv[a.ctl->level];
     const uint64_t nraw = umin64(L->raw, a.raw_cap);
@@ -1039,6 +1280,7 @@ __device__ __forceinline__ void expand_unit_w(const BatchArgs& a, LevelRec* Ln, 
 __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_w(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                              cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
+    count_self(ctl);
     if (!ctl->cont) return;
     const uint32_t level = ctl->level;
     const uint64_t gblk0 = ctl->gblk0;
@@ -1497,6 +1739,7 @@ __device__ __forceinline__ void expand_lt_body(const BatchArgs& a, const uint32_
 
 __global__ void __launch_bounds__(kThreads) k_expand_lt(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                       cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
     if (!a.ctl->cont) return;
     expand_lt_body<false>(a, tstart, h_level, use_cond);
 }
@@ -1524,20 +1767,9 @@ __device__ __forceinline__ void grid_barrier(Ctl* c) {
     __syncthreads();
 }
 
-// IC: the same cooperative level loop (BPT_IC_PERSIST=1); same-launch data is read through L2.
-template <bool kC64>
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_levels_ic(BatchArgs a, uint32_t* __restrict__ tstart,
-                                                                       uint64_t tstart_cap) {
-    while (__ldcg(&a.ctl->cont)) {
-        compact_body<true>(a, tstart, tstart_cap, kUnitIC);
-        grid_barrier(a.ctl);
-        expand_ic_body<kC64, true>(a, tstart, (cudaGraphConditionalHandle)0, 0);
-        grid_barrier(a.ctl);
-    }
-}
-
 __global__ void __launch_bounds__(kThreads) k_levels_lt(BatchArgs a, uint32_t* __restrict__ tstart,
                                                       uint64_t tstart_cap) {
+    count_self(a.ctl);
     while (__ldcg(&a.ctl->cont)) {
         compact_body<true>(a, tstart, tstart_cap, kTile);
         grid_barrier(a.ctl);
@@ -1554,6 +1786,7 @@ __global__ void __launch_bounds__(kThreads) k_levels_lt(BatchArgs a, uint32_t* _
 // condition (stop early on an error).
 __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, int use_cond) {
     Ctl* c = a.ctl;
+    count_self(c);
     const uint32_t used = c->level + 2;
     for (uint32_t i = threadIdx.x; i < used && i < (uint32_t)kMaxLevels; i += blockDim.x) {
         LevelRec z{};
@@ -1574,9 +1807,9 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 
 int g_expand_grid = 0;
 int g_expand_grid_w = 0;
+int g_expand_grid_t = 0;
 int g_expand_grid_lt = 0;
-int g_levels_grid_lt = 0;
-int g_levels_grid_ic = 0;
+int g_levels_per_sm_lt = 0;  // co-resident blocks per SM of the cooperative LT loop
 int g_compact_grid = 0;
 
 }  // namespace
@@ -1633,13 +1866,18 @@ int expand_grid() {
     if (!g_expand_grid) {
         int per_sm = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_lt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
-        BPT_CUDA(cudaFuncSetAttribute(k_expand_ic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(WarpScratch) * kWarps)));
-        BPT_CUDA(cudaFuncSetAttribute(k_expand_ic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(WarpScratch) * kWarps)));
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true>, kThreads,
+        for (void* f : {(void*)k_expand_ic<true, true>, (void*)k_expand_ic<true, false>, (void*)k_expand_ic<false, false>})
+            BPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(WarpScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true, true>, kThreads,
                                                                sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(TaskScratch) * kWarps)));
+        int per_sm_t = 0;
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_expand_tasks, kThreads,
+                                                               sizeof(TaskScratch) * kWarps));
+        g_expand_grid_t = num_sms() * (per_sm_t > 0 ? per_sm_t : 1);
         int per_sm_w = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(WarpScratchW) * kWarps)));
@@ -1652,17 +1890,7 @@ int expand_grid() {
         int per_sm_pl = 0;  // the cooperative level loop must be co-resident
         BPT_CUDA(cudaFuncSetAttribute(k_levels_lt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pl, k_levels_lt, kThreads, sizeof(SmemTile)));
-        // few blocks: the levels are thin, and a grid barrier costs ~ the number of blocks
-        const char* gs = getenv("BPT_LT_BLOCKS_PER_SM");
-        const int want = gs ? atoi(gs) : 1;
-        g_levels_grid_lt = num_sms() * std::max(1, std::min(want, per_sm_pl > 0 ? per_sm_pl : 1));
-        int per_sm_pi = 0;
-        for (void* f : {(void*)k_levels_ic<true>, (void*)k_levels_ic<false>})
-            BPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(sizeof(WarpScratch) * kWarps)));
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pi, k_levels_ic<true>, kThreads,
-                                                               sizeof(WarpScratch) * kWarps));
-        g_levels_grid_ic = num_sms() * (per_sm_pi > 0 ? per_sm_pi : 1);
+        g_levels_per_sm_lt = per_sm_pl > 0 ? per_sm_pl : 1;
         int per_sm_c = 0;
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact, kThreads, 0));
         g_compact_grid = num_sms() * (per_sm_c > 0 ? per_sm_c : 1);
@@ -1670,15 +1898,15 @@ int expand_grid() {
     return g_expand_grid;
 }
 
-// LT batches run their level loop as one cooperative launch (BPT_LT_PERSIST=0: per-level launches)
-bool level_loop_persistent(const BatchArgs& a) {
-    if (a.wide) return false;
-    if (a.model == BPT_IC) {
-        const char* pi = getenv("BPT_IC_PERSIST");
-        return pi && pi[0] == '1';
-    }
-    const char* pl = getenv("BPT_LT_PERSIST");
-    return !(pl && pl[0] == '0');
+// Fused LT batches run their level loop as one cooperative launch (BPT_FLAG_LT_LEVELS: per-level
+// launches instead); IC always launches per level (a cooperative IC loop measured slower: its
+// same-launch data would have to bypass L1, DESIGN §11 (h))
+bool level_loop_persistent(const BatchArgs& a) { return a.model == BPT_LT && !a.wide && a.lt_persist; }
+
+// few blocks: the LT levels are thin, and a grid barrier costs ~ the number of blocks
+static unsigned levels_grid_lt(const BatchArgs& a) {
+    expand_grid();
+    return (unsigned)(num_sms() * std::max(1, std::min(a.lt_blocks_per_sm > 0 ? a.lt_blocks_per_sm : 1, g_levels_per_sm_lt)));
 }
 
 static unsigned init_grid(const BatchArgs& a) { return (unsigned)(((uint64_t)a.slots_max * 64 + 255) / 256); }
@@ -1707,10 +1935,12 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
     }
     k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model));
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
-    if (a.model == BPT_IC && a.colors == 64)
-        k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
+    if (a.model == BPT_IC && a.touched)
+        k_expand_tasks<<<g_expand_grid_t, kThreads, sizeof(TaskScratch) * kWarps, st>>>(a, tstart, h0, 0);
+    else if (a.model == BPT_IC && a.colors == 64)
+        k_expand_ic<true, false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
-        k_expand_ic<false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        k_expand_ic<false, false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else
         k_expand_lt<<<g_expand_grid_lt, kThreads, sizeof(SmemTile), st>>>(a, tstart, h0, 0);
     if (ev1) BPT_CUDA(cudaEventRecord(ev1, st));
@@ -1769,12 +1999,8 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     if (lt_persist) {
         // the whole level loop as one cooperative launch (grid barriers between phases)
         void* lv_args[] = {&args, &tstart, &tstart_cap};
-        cudaGraphNode_t n_lv =
-            a.model == BPT_IC
-                ? add_kernel(body, &n_init, a.colors == 64 ? (void*)k_levels_ic<true> : (void*)k_levels_ic<false>,
-                             dim3(g_levels_grid_ic), dim3(kThreads), sizeof(WarpScratch) * kWarps, lv_args)
-                : add_kernel(body, &n_init, (void*)k_levels_lt, dim3(g_levels_grid_lt), dim3(kThreads),
-                             sizeof(SmemTile), lv_args);
+        cudaGraphNode_t n_lv = add_kernel(body, &n_init, (void*)k_levels_lt, dim3(levels_grid_lt(a)), dim3(kThreads),
+                                          sizeof(SmemTile), lv_args);
         cudaLaunchAttributeValue coop{};
         coop.cooperative = 1;
         BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
@@ -1806,8 +2032,11 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     cudaGraphNode_t n_exp = a.wide
         ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),
                      sizeof(WarpScratchW) * kWarps, exp_args)
+        : a.model == BPT_IC && a.touched
+        ? add_kernel(lbody, &n_cmp, (void*)k_expand_tasks, dim3(g_expand_grid_t), dim3(kThreads),
+                     sizeof(TaskScratch) * kWarps, exp_args)
         : a.model == BPT_IC
-        ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
+        ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true, false> : (void*)k_expand_ic<false, false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
     // the expansion's last block advances the level and sets the loop condition

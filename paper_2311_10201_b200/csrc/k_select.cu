@@ -218,7 +218,8 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     BPT_CUDA(cudaMemsetAsync(cov.p, 0, blocks * 8 + 8, st));
     BPT_CUDA(cudaMemsetAsync(keys.p, 0, (uint64_t)k * 8, st));
     const unsigned vgrid = (unsigned)umin64(((uint64_t)n + 4 * kSelThreads - 1) / (4 * kSelThreads), (uint64_t)num_sms() * 4);
-    const unsigned ggrid = (unsigned)umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4);
+    // >= 1 block: a rank without local blocks still marks v* selected (and joins every collective)
+    const unsigned ggrid = (unsigned)umax64(1, umin64((blocks + 255) / 256, (uint64_t)num_sms() * 4));
     const unsigned dgrid = (unsigned)umin64(((uint64_t)n + 255) / 256, (uint64_t)num_sms() * 8);
     const uint64_t shard_len = (uint64_t)S.n_pad / world;
     using clk = std::chrono::steady_clock;

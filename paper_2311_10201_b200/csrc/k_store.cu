@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     __shared__ unsigned long long s_mask[kW][32];
     __shared__ uint32_t s_size[kW][64];
     __shared__ unsigned long long s_el[kW];
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)  // launch evidence (Ctl::kernels_run)
+        atomicAdd(&const_cast<Ctl*>(ctl)->kernels_run, 1ull);
     if (blockIdx.y >= ctl->slots) return;
     const uint64_t blk = ctl->blk0 + blockIdx.y;
     uint64_t* V = store + (size_t)blk * n;

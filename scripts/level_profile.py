@@ -41,7 +41,7 @@ def main():
         out[f"ms_expand_{mode}"] = info["ms_expand"]
         st = s.level_stats()
         s.close()
-    st = np.asarray(st, dtype=np.int64).reshape(-1, 6)
+    st = np.asarray(st, dtype=np.int64).reshape(-1, 8)
     work = st[:, 4]
     raw = st[:, 2]
     out["levels"] = int(len(st))

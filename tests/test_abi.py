@@ -35,9 +35,12 @@ def test_header_constants_match_binding():
     """Every #define / enum value of include/bpt.h that the binding mirrors has the same value."""
     import paper_2311_10201_b200 as bpt
     hdr = open(os.path.join(ROOT, "include", "bpt.h")).read()
-    defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z]+) (\w+)", hdr)}
-    assert defs == {"BPT_FLAG_PROFILE": bpt.FLAG_PROFILE, "BPT_FLAG_WIDE": bpt.FLAG_WIDE,
-                    "BPT_FLAG_SPARSE": bpt.FLAG_SPARSE}
+    defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z_]+) (\w+)", hdr)}
+    assert defs == {f"BPT_{name}": getattr(bpt, name) for name in
+                    ("FLAG_PROFILE", "FLAG_WIDE", "FLAG_SPARSE", "FLAG_LT_FUSED", "FLAG_LT_DENSE", "FLAG_LT_REWALK",
+                     "FLAG_LT_LEVELS", "FLAG_QUEUE")}
+    flags = list(defs.values())
+    assert len(set(flags)) == len(flags) and all(f & (f - 1) == 0 for f in flags)  # distinct single bits
     enums = dict((k, int(v)) for k, v in re.findall(r"(BPT_E[A-Z]+|BPT_OK)\s*=\s*(-?\d+)", hdr))
     for k in ("BPT_OK", "BPT_EINVAL", "BPT_ENOMEM", "BPT_ECUDA", "BPT_ENCCL", "BPT_ESTATE"):
         assert enums[k] == getattr(bpt, k)

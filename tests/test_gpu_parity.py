@@ -42,6 +42,42 @@ def check_full(bpt, s, ref, theta):
     assert np.array_equal(mem, ref["members"])
 
 
+# ------------------------------------------------------------------ coins (reading C-1), device side
+
+def test_device_philox_kat(bpt):
+    """SURVEY §8(c) P-1 on the device: the Philox2x32-10 every coin and start vertex of the CUDA
+    path goes through reproduces the Random123 known-answer vectors, and agrees with the oracle's
+    independent copy on random counters."""
+    kat = json.load(open(os.path.join(GOLD, "philox_kat.json")))["philox2x32_10"]
+    rows = np.array([[int(c0, 16), int(c1, 16), int(k, 16)] for c0, c1, k, _, _ in kat], np.uint32)
+    want = np.array([[int(o0, 16), int(o1, 16)] for _, _, _, o0, o1 in kat], np.uint32)
+    assert np.array_equal(bpt.selftest_philox(rows), want)
+    rng = np.random.default_rng(11)
+    r = rng.integers(0, 1 << 32, size=(2000, 3), dtype=np.uint64).astype(np.uint32)
+    got = bpt.selftest_philox(r)
+    for i in range(0, 2000, 97):
+        assert tuple(int(x) for x in got[i]) == oracle.philox2x32_10(int(r[i, 0]), int(r[i, 1]), int(r[i, 2]))
+
+
+def test_launch_evidence_counts(bpt):
+    """bpt_kernel_launch_count counts host launches (one per graph launch in graph mode);
+    bpt_graph_kernel_count counts the kernels the sampling graph ran, counted on the device:
+    per batch init + finalize + next_batch, per level compact + expand."""
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    h0, d0 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
+    s = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1)
+    h1, d1 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
+    info = s.info
+    assert h1 - h0 == 1  # the graph launch
+    assert d1 - d0 == 3 * info["batches"] + 2 * info["levels_total"]
+    assert info["kernel_launches"] == (h1 - h0) + (d1 - d0)
+    p = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1, profile=True)
+    assert bpt.graph_kernel_count() == d1  # profile mode launches directly
+    assert bpt.kernel_launch_count() - h1 >= 3 * p.info["batches"] + 2 * p.info["levels_total"]
+
+
 # ------------------------------------------------------------------ A0/A1 builder
 
 def test_reverse_csr_equals_oracle_transpose(bpt):
@@ -269,14 +305,13 @@ def test_ragged_theta_and_ranges(bpt):
             assert np.array_equal(off, ref["offsets"][first:first + count + 1] - ref["offsets"][first])
 
 
-@pytest.mark.parametrize("mode", ["ic", "ic_wide", "lt", "lt_dense"])
-def test_graph_without_edges(bpt, monkeypatch, mode):
+@pytest.mark.parametrize("mode", ["ic", "ic_queue", "ic_wide", "lt", "lt_dense", "lt_fused"])
+def test_graph_without_edges(bpt, mode):
     n = 10
-    if mode == "lt_dense":
-        monkeypatch.setenv("BPT_LT_DENSE", "1")
+    flags = {"lt_dense": bpt.FLAG_LT_DENSE, "lt_fused": bpt.FLAG_LT_FUSED, "ic_queue": bpt.FLAG_QUEUE}.get(mode, 0)
     model = bpt.LT if mode.startswith("lt") else bpt.IC
     g = bpt.Graph(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), w_q31=np.zeros(0, np.uint32), model=model)
-    s = g.sample(100, seed=4, wide=mode == "ic_wide")
+    s = g.sample(100, seed=4, wide=mode == "ic_wide", flags=flags)
     off, mem = s.extract(0, 100)
     assert mem.tolist() == [oracle.start_vertex(i, n, 4) for i in range(100)]
     seeds, gains, sigma = s.select_seeds(n)
@@ -317,42 +352,41 @@ def test_lt_parity_scaled(bpt):
 
 
 @pytest.mark.parametrize("model", ["IC", "LT"])
-def test_level_loop_variants(bpt, monkeypatch, model):
-    """The execution models of the sampling loop give the same RRR sets, seeds and exact work
-    counters: per-level launches inside the graph's conditional WHILE node, one cooperative
-    launch per batch with grid barriers (LT fused default; IC opt-in BPT_IC_PERSIST=1), the
-    host-driven profiling mode, and for LT the one-walk-per-thread sampler (LT default)."""
+def test_level_loop_variants(bpt, model):
+    """The execution forms of the sampling loop give the same RRR sets, seeds and exact work
+    counters. IC: the touched-bitmap frontier (default) and the first-setter queue
+    (BPT_FLAG_QUEUE), each in the graph's conditional WHILE loop and in the host-driven profiling
+    mode. LT: the fused level-synchronous loop (one cooperative launch per batch, or per-level
+    launches with BPT_FLAG_LT_LEVELS) and the one-walk-per-thread sampler (default; sparse
+    member-list store, lists by a second walk, or the dense store)."""
     if model == "IC":
         cfg = graphgen.CONFIGS["C1"]
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr)
-        variants = [{"BPT_IC_PERSIST": "1"}, {"BPT_IC_PERSIST": "0"}]
+        variants = [0, bpt.FLAG_QUEUE]
     else:
         cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 12, theta=2048)
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.LT, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
-        variants = [{"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "0"}, {"BPT_LT_FUSED": "1", "BPT_LT_PERSIST": "1"},
-                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "0"},   # walks, sparse store (default)
-                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "0", "BPT_LT_REWALK": "1"},  # lists by a 2nd walk
-                    {"BPT_LT_FUSED": "0", "BPT_LT_DENSE": "1"}]   # walks, dense store
+        variants = [bpt.FLAG_LT_FUSED | bpt.FLAG_LT_LEVELS, bpt.FLAG_LT_FUSED,
+                    0,                        # walks, sparse store (default)
+                    bpt.FLAG_LT_REWALK,       # lists by a 2nd walk
+                    bpt.FLAG_LT_DENSE]        # walks, dense store
     infos = []
-    for env in variants:
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
+    for vflags in variants:
         rows = []
         for colors, batch, profile in ((64, 1, False), (64, 5, False), (8, 2, False), (64, 3, True)):
-            s = g.sample(cfg.theta, colors=colors, seed=cfg.seed, batch_groups=batch, profile=profile)
+            s = g.sample(cfg.theta, colors=colors, seed=cfg.seed, batch_groups=batch, profile=profile, flags=vflags)
             check_full(bpt, s, ref, cfg.theta)
             seeds, gains, _ = s.select_seeds(cfg.k)
             assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
             info = s.info
-            walker = model == "LT" and env.get("BPT_LT_FUSED") == "0"
+            walker = model == "LT" and not (vflags & bpt.FLAG_LT_FUSED)
             if walker:
                 dense_bytes = (cfg.theta + 63) // 64 * cfg.n * 8
-                assert (info["store_bytes"] >= dense_bytes) == (env["BPT_LT_DENSE"] == "1")
-                monkeypatch.delenv("BPT_LT_REWALK", raising=False)  # bitmap vs lists
+                assert (info["store_bytes"] >= dense_bytes) == bool(vflags & bpt.FLAG_LT_DENSE)
             rows.append((info["e_phys"], info["e_logical"], info["members"]) if walker else
                         (colors, batch, info["e_phys"], info["e_logical"], info["members"], info["levels_total"]))
             s.close()
