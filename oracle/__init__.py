@@ -66,6 +66,16 @@ def lib():
     L.or_greedy.restype = _i
     L.or_sigma_hat.argtypes = [_u32, _u64, _u64]
     L.or_sigma_hat.restype = ctypes.c_double
+    L.or_store_build.argtypes = [_p, _u64, _u64, _u64, _u32, _i, _u32]
+    L.or_store_build.restype = _p
+    L.or_store_free.argtypes = [_p]
+    L.or_store_free.restype = None
+    L.or_store_info.argtypes = [_p, _p, _p, _p, _p, _p, _p]
+    L.or_store_info.restype = None
+    L.or_store_members.argtypes = [_p, _u64, _p]
+    L.or_store_members.restype = _u32
+    L.or_store_greedy.argtypes = [_p, _u32, _p, _p]
+    L.or_store_greedy.restype = _i
     return L
 
 
@@ -177,6 +187,51 @@ class Graph:
         lib().or_group_work(self._h, seed, s0, s1, _ptr(ep), _ptr(el), _ptr(lv), _ptr(fr), cap)
         return {"e_phys": int(ep[0]), "e_logical": int(el[0]), "levels": int(lv[0]),
                 "frontier": fr[: int(lv[0])].copy()}
+
+
+class Store:
+    """RRR store of samples [s0, s0 + count) (SURVEY §8(c) oracle step 3: sorted lists for small
+    sets, n-bit bitsets for large ones), with per-group E_phys / level structure and a greedy
+    that runs on it -- so full-size configs fit host memory (C2: ~20 GB instead of ~190 GB)."""
+
+    def __init__(self, graph: "Graph", seed: int, s0: int, count: int, colors: int = 64,
+                 threads: int | None = None, list_max: int = 0):
+        self.graph, self.count, self.colors, self.n = graph, count, colors, graph.n
+        self.ngroups = (count + colors - 1) // colors
+        h = lib().or_store_build(graph._h, seed, s0, count, colors, threads or default_threads(), list_max)
+        if not h:
+            raise ValueError("oracle store: IC only, and BFS levels must stay below 64")
+        self._h = h
+        self.sizes = np.empty(count, dtype=np.uint32)
+        self.digests = np.empty(count, dtype=np.uint64)
+        self.e_phys = np.empty(self.ngroups, dtype=np.uint64)
+        self.levels = np.empty(self.ngroups, dtype=np.uint32)
+        self.frontier = np.empty((self.ngroups, 64), dtype=np.uint64)
+        el = np.zeros(1, dtype=np.uint64)
+        lib().or_store_info(h, _ptr(self.sizes), _ptr(self.digests), _ptr(self.e_phys), _ptr(self.levels),
+                            _ptr(self.frontier), _ptr(el))
+        self.e_logical = int(el[0])
+
+    def members(self, i: int) -> np.ndarray:
+        out = np.empty(max(int(self.sizes[i]), 1), dtype=np.uint32)
+        c = lib().or_store_members(self._h, i, _ptr(out))
+        return out[:c].copy()
+
+    def greedy(self, k: int):
+        seeds = np.empty(k, dtype=np.uint32)
+        gains = np.empty(k, dtype=np.uint64)
+        if lib().or_store_greedy(self._h, k, _ptr(seeds), _ptr(gains)) != 0:
+            raise ValueError("oracle store greedy: bad k")
+        return seeds, gains
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().or_store_free(h)
+            except Exception:
+                pass
+            self._h = None
 
 
 def greedy(n: int, set_off, members, k: int, lazy: bool = False):

@@ -475,3 +475,191 @@ int or_greedy(uint32_t n, uint64_t nsets, const uint64_t* set_off, const uint32_
 double or_sigma_hat(uint32_t n, uint64_t covered, uint64_t theta) {
     return (double)n * (double)covered / (double)theta;
 }
+
+/* ------------------------------------------------------------------------------------
+ * RRR store of a sample range (SURVEY §8(c) oracle step 3): every sample kept as a
+ * sorted u32 member list if |RR_s| <= list_max (default n/32), else as an n-bit
+ * bitset (bit v of word v/64 set iff v in RR_s). Built group by group (traversal
+ * group = `colors` consecutive samples, reading C-9): for each group the distinct
+ * (v, L) pairs reached by its samples (L = BFS level d_s(v) < 64) give
+ *     E_phys(group)      = sum over distinct (v, L) of indeg(v)
+ *     frontier(group)[L] = number of distinct v with some d_s(v) = L
+ * -- the definitions or_group_work uses, counted with a per-vertex level mask instead
+ * of a sort (levels >= 64 make the call fail; IC levels are ~10).
+ * Greedy on the store: max-k-cover (reading C-11) with the occurrence count
+ * of every vertex kept current: a newly covered sample leaves the count of each of
+ * its members (the gain of v = number of uncovered samples containing v).
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t n, colors;
+    uint64_t s0, count, ngroups;
+    uint32_t list_max;
+    uint32_t* size;        /* [count] */
+    uint64_t* digest;      /* [count] */
+    uint32_t** list;       /* [count] sorted members, or NULL */
+    uint64_t** bits;       /* [count] n-bit set, or NULL */
+    uint64_t* e_phys;      /* [ngroups] */
+    uint32_t* levels;      /* [ngroups] */
+    uint64_t* frontier;    /* [ngroups][64] */
+    uint64_t e_logical;
+} or_store;
+
+typedef struct {
+    const or_graph* g; or_keys k; or_store* S; atomic_ulong next; atomic_int fail;
+    pthread_mutex_t mu;
+} store_job;
+
+static void* store_worker(void* arg) {
+    store_job* J = (store_job*)arg;
+    or_store* S = J->S;
+    const or_graph* g = J->g;
+    or_scratch w; scratch_init(&w, g->n);
+    uint64_t* lvmask = (uint64_t*)calloc(g->n, sizeof(uint64_t));
+    uint32_t* touched = (uint32_t*)malloc((size_t)g->n * sizeof(uint32_t));
+    uint64_t el_sum = 0;
+    for (;;) {
+        uint64_t grp = atomic_fetch_add(&J->next, 1);   /* claim one traversal group */
+        if (grp >= S->ngroups) break;
+        uint64_t a = grp * S->colors, b = a + S->colors;
+        if (b > S->count) b = S->count;
+        uint32_t ntouched = 0;
+        for (uint64_t i = a; i < b; i++) {
+            uint64_t el = 0;
+            uint32_t size = run_sample(g, &J->k, S->s0 + i, &w, &el);
+            el_sum += el;
+            uint64_t d = 0;
+            for (uint32_t j = 0; j < size; j++) {
+                uint32_t v = w.queue[j], L = w.level[v];
+                d += or_digest_mix(v);
+                if (L >= 64) { atomic_store(&J->fail, 1); continue; }
+                if (!lvmask[v]) touched[ntouched++] = v;
+                lvmask[v] |= 1ULL << L;
+            }
+            S->size[i] = size; S->digest[i] = d;
+            if (size <= S->list_max) {
+                uint32_t* l = (uint32_t*)malloc((size ? size : 1) * sizeof(uint32_t));
+                memcpy(l, w.queue, (size_t)size * sizeof(uint32_t));
+                qsort(l, size, sizeof(uint32_t), cmp_u32);
+                S->list[i] = l;
+            } else {
+                uint64_t* bs = (uint64_t*)calloc(((size_t)S->n + 63) / 64, sizeof(uint64_t));
+                for (uint32_t j = 0; j < size; j++) bs[w.queue[j] >> 6] |= 1ULL << (w.queue[j] & 63);
+                S->bits[i] = bs;
+            }
+        }
+        uint64_t ep = 0; uint32_t nlev = 0;
+        uint64_t* fr = S->frontier + grp * 64;
+        for (uint32_t t = 0; t < ntouched; t++) {
+            uint32_t v = touched[t];
+            uint64_t m = lvmask[v];
+            ep += (g->roff[v + 1] - g->roff[v]) * (uint64_t)__builtin_popcountll(m);
+            for (uint32_t L = 0; L < 64; L++)
+                if (m >> L & 1) { fr[L]++; if (L + 1 > nlev) nlev = L + 1; }
+            lvmask[v] = 0;
+        }
+        S->e_phys[grp] = ep; S->levels[grp] = nlev;
+    }
+    pthread_mutex_lock(&J->mu);
+    S->e_logical += el_sum;
+    pthread_mutex_unlock(&J->mu);
+    free(lvmask); free(touched);
+    scratch_free(&w);
+    return NULL;
+}
+
+void or_store_free(or_store* S) {
+    if (!S) return;
+    for (uint64_t i = 0; i < S->count; i++) { free(S->list[i]); free(S->bits[i]); }
+    free(S->list); free(S->bits); free(S->size); free(S->digest);
+    free(S->e_phys); free(S->levels); free(S->frontier); free(S);
+}
+
+/* samples [s0, s0 + count), groups of `colors`; list_max = 0 selects n/32 */
+or_store* or_store_build(const or_graph* g, uint64_t seed, uint64_t s0, uint64_t count, uint32_t colors,
+                         int nthreads, uint32_t list_max) {
+    if (colors == 0 || g->model != 0) return NULL;
+    or_store* S = (or_store*)calloc(1, sizeof(or_store));
+    S->n = g->n; S->colors = colors; S->s0 = s0; S->count = count;
+    S->ngroups = (count + colors - 1) / colors;
+    S->list_max = list_max ? list_max : g->n / 32;
+    S->size = (uint32_t*)calloc(count ? count : 1, sizeof(uint32_t));
+    S->digest = (uint64_t*)calloc(count ? count : 1, sizeof(uint64_t));
+    S->list = (uint32_t**)calloc(count ? count : 1, sizeof(uint32_t*));
+    S->bits = (uint64_t**)calloc(count ? count : 1, sizeof(uint64_t*));
+    S->e_phys = (uint64_t*)calloc(S->ngroups ? S->ngroups : 1, sizeof(uint64_t));
+    S->levels = (uint32_t*)calloc(S->ngroups ? S->ngroups : 1, sizeof(uint32_t));
+    S->frontier = (uint64_t*)calloc((S->ngroups ? S->ngroups : 1) * 64, sizeof(uint64_t));
+    store_job J;
+    J.g = g; J.k = keys_of(seed); J.S = S;
+    atomic_init(&J.next, 0); atomic_init(&J.fail, 0);
+    pthread_mutex_init(&J.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, store_worker, &J);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    free(th);
+    pthread_mutex_destroy(&J.mu);
+    if (atomic_load(&J.fail)) { or_store_free(S); return NULL; }
+    return S;
+}
+
+void or_store_info(const or_store* S, uint32_t* sizes, uint64_t* digests, uint64_t* e_phys, uint32_t* levels,
+                   uint64_t* frontier, uint64_t* e_logical) {
+    if (sizes) memcpy(sizes, S->size, S->count * sizeof(uint32_t));
+    if (digests) memcpy(digests, S->digest, S->count * sizeof(uint64_t));
+    if (e_phys) memcpy(e_phys, S->e_phys, S->ngroups * sizeof(uint64_t));
+    if (levels) memcpy(levels, S->levels, S->ngroups * sizeof(uint32_t));
+    if (frontier) memcpy(frontier, S->frontier, S->ngroups * 64 * sizeof(uint64_t));
+    if (e_logical) *e_logical = S->e_logical;
+}
+
+/* members of sample s0 + i, ascending; returns the size */
+uint32_t or_store_members(const or_store* S, uint64_t i, uint32_t* out) {
+    if (S->list[i]) { memcpy(out, S->list[i], (size_t)S->size[i] * sizeof(uint32_t)); return S->size[i]; }
+    uint32_t c = 0;
+    for (uint32_t wd = 0; wd < (S->n + 63) / 64; wd++)
+        for (uint64_t m = S->bits[i][wd]; m; m &= m - 1) out[c++] = wd * 64 + (uint32_t)__builtin_ctzll(m);
+    return c;
+}
+
+static int store_contains(const or_store* S, uint64_t i, uint32_t v) {
+    if (S->bits[i]) return (int)(S->bits[i][v >> 6] >> (v & 63) & 1);
+    uint32_t lo = 0, hi = S->size[i];
+    const uint32_t* l = S->list[i];
+    while (lo < hi) { uint32_t mid = (lo + hi) / 2; if (l[mid] < v) lo = mid + 1; else hi = mid; }
+    return lo < S->size[i] && l[lo] == v;
+}
+
+static void store_leave(const or_store* S, uint64_t i, uint64_t* cnt) {
+    if (S->list[i]) { for (uint32_t j = 0; j < S->size[i]; j++) cnt[S->list[i][j]]--; return; }
+    for (uint32_t wd = 0; wd < (S->n + 63) / 64; wd++)
+        for (uint64_t m = S->bits[i][wd]; m; m &= m - 1) cnt[wd * 64 + (uint32_t)__builtin_ctzll(m)]--;
+}
+
+int or_store_greedy(const or_store* S, uint32_t k, uint32_t* seeds, uint64_t* gains) {
+    if (k == 0 || k > S->n) return -1;
+    uint64_t* cnt = (uint64_t*)calloc(S->n, sizeof(uint64_t));
+    uint8_t* covered = (uint8_t*)calloc(S->count ? S->count : 1, 1);
+    uint8_t* selected = (uint8_t*)calloc(S->n, 1);
+    for (uint64_t i = 0; i < S->count; i++) {   /* occurrence counts: gain of every vertex */
+        if (S->list[i]) { for (uint32_t j = 0; j < S->size[i]; j++) cnt[S->list[i][j]]++; continue; }
+        for (uint32_t wd = 0; wd < (S->n + 63) / 64; wd++)
+            for (uint64_t m = S->bits[i][wd]; m; m &= m - 1) cnt[wd * 64 + (uint32_t)__builtin_ctzll(m)]++;
+    }
+    for (uint32_t r = 0; r < k; r++) {
+        int64_t best = -1; uint64_t bg = 0;
+        for (uint32_t v = 0; v < S->n; v++) {
+            if (selected[v]) continue;
+            if (best < 0 || cnt[v] > bg) { best = v; bg = cnt[v]; }   /* strict: smallest id wins ties */
+        }
+        uint32_t b = (uint32_t)best;
+        selected[b] = 1; seeds[r] = b; gains[r] = bg;
+        for (uint64_t i = 0; i < S->count; i++) {
+            if (covered[i] || !store_contains(S, i, b)) continue;
+            covered[i] = 1;
+            store_leave(S, i, cnt);
+        }
+    }
+    free(cnt); free(covered); free(selected);
+    return 0;
+}

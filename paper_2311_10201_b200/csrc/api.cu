@@ -170,13 +170,16 @@ int num_sms() {
 }
 
 // launchers defined in other translation units
-uint32_t expand_unit(int model);
+uint32_t expand_unit(int model, bool bitmap);
 void launch_compact(const BatchArgs& a, int level, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st);
 void launch_expand(const BatchArgs& a, int level, const uint32_t* tstart, cudaStream_t st);
 void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
                    cudaStream_t st);
 void compute_digests(const Samples& S, cudaStream_t st);
 void comm_unique_id(void* out);
+#ifdef BPT_HIST
+void dump_hist();
+#endif
 void selftest_philox(const uint32_t* d_in, uint32_t* d_out, uint64_t count, cudaStream_t st);
 double bench_philox(uint64_t iters, uint64_t* calls_out, cudaStream_t st);
 void comm_init(Comm* c, const void* uid);
@@ -462,7 +465,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     const bool bitmap = S.model == BPT_IC && C == 64 && !wide && !(opt.flags & BPT_FLAG_QUEUE);
     if (wide) want = kWide;
     uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
-    const uint32_t tile = wide ? kUnitWide : expand_unit(S.model);
+    const uint32_t tile = wide ? kUnitWide : expand_unit(S.model, bitmap);
     const uint64_t tiles = (n + 1023) / 1024;  // bitmap: 1,024-vertex tiles per slot
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
         raw_cap = umin64(wide ? n : sl * slices * n, (1ull << 28) - 1);  // wide: one entry per vertex
@@ -659,6 +662,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         g_graph_kernels += cf.kernels_run;
     }
     I.kernel_launches = g_launches - launches0 + (profile ? 0 : cf.kernels_run);
+#ifdef BPT_HIST
+    dump_hist();
+#endif
     I.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     if (getenv("BPT_TRACE")) {
         auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };

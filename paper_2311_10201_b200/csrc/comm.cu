@@ -1,7 +1,8 @@
 // comm.cu -- NCCL plumbing for multi-GPU seed selection: one process per GPU,
 // a 128-byte ncclUniqueId bootstrapped by the caller (e.g. torch.distributed). Sampling
-// itself never communicates; selection issues one ReduceScatter(count, sum) and one
-// 8-byte AllReduce(max) per greedy round, enqueued on the caller's stream.
+// itself never communicates. Selection over dense stores issues one ReduceScatter(count, sum)
+// and one 8-byte AllReduce(max) per greedy round; over member-list stores it gathers all
+// lists once (AllGather) and needs no collective per round. Enqueued on the caller's stream.
 #include <nccl.h>
 
 #include "internal.cuh"
@@ -41,6 +42,18 @@ void comm_reduce_scatter_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint
 
 void comm_broadcast(Comm* c, const void* send, void* recv, uint64_t bytes, int root, cudaStream_t st) {
     check_nccl(ncclBroadcast(send, recv, bytes, ncclUint8, root, (ncclComm_t)c->nccl, st), "ncclBroadcast");
+}
+
+void comm_allreduce_sum_u32(Comm* c, uint32_t* buf, uint64_t count, cudaStream_t st) {
+    check_nccl(ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, (ncclComm_t)c->nccl, st), "ncclAllReduce");
+}
+
+void comm_allgather_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint64_t count, cudaStream_t st) {
+    check_nccl(ncclAllGather(send, recv, count, ncclUint32, (ncclComm_t)c->nccl, st), "ncclAllGather");
+}
+
+void comm_allgather_u64(Comm* c, const uint64_t* send, uint64_t* recv, uint64_t count, cudaStream_t st) {
+    check_nccl(ncclAllGather(send, recv, count, ncclUint64, (ncclComm_t)c->nccl, st), "ncclAllGather");
 }
 
 void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st) {

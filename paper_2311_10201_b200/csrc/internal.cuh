@@ -142,6 +142,10 @@ struct Samples {
     // lists (list_off, list_mem); the selection uses a vertex -> samples index built on demand
     bool sparse = false;
     DevBuf inv_off, inv_s;
+    // multi-rank sparse selection: every rank's lists gathered once (offsets over all ranks'
+    // samples, padded members, global occurrence counts)
+    DevBuf g_off, g_mem, g_count0;
+    uint64_t g_n = 0;
 };
 
 // ------------------------------------------------------------------ launchers

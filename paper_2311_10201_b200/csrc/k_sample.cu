@@ -466,6 +466,9 @@ __device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphCondi
 #ifndef BPT_WIN_IC
 #define BPT_WIN_IC 3
 #endif
+#ifdef BPT_HIST
+__device__ unsigned long long g_hist[16 * 80];
+#endif
 constexpr int kWinIC = BPT_WIN_IC;       // 32-lane windows per warp work unit
 static_assert(kWinIC >= 1 && kWinIC <= 4, "the window search packs <= 3 window prefixes into 8-bit fields");
 constexpr int kUnitIC = 32 * kWinIC;
@@ -566,6 +569,20 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     uint32_t c[kWinIC], tot = 0;
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) { c[w] = __popcll(live[w]); tot += c[w]; }
+#ifdef BPT_HIST
+    {  // diagnostic build only: live-colour histogram per level, and per unit the lane totals' sum / max
+        const uint32_t lvl = min(a.ctl->level, 15u);
+        for (int w = 0; w < kWinIC; ++w)
+            if (c[w]) atomicAdd(&g_hist[lvl * 80 + c[w]], 1ull);
+        const uint32_t mx = __reduce_max_sync(kFull, tot), sm = __reduce_add_sync(kFull, tot);
+        if (lane == 0) {
+            atomicAdd(&g_hist[lvl * 80 + 65], (unsigned long long)sm);
+            atomicAdd(&g_hist[lvl * 80 + 66], (unsigned long long)mx);
+            atomicAdd(&g_hist[lvl * 80 + 67], 1ull);
+            atomicAdd(&g_hist[lvl * 80 + 68], (unsigned long long)((sm + 31) / 32));
+        }
+    }
+#endif
     const uint32_t incl = warp_incl_scan_u32(tot, lane);
     const uint32_t ntask = __shfl_sync(kFull, incl, 31);
     uint64_t pass[kWinIC];
@@ -746,38 +763,40 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchAr
     expand_ic_body<kC64, kBm, false>(a, tstart, h_level, use_cond);
 }
 
-// ------------------------------------------------------------------------ IC expansion, task lists
-// The product's IC expansion (64 colours, touched-bitmap frontier). Same units, entry lookup and
-// loads as expand_unit_ic; the coins differ in how the live (edge, colour) pairs reach the lanes:
-// every lane writes its own pairs, lowest colour first, as 16-bit task words (item << 6 | colour)
-// into a per-warp list at its exclusive prefix, and the warp then evaluates the list 32 tasks at
-// a time -- one shared-memory read decodes a task (no owner search, no rank select). A lane's
-// write loop runs once per live colour of its items (0 for most edges; ~1.4 for a live edge at
-// the heavy levels). Passing colours are OR-merged per item in shared memory, then into N[u]
-// with one fire-and-forget OR per item (Listing 1 line 14), and u is marked in the touched
-// bitmap when its N was empty at the gather (see expand_unit_ic).
-constexpr uint32_t kTaskCap = 256;  // task words per warp per pass (a unit with more runs several passes)
-
-struct TaskScratch {
-    uint2 et[kUnitIC];                     // per item: {edge id, threshold}
-    uint32_t sb[kUnitIC];                  // per item: global id of colour 0 of its block
-    uint32_t pass[kUnitIC][2];             // per item: passing colours (ATOMS.OR on 32-bit halves)
-    unsigned short task[kTaskCap];         // item << 6 | colour
+// ------------------------------------------------------------------------ IC expansion (product)
+// The product's IC expansion (64 colours, touched-bitmap frontier), Listing 1 lines 9-15
+// (P:168-174). Work units of kUnitIC = 32 * kWinIC consecutive reverse-edge reads (items) per
+// warp, kWinIC windows of 32 lanes; the entry of every item from the unit's first entry (tstart)
+// and a popcount of the entry-start bitmap; the windows' loads (entry, {src, thr} record,
+// {V, N}[u]) issued together; live = mask & ~(V | N) (N: colours another edge already merged into
+// u this level -- a stale N only skips fewer coins). Measured at the heavy levels (C2): 11% of
+// items carry a live colour, ~7 on average, so the live (item, colour) pairs are flattened into
+// one task list per unit and evaluated 32 at a time: the owner lane by a 5-step search of the
+// lanes' exclusive task prefix, the window by the owner's packed window prefix, the colour by a
+// rank select in the owner's live mask; one 16-byte shared load brings {edge id, thr, live}.
+// Passing colours are OR-merged per item in shared memory, then into N[u] by one fire-and-forget
+// OR per item; u is marked in the touched bitmap when its N was empty at the gather (the first OR
+// of a level into N[u] comes from such an item, so every vertex with a non-empty N is marked).
+struct BmScratch {
+    uint4 item[kWinIC][32];                 // live items: {edge id, thr, live lo, live hi}
+    unsigned long long pass[kWinIC][32];    // live items: passing colours (ATOMS.OR on 32-bit halves)
+    uint32_t sb[kWinIC][32];                // live items: global id of colour 0 of the item's block
+    uint32_t excl[32];                      // exclusive prefix of the lanes' task counts
+    uint32_t cum[32];                       // per-lane window prefix: c0 | (c0+c1) << 8 | (c0+c1+c2) << 16
 };
 
 template <bool kWhole>
-__device__ __forceinline__ void expand_unit_tasks(const BatchArgs& a, TaskScratch& W, int lane, uint32_t le_mask,
-                                                  uint32_t unit, uint32_t rem, uint32_t jc0, uint64_t gblk0,
-                                                  unsigned long long& coins, unsigned long long& atoms,
-                                                  bool& any_pass) {
+__device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, int lane, uint32_t le_mask,
+                                               uint32_t unit, uint32_t rem, uint32_t jc0, uint64_t gblk0,
+                                               unsigned long long& coins, unsigned long long& atoms,
+                                               bool& any_pass) {
     const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
-    // ---- entry of every item (jc0 holds item 0; the compaction marked every entry start)
     uint32_t mw[kWinIC];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) mw[w] = a.umask[(size_t)unit * kWinIC + w];
+    for (int w = 0; w < kWinIC; ++w) mw[w] = __ldg(&a.umask[(size_t)unit * kWinIC + w]);
     __syncwarp();
     if (lane < kWinIC) a.umask[(size_t)unit * kWinIC + lane] = 0;
-    mw[0] &= ~1u;
+    mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
     uint32_t jl[kWinIC];
     uint32_t before = jc0;
 #pragma unroll
@@ -785,86 +804,90 @@ __device__ __forceinline__ void expand_unit_tasks(const BatchArgs& a, TaskScratc
         jl[w] = before + __popc(mw[w] & le_mask);
         before += __popc(mw[w]);
     }
-    // ---- loads of the windows issued together
     uint4 ent[kWinIC];
     uint2 rc[kWinIC];
-    uint32_t vidx[kWinIC];  // working-mask index slot * n + u of the item's source vertex
-    uint32_t tword[kWinIC]; // its touched-bitmap word, ~0 if N[u] was not empty at the gather
-    uint32_t tbits = 0;     // 5-bit positions of u in those words
-    uint64_t left[kWinIC];  // live colours whose coins are not evaluated yet
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) ent[w] = a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0];
+    for (int w = 0; w < kWinIC; ++w) ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
         const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
         rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
     }
+    uint32_t vidx[kWinIC], tword[kWinIC], tbits = 0, c[kWinIC], tot = 0;
+    uint64_t live[kWinIC];
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
         vidx[w] = ent[w].y * a.n + rc[w].x;
         const ulonglong2 vn = ld_keep(&a.VN[vidx[w]]);
-        left[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
+        live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
+        if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
         tword[w] = vn.y == 0 ? ent[w].y * a.tiles * 32 + (rc[w].x >> 5) : ~0u;
         tbits |= (rc[w].x & 31u) << (5 * w);
-        if (!kWhole && 32u * w + lane >= rem) left[w] = 0;
+        c[w] = __popcll(live[w]);
+        tot += c[w];
     }
-    uint32_t tot = 0;
+    const uint32_t incl = warp_incl_scan_u32(tot, lane);
+    const uint32_t ntask = __shfl_sync(kFull, incl, 31);
+    if (ntask == 0) return;
+    uint32_t cm = 0, run = 0;
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) tot += __popcll(left[w]);
-    if (!__any_sync(kFull, tot != 0)) return;
-    // ---- coin tasks: per-item data, then the lanes' task words, evaluated 32 at a time
+    for (int w = 0; w < 3; ++w) {
+        if (w < kWinIC - 1) run += c[w];
+        cm |= (w < kWinIC - 1 ? run : 0xffu) << (8 * w);
+    }
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) {
-        const uint32_t it = 32u * w + lane;
-        W.et[it] = make_uint2(t0l + it + ent[w].x, rc[w].y);
-        W.sb[it] = (uint32_t)(64ull * (gblk0 + ent[w].y));
-        W.pass[it][0] = 0;
-        W.pass[it][1] = 0;
+        if (live[w]) {
+            W.item[w][lane] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, (uint32_t)live[w],
+                                         (uint32_t)(live[w] >> 32));
+            W.sb[w][lane] = (uint32_t)(64ull * (gblk0 + ent[w].y));
+            W.pass[w][lane] = 0;
+        }
     }
-    while (true) {  // one pass per kTaskCap tasks (one pass for nearly every unit)
-        const uint32_t incl = warp_incl_scan_u32(tot, lane);
-        const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-        uint32_t pos = incl - tot;
+    W.excl[lane] = incl - tot;
+    W.cum[lane] = cm;
+    __syncwarp();
+    for (uint32_t b = 0; b < ntask; b += 32) {
+        const uint32_t k = b + lane;
+        if (k < ntask) {
+            uint32_t o = 0;  // owner lane = largest lane with excl <= k
 #pragma unroll
-        for (int w = 0; w < kWinIC; ++w) {
-            while (left[w] && pos < kTaskCap) {
-                const uint32_t b = __ffsll((long long)left[w]) - 1;
-                W.task[pos++] = (unsigned short)(((32u * w + lane) << 6) | b);
-                left[w] &= left[w] - 1;
+            for (int step = 16; step > 0; step >>= 1)
+                if (W.excl[o + step] <= k) o += step;
+            uint32_t r = k - W.excl[o];
+            const uint32_t cmo = W.cum[o];
+            uint32_t w = 0, base = 0;  // window of the task: last window whose prefix <= r
+#pragma unroll
+            for (int q = 0; q < kWinIC - 1; ++q) {
+                const uint32_t pq = (cmo >> (8 * q)) & 0xffu;
+                if (r >= pq) { w = q + 1; base = pq; }
+            }
+            const uint4 it = W.item[w][o];
+            const uint32_t bit = nth_set_bit64(((uint64_t)it.w << 32) | it.z, r - base);
+            const uint32_t x = philox2x32_10(it.x, W.sb[w][o] + bit, a.k_ic).x;
+            if ((x >> 1) < it.y)
+                atomicOr(reinterpret_cast<uint32_t*>(&W.pass[w][o]) + (bit >> 5), 1u << (bit & 31));
+        }
+    }
+    if (lane == 0) coins += ntask;
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < kWinIC; ++w) {
+        if (live[w]) {
+            const unsigned long long pass = W.pass[w][lane];
+            if (pass) {
+                ++atoms;
+                atomicOr(&a.VN[vidx[w]].y, pass);
+                if (tword[w] != ~0u) atomicOr(&a.touched[tword[w]], 1u << ((tbits >> (5 * w)) & 31u));
+                any_pass = true;
             }
         }
-        __syncwarp();
-        const uint32_t nt = min(ntask, kTaskCap);
-        for (uint32_t k = lane; k < nt; k += 32) {
-            const uint32_t t = W.task[k];
-            const uint32_t it = t >> 6, b = t & 63u;
-            const uint2 x = W.et[it];
-            const uint32_t r = philox2x32_10(x.x, W.sb[it] + b, a.k_ic).x;
-            if ((r >> 1) < x.y) atomicOr(&W.pass[it][b >> 5], 1u << (b & 31));
-        }
-        if (lane == 0) coins += nt;
-        __syncwarp();
-        if (ntask <= kTaskCap) break;
-        tot = 0;
-#pragma unroll
-        for (int w = 0; w < kWinIC; ++w) tot += __popcll(left[w]);
     }
-    // ---- merges: fire-and-forget ORs into N[u]; u marked in the touched bitmap when its N was empty
-#pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
-        const uint32_t it = 32u * w + lane;
-        const uint64_t pass = ((uint64_t)W.pass[it][1] << 32) | W.pass[it][0];
-        if (pass) {
-            ++atoms;
-            atomicOr(&a.VN[vidx[w]].y, pass);
-            if (tword[w] != ~0u) atomicOr(&a.touched[tword[w]], 1u << ((tbits >> (5 * w)) & 31u));
-            any_pass = true;
-        }
-    }
+    __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_tasks(BatchArgs a, const uint32_t* __restrict__ tstart,
-                                                                 cudaGraphConditionalHandle h_level, int use_cond) {
+__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_bm(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                              cudaGraphConditionalHandle h_level, int use_cond) {
     count_self(a.ctl);
     if (!a.ctl->cont) return;
     Ctl* ctl = a.ctl;
@@ -885,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_tasks(Batc
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TaskScratch& W = reinterpret_cast<TaskScratch*>(smem_raw)[threadIdx.x >> 5];
+    BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
     __shared__ unsigned long long red[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
@@ -895,12 +918,159 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_tasks(Batc
     unsigned long long coins = 0, atoms = 0;
     bool any_pass = false;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
-        const uint32_t jc0 = tstart[unit];
+        const uint32_t jc0 = __ldg(&tstart[unit]);
         if (unit < nfull)
-            expand_unit_tasks<true>(a, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
+            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
         else
-            expand_unit_tasks<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC), jc0, gblk0,
-                                     coins, atoms, any_pass);
+            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC), jc0, gblk0,
+                                  coins, atoms, any_pass);
+    }
+    if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
+    unsigned long long ct = block_sum_ull(coins, red);
+    if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
+    unsigned long long at = block_sum_ull(atoms, red);
+    if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
+    finish_expand(a, h_level, use_cond, active);
+}
+
+// ------------------------------------------------------------------------ IC expansion, lane chunks
+// The product's IC expansion (64 colours, touched-bitmap frontier): Listing 1 lines 9-15
+// with each lane owning kLcK CONSECUTIVE work items (reverse-edge reads) of a
+// 32 * kLcK-item warp unit, so the per-item work is a handful of instructions:
+//   * entry lookup once per lane (tstart + a popcount of the unit's entry-start bits), a new
+//     entry record only where one starts inside the lane's chunk (entries average ~30-40 items at
+//     the heavy levels);
+//   * per item: the {src, thr} record, the {V, N}[u] gather (kLcP items per phase in flight per
+//     lane), live = mask & ~(V | N);
+//   * coins lane-locally: every live colour c of the item draws coin(s_c, e) (readings C-1/C-2);
+//     lanes of one entry see similar live counts, so the warp's loop runs ~the lanes' common count;
+//   * merges with one fire-and-forget OR into N[u] per passing item; u is marked in the touched
+//     bitmap when its N was empty at the gather (the first OR of a level into N[u] comes from such
+//     an item, so every vertex with a non-empty N is marked).
+// No shared memory: the whole L1 caches the hub vertices' {V, N} sectors and the records.
+#ifndef BPT_LC_K
+#define BPT_LC_K 8
+#endif
+constexpr int kLcK = BPT_LC_K;      // items per lane
+#ifndef BPT_LC_P
+#define BPT_LC_P 4
+#endif
+constexpr int kLcP = BPT_LC_P;      // items per phase (loads in flight per lane)
+constexpr int kLcUnit = 32 * kLcK;  // items per warp unit
+#ifdef BPT_EXPAND_LC
+constexpr bool kBmLc = true;        // bitmap mode expands with k_expand_lc (experiment)
+#else
+constexpr bool kBmLc = false;       // bitmap mode expands with k_expand_ic<true, true>
+#endif
+static_assert(kLcK % kLcP == 0 && kLcK <= 8, "a lane's entry-start bits are one byte");
+
+__device__ __forceinline__ uint2 ld_rec_l1(const uint2* p) {  // L1-allocating (the lanes' chunks share lines)
+    uint2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_first()));
+    return r;
+}
+
+template <bool kWhole>
+__device__ __forceinline__ void expand_unit_lc(const BatchArgs& a, int lane, uint32_t unit, uint32_t rem, uint32_t jc0,
+                                               uint64_t gblk0, unsigned long long& coins, unsigned long long& atoms,
+                                               bool& any_pass) {
+    constexpr uint32_t kWords = kLcUnit / 32;
+    const uint32_t t0 = unit * (uint32_t)kLcUnit;  // mod 2^32: edge ids are t + delta (mod 2^32)
+    const uint32_t p0 = (uint32_t)kLcK * lane;     // the lane's first item in the unit
+    // ---- entry-start bits of the lane's items (item 0 of the unit is in jc0)
+    const uint32_t wv = __ldg(&a.umask[(size_t)unit * kWords + (p0 >> 5)]);
+    __syncwarp();
+    if (lane < (int)kWords) a.umask[(size_t)unit * kWords + lane] = 0;  // cleared for the next level
+    uint32_t bits = (wv >> (p0 & 31)) & ((1u << kLcK) - 1u);
+    if (lane == 0) bits &= ~1u;
+    const uint32_t cnt = __popc(bits);
+    const uint32_t j0 = jc0 + warp_incl_scan_u32(cnt, lane) - cnt;  // entry of the item before the chunk
+#pragma unroll
+    for (int ph = 0; ph < kLcK / kLcP; ++ph) {
+        uint32_t e[kLcP], thr[kLcP], sb[kLcP], vidx[kLcP], tword[kLcP], tbits = 0;
+        uint64_t live[kLcP];
+        uint2 rc[kLcP];
+        uint4 ent = __ldg(&a.q[j0 + __popc(bits & ((2u << (kLcP * ph)) - 1u))]);
+#pragma unroll
+        for (int ii = 0; ii < kLcP; ++ii) {
+            const int i = kLcP * ph + ii;
+            if (ii > 0 && ((bits >> i) & 1u)) ent = __ldg(&a.q[j0 + __popc(bits & ((2u << i) - 1u))]);
+            const bool ok = kWhole || p0 + i < rem;
+            e[ii] = t0 + p0 + i + ent.x;
+            rc[ii] = ld_rec_l1(&a.rec[ok ? e[ii] : 0u]);  // items past the level's end: masked below
+            vidx[ii] = ent.y * a.n;
+            sb[ii] = (uint32_t)(64ull * (gblk0 + ent.y));
+            live[ii] = ok ? (((uint64_t)ent.w << 32) | ent.z) : 0ull;
+            tword[ii] = ent.y * a.tiles * 32;
+        }
+#pragma unroll
+        for (int ii = 0; ii < kLcP; ++ii) {
+            vidx[ii] += rc[ii].x;
+            thr[ii] = rc[ii].y;
+            const ulonglong2 vn = ld_keep(&a.VN[vidx[ii]]);
+            live[ii] &= ~(vn.x | vn.y);
+            tword[ii] = vn.y == 0 ? tword[ii] + (rc[ii].x >> 5) : ~0u;
+            tbits |= (rc[ii].x & 31u) << (5 * ii);
+        }
+#pragma unroll
+        for (int ii = 0; ii < kLcP; ++ii) {
+            uint64_t m = live[ii], pass = 0;
+            coins += __popcll(m);
+            while (m) {
+                const uint32_t c = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const uint32_t x = philox2x32_10(e[ii], sb[ii] + c, a.k_ic).x;
+                if ((x >> 1) < thr[ii]) pass |= 1ull << c;
+            }
+            if (pass) {
+                ++atoms;
+                atomicOr(&a.VN[vidx[ii]].y, pass);
+                if (tword[ii] != ~0u) atomicOr(&a.touched[tword[ii]], 1u << ((tbits >> (5 * ii)) & 31u));
+                any_pass = true;
+            }
+        }
+    }
+}
+
+#ifndef BPT_LC_MINB
+#define BPT_LC_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, BPT_LC_MINB) k_expand_lc(BatchArgs a, const uint32_t* __restrict__ tstart,
+                                                              cudaGraphConditionalHandle h_level, int use_cond) {
+    count_self(a.ctl);
+    if (!a.ctl->cont) return;
+    Ctl* ctl = a.ctl;
+    const uint32_t level = ctl->level;
+    const uint64_t gblk0 = ctl->gblk0;
+    const LevelRec* L = &a.lv[level];
+    LevelRec* Ln = &a.lv[level + 1];
+    const unsigned long long packed = L->packed;
+    const uint64_t nq = packed >> kPackShift;
+    const uint64_t total = packed & kEdgeMask;
+    const bool idle = nq == 0 || L->overflow;
+    const uint32_t active =
+        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kLcUnit * kWarps - 1) / ((uint64_t)kLcUnit * kWarps)));
+    if (blockIdx.x >= active) return;
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    if (idle) {
+        finish_expand(a, h_level, use_cond, active);
+        return;
+    }
+    __shared__ unsigned long long red[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t nunits = (uint32_t)((total + kLcUnit - 1) / kLcUnit);
+    const uint32_t nfull = (uint32_t)(total / kLcUnit);
+    const uint32_t nwarps = active * kWarps;
+    unsigned long long coins = 0, atoms = 0;
+    bool any_pass = false;
+    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
+        const uint32_t jc0 = __ldg(&tstart[unit]);
+        if (unit < nfull)
+            expand_unit_lc<true>(a, lane, unit, kLcUnit, jc0, gblk0, coins, atoms, any_pass);
+        else
+            expand_unit_lc<false>(a, lane, unit, (uint32_t)(total - (uint64_t)unit * kLcUnit), jc0, gblk0, coins, atoms,
+                                  any_pass);
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
     unsigned long long ct = block_sum_ull(coins, red);
@@ -1808,6 +1978,7 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 int g_expand_grid = 0;
 int g_expand_grid_w = 0;
 int g_expand_grid_t = 0;
+int g_expand_grid_b = 0;
 int g_expand_grid_lt = 0;
 int g_levels_per_sm_lt = 0;  // co-resident blocks per SM of the cooperative LT loop
 int g_compact_grid = 0;
@@ -1860,7 +2031,9 @@ void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, ui
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_lists");
 }
 
-uint32_t expand_unit(int model) { return model == BPT_IC ? (uint32_t)kUnitIC : kTile; }
+uint32_t expand_unit(int model, bool bitmap) {
+    return model == BPT_IC ? (bitmap && kBmLc ? (uint32_t)kLcUnit : (uint32_t)kUnitIC) : kTile;
+}
 
 int expand_grid() {
     if (!g_expand_grid) {
@@ -1872,11 +2045,13 @@ int expand_grid() {
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true, true>, kThreads,
                                                                sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
-        BPT_CUDA(cudaFuncSetAttribute(k_expand_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(TaskScratch) * kWarps)));
-        int per_sm_t = 0;
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_expand_tasks, kThreads,
-                                                               sizeof(TaskScratch) * kWarps));
+        int per_sm_t = 0, per_sm_b = 0;
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_expand_lc, kThreads, 0));
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_bm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(BmScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_expand_bm, kThreads,
+                                                               sizeof(BmScratch) * kWarps));
+        g_expand_grid_b = num_sms() * (per_sm_b > 0 ? per_sm_b : 1);
         g_expand_grid_t = num_sms() * (per_sm_t > 0 ? per_sm_t : 1);
         int per_sm_w = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1933,10 +2108,11 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
         ::bpt::check_cuda(cudaGetLastError(), "launch wide level kernels");
         return;
     }
-    k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model));
+    k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model, a.touched != nullptr));
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
     if (a.model == BPT_IC && a.touched)
-        k_expand_tasks<<<g_expand_grid_t, kThreads, sizeof(TaskScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        kBmLc ? k_expand_lc<<<g_expand_grid_t, kThreads, 0, st>>>(a, tstart, h0, 0)
+              : k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC && a.colors == 64)
         k_expand_ic<true, false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
@@ -2022,7 +2198,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     cudaGraphNode_t n_level;
     BPT_CUDA(cudaGraphAddNode(&n_level, body, &n_init, 1, &cl));
     cudaGraph_t lbody = cl.conditional.phGraph_out[0];
-    uint32_t unit = expand_unit(a.model);
+    uint32_t unit = expand_unit(a.model, a.touched != nullptr);
     void* cmp_args[] = {&args, &tstart, &tstart_cap, &unit};
     void* cmpw_args[] = {&args, &tstart, &tstart_cap};
     cudaGraphNode_t n_cmp = a.wide
@@ -2033,8 +2209,9 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),
                      sizeof(WarpScratchW) * kWarps, exp_args)
         : a.model == BPT_IC && a.touched
-        ? add_kernel(lbody, &n_cmp, (void*)k_expand_tasks, dim3(g_expand_grid_t), dim3(kThreads),
-                     sizeof(TaskScratch) * kWarps, exp_args)
+        ? (kBmLc ? add_kernel(lbody, &n_cmp, (void*)k_expand_lc, dim3(g_expand_grid_t), dim3(kThreads), 0, exp_args)
+                 : add_kernel(lbody, &n_cmp, (void*)k_expand_bm, dim3(g_expand_grid_b), dim3(kThreads),
+                              sizeof(BmScratch) * kWarps, exp_args))
         : a.model == BPT_IC
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true, false> : (void*)k_expand_ic<false, false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
@@ -2053,3 +2230,17 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
 }
 
 }  // namespace bpt
+
+#ifdef BPT_HIST
+namespace bpt {
+void dump_hist() {  // diagnostic build only
+    unsigned long long h[16 * 80];
+    cudaMemcpyFromSymbol(h, g_hist, sizeof(h));
+    fprintf(stderr, "{\"hist\": [");
+    for (int i = 0; i < 16 * 80; ++i) fprintf(stderr, "%s%llu", i ? "," : "", h[i]);
+    fprintf(stderr, "]}\n");
+    unsigned long long z[16 * 80] = {};
+    cudaMemcpyToSymbol(g_hist, z, sizeof(z));
+}
+}  // namespace bpt
+#endif

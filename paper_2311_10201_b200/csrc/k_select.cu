@@ -9,6 +9,9 @@
 //           (3) count[v] -= sum over listed g of popcount(V_g[v] & new_g)
 // Each sample leaves `count` exactly once, so the decrements over all rounds cost at most one
 // pass over the store plus the few blocks touched by later rounds.
+// Member-list stores (LT): the same greedy through a vertex -> samples index; with W > 1 ranks
+// every rank gathers all ranks' lists once (AllGather) and runs the rounds
+// locally, so the k rounds need no collective at all.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -21,6 +24,9 @@ size_t scan_temp_bytes(uint64_t count);
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp, cudaStream_t st);
 void comm_reduce_scatter_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint64_t recv_count, cudaStream_t st);
 void comm_allreduce_max_u64(Comm* c, unsigned long long* buf, uint64_t count, cudaStream_t st);
+void comm_allreduce_sum_u32(Comm* c, uint32_t* buf, uint64_t count, cudaStream_t st);
+void comm_allgather_u32(Comm* c, const uint32_t* send, uint32_t* recv, uint64_t count, cudaStream_t st);
+void comm_allgather_u64(Comm* c, const uint64_t* send, uint64_t* recv, uint64_t count, cudaStream_t st);
 
 namespace {
 
@@ -206,6 +212,93 @@ static bool build_lists(const Samples& S, cudaStream_t st) {
     return M.lists_ok = true;
 }
 
+// Sparse stores (member lists, e.g. LT): the selection index over a list collection -- the
+// vertex -> samples inverted index and, per round, the samples containing v* leave the counts of
+// all their members (each sample leaves once: total work = one pass over the lists).
+struct ListIndex {
+    const uint64_t* off = nullptr;   // [nlists + 1]
+    const uint32_t* mem = nullptr;
+    uint64_t nlists = 0;
+    const uint32_t* count0 = nullptr;  // occurrences over these lists, [n_pad]
+};
+
+static void build_inverted(Samples& M, const ListIndex& L, uint32_t n, cudaStream_t st) {
+    M.inv_off.alloc((uint64_t)(n + 1) * 8);
+    DevBuf wide((uint64_t)(n + 1) * 8), temp(scan_temp_bytes(n + 1));
+    BPT_CUDA(cudaMemsetAsync(wide.p, 0, wide.bytes, st));
+    k_widen_u32<<<num_sms() * 4, 256, 0, st>>>(L.count0, wide.as<uint64_t>(), n);
+    exclusive_scan_u64(wide.as<uint64_t>(), M.inv_off.as<uint64_t>(), n + 1, temp.p, st);
+    count_launch();
+    uint64_t total = 0;
+    BPT_CUDA(cudaMemcpyAsync(&total, M.inv_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    M.inv_s.alloc(total * 4 + 4);
+    DevBuf cursor((uint64_t)n * 4);
+    BPT_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes, st));
+    const unsigned g = (unsigned)umin64((L.nlists * 32 + 255) / 256, (uint64_t)num_sms() * 16);
+    if (g) k_inv_scatter<<<g, 256, 0, st>>>(L.off, L.mem, L.nlists, M.inv_off.as<uint64_t>(), cursor.as<uint32_t>(),
+                                            M.inv_s.as<uint32_t>());
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_inv_scatter");
+    BPT_CUDA(cudaStreamSynchronize(st));
+}
+
+// Multi-rank sparse store: every rank gathers all ranks' member lists once (one AllGather of the
+// list sizes and one of the members) and then runs the whole greedy
+// locally -- no collective per round; every rank computes the same seeds from the same data.
+static void gather_lists(Samples& M, cudaStream_t st) {
+    Comm* c = M.comm;
+    const int W = c->world;
+    const uint64_t nlocal = M.s1 - M.s0;
+    const uint64_t total = M.info.members;
+    DevBuf hdr(16), hdr_all((uint64_t)W * 16);
+    const uint64_t mine[2] = {nlocal, total};
+    BPT_CUDA(cudaMemcpyAsync(hdr.p, mine, 16, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(c, hdr.as<uint64_t>(), hdr_all.as<uint64_t>(), 2, st);
+    std::vector<uint64_t> h((size_t)W * 2);
+    BPT_CUDA(cudaMemcpyAsync(h.data(), hdr_all.p, (size_t)W * 16, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    uint64_t max_n = 1, max_t = 1;
+    for (int r = 0; r < W; ++r) { max_n = umax64(max_n, h[2 * r]); max_t = umax64(max_t, h[2 * r + 1]); }
+    // local sizes and members, padded to the largest rank's
+    DevBuf sz(max_n * 4), mem(max_t * 4), sz_all((uint64_t)W * max_n * 4), mem_all((uint64_t)W * max_t * 4);
+    BPT_CUDA(cudaMemsetAsync(sz.p, 0, sz.bytes, st));
+    if (nlocal) BPT_CUDA(cudaMemcpyAsync(sz.p, M.sizes.p, nlocal * 4, cudaMemcpyDeviceToDevice, st));
+    if (total) BPT_CUDA(cudaMemcpyAsync(mem.p, M.list_mem.p, total * 4, cudaMemcpyDeviceToDevice, st));
+    comm_allgather_u32(c, sz.as<uint32_t>(), sz_all.as<uint32_t>(), max_n, st);
+    comm_allgather_u32(c, mem.as<uint32_t>(), mem_all.as<uint32_t>(), max_t, st);
+    // drop the padding: rank r's members (gathered at r * max_t) move to one contiguous array
+    uint64_t tall = 0;
+    for (int r = 0; r < W; ++r) tall += h[2 * r + 1];
+    M.g_mem.alloc(tall * 4 + 4);
+    for (int r = 0; r < W; ++r) {
+        uint64_t before = 0;
+        for (int q = 0; q < r; ++q) before += h[2 * q + 1];
+        if (h[2 * r + 1])
+            BPT_CUDA(cudaMemcpyAsync(M.g_mem.as<uint32_t>() + before, mem_all.as<uint32_t>() + (uint64_t)r * max_t,
+                                     h[2 * r + 1] * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    // global list offsets over all ranks' samples, in rank order
+    std::vector<uint32_t> hs((size_t)W * max_n);
+    BPT_CUDA(cudaMemcpyAsync(hs.data(), sz_all.p, hs.size() * 4, cudaMemcpyDeviceToHost, st));
+    BPT_CUDA(cudaStreamSynchronize(st));
+    uint64_t nall = 0;
+    for (int r = 0; r < W; ++r) nall += h[2 * r];
+    std::vector<uint64_t> off(nall + 1);
+    uint64_t i = 0, o = 0;
+    for (int r = 0; r < W; ++r)
+        for (uint64_t j = 0; j < h[2 * r]; ++j) { off[i++] = o; o += hs[(size_t)r * max_n + j]; }
+    off[nall] = o;
+    M.g_off.alloc((nall + 1) * 8);
+    BPT_CUDA(cudaMemcpyAsync(M.g_off.p, off.data(), (nall + 1) * 8, cudaMemcpyHostToDevice, st));
+    M.g_n = nall;
+    // occurrences over all ranks' samples
+    M.g_count0.alloc((uint64_t)M.n_pad * 4);
+    BPT_CUDA(cudaMemcpyAsync(M.g_count0.p, M.count0.p, (uint64_t)M.n_pad * 4, cudaMemcpyDeviceToDevice, st));
+    comm_allreduce_sum_u32(c, M.g_count0.as<uint32_t>(), M.n_pad, st);
+    BPT_CUDA(cudaStreamSynchronize(st));
+}
+
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st) {
     const uint32_t n = S.n;
     Comm* comm = S.comm;
@@ -225,37 +318,23 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     const bool lists = build_lists(S, st);
-    DevBuf covered(S.sparse ? (S.s1 - S.s0) * 4 + 4 : 4);
+    // sparse stores: the lists the selection runs on (all ranks' lists, gathered once, if W > 1)
+    ListIndex L;
     if (S.sparse) {
-        BPT_CUDA(cudaMemsetAsync(covered.p, 0, covered.bytes, st));
-        if (!S.inv_off.p) {  // vertex -> samples index, built once per handle (device scan)
-            Samples& M = const_cast<Samples&>(S);
-            M.inv_off.alloc((uint64_t)(n + 1) * 8);
-            DevBuf wide((uint64_t)(n + 1) * 8), temp(scan_temp_bytes(n + 1));
-            BPT_CUDA(cudaMemsetAsync(wide.p, 0, wide.bytes, st));
-            k_widen_u32<<<num_sms() * 4, 256, 0, st>>>(S.count0.as<uint32_t>(), wide.as<uint64_t>(), n);
-            exclusive_scan_u64(wide.as<uint64_t>(), M.inv_off.as<uint64_t>(), n + 1, temp.p, st);
-            count_launch();
-            uint64_t total = 0;
-            BPT_CUDA(cudaMemcpyAsync(&total, M.inv_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
-            BPT_CUDA(cudaStreamSynchronize(st));
-            M.inv_s.alloc(total * 4 + 4);
-            DevBuf cursor((uint64_t)n * 4);
-            BPT_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes, st));
-            const uint64_t nl = S.s1 - S.s0;
-            const unsigned g = (unsigned)umin64((nl * 32 + 255) / 256, (uint64_t)num_sms() * 16);
-            if (g) k_inv_scatter<<<g, 256, 0, st>>>(S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), nl,
-                                                    M.inv_off.as<uint64_t>(), cursor.as<uint32_t>(),
-                                                    M.inv_s.as<uint32_t>());
-            count_launch();
-            ::bpt::check_cuda(cudaGetLastError(), "launch k_inv_scatter");
-            BPT_CUDA(cudaStreamSynchronize(st));
-        }
+        Samples& M = const_cast<Samples&>(S);
+        if (world > 1 && !M.g_off.p) gather_lists(M, st);
+        L = world > 1 ? ListIndex{M.g_off.as<uint64_t>(), M.g_mem.as<uint32_t>(), M.g_n, M.g_count0.as<uint32_t>()}
+                      : ListIndex{S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(), S.s1 - S.s0,
+                                  S.count0.as<uint32_t>()};
+        if (!S.inv_off.p) build_inverted(M, L, n, st);  // vertex -> samples index, once per handle
+        BPT_CUDA(cudaMemcpyAsync(count.p, L.count0, (uint64_t)S.n_pad * 4, cudaMemcpyDeviceToDevice, st));
     }
+    DevBuf covered(S.sparse ? L.nlists * 4 + 4 : 4);
+    if (S.sparse) BPT_CUDA(cudaMemsetAsync(covered.p, 0, covered.bytes, st));
     const auto t1 = clk::now();
     for (uint32_t r = 0; r < k; ++r) {
         unsigned long long* key = keys.as<unsigned long long>() + r;
-        if (world > 1) {
+        if (world > 1 && !S.sparse) {
             comm_reduce_scatter_u32(comm, count.as<uint32_t>(), shard.as<uint32_t>(), shard_len, st);
             k_argmax<<<vgrid, kSelThreads, 0, st>>>(shard.as<uint32_t>(), shard_len, (uint64_t)rank * shard_len, n,
                                                     sel.as<uint8_t>(), key, nlist.as<uint32_t>());
@@ -268,8 +347,7 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
         }
         if (S.sparse) {
             k_cover_sparse<<<num_sms() * 4, 256, 0, st>>>(key, S.inv_off.as<uint64_t>(), S.inv_s.as<uint32_t>(),
-                                                           S.list_off.as<uint64_t>(), S.list_mem.as<uint32_t>(),
-                                                           covered.as<uint32_t>(), sel.as<uint8_t>(),
+                                                           L.off, L.mem, covered.as<uint32_t>(), sel.as<uint8_t>(),
                                                            count.as<uint32_t>());
             count_launch();
             ::bpt::check_cuda(cudaGetLastError(), "launch k_cover_sparse");

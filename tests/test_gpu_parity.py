@@ -598,3 +598,27 @@ def test_shard_invariance_and_occurrences(bpt, c2_small):
             acc += s.occurrences()
         assert np.array_equal(acc, occ.astype(np.uint64))
 
+
+
+def test_empty_rank_shard_selection(bpt):
+    """A rank that owns no 64-sample block (ceil(theta/64) < W) still runs the selection: its
+    count vector is empty and it marks the chosen vertices (a zero-size grid used to
+    fail here). theta = 64 over W = 2: shard 0 owns blocks [0, 0) -- empty -- and shard 1 the
+    only block, which alone gives the oracle's seeds."""
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    ref = oracle_all(row_ptr, col, thr, oracle.IC, 64, cfg.seed, k=cfg.k)
+    for flags in (0, bpt.FLAG_QUEUE):
+        e = g.sample(64, seed=cfg.seed, shard=(2, 0), flags=flags)
+        assert e.s0 == e.s1 == 0
+        seeds, gains, _ = e.select_seeds(cfg.k)
+        assert int(gains.sum()) == 0 and seeds.tolist() == list(range(cfg.k))
+        f = g.sample(64, seed=cfg.seed, shard=(2, 1), flags=flags)
+        assert (f.s0, f.s1) == (0, 64)
+        seeds, gains, _ = f.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+    gl = bpt.Graph(row_ptr, col, w_q31=graphgen.weights_lt(cfg.n, col, seed=3), model=bpt.LT)
+    s = gl.sample(64, seed=cfg.seed, shard=(2, 0))
+    seeds, gains, _ = s.select_seeds(cfg.k)
+    assert int(gains.sum()) == 0

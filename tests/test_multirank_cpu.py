@@ -106,3 +106,57 @@ def test_shard_range_tiles_theta():
             assert rs[0][0] == 0 and rs[-1][1] == theta
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert all(r[0] % 64 == 0 for r in rs)
+
+
+def _gather_worker(rank, world, port, theta, k, out_q):
+    """Member-list stores (LT): each rank samples its shard, the lists are gathered once
+    (sizes, then members, padded to the largest rank and compacted back in rank order) and
+    every rank runs the whole greedy locally -- the protocol of k_select.cu gather_lists."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 11, theta=theta)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT)
+    s0, s1 = graphgen.shard_range(theta, world, rank)
+    sizes, _, _, off, mem = g.sample_many(cfg.seed, np.arange(s0, s1, dtype=np.uint64), threads=2, members=True)
+    hdr = torch.tensor([s1 - s0, len(mem)], dtype=torch.int64)
+    hdrs = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(hdrs, hdr)
+    max_n = max(1, max(int(h[0]) for h in hdrs))
+    max_t = max(1, max(int(h[1]) for h in hdrs))
+    sz = torch.zeros(max_n, dtype=torch.int64)
+    sz[: s1 - s0] = torch.from_numpy(sizes.astype(np.int64))
+    mm = torch.zeros(max_t, dtype=torch.int64)
+    mm[: len(mem)] = torch.from_numpy(mem.astype(np.int64))
+    sz_all = [torch.zeros(max_n, dtype=torch.int64) for _ in range(world)]
+    mm_all = [torch.zeros(max_t, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sz_all, sz)
+    dist.all_gather(mm_all, mm)
+    g_sizes = np.concatenate([sz_all[r][: int(hdrs[r][0])].numpy() for r in range(world)])
+    g_mem = np.concatenate([mm_all[r][: int(hdrs[r][1])].numpy() for r in range(world)]).astype(np.uint32)
+    g_off = np.concatenate([[0], np.cumsum(g_sizes)]).astype(np.uint64)
+    seeds, gains = oracle.greedy(cfg.n, g_off, g_mem, k)
+    out_q.put((rank, seeds.tolist(), gains.tolist()))
+    dist.destroy_process_group()
+
+
+def test_gathered_list_selection_equals_greedy():
+    world, theta, k = 2, 64 * 9 + 5, 10  # ragged: the ranks own 5 and 5 blocks, the last one partial
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, theta, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 11, theta=theta)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT)
+    _, _, _, off, mem = g.sample_many(cfg.seed, np.arange(theta, dtype=np.uint64), members=True)
+    seeds, gains = oracle.greedy(cfg.n, off, mem, k)
+    for r in res:
+        assert r[1] == seeds.tolist() and r[2] == gains.tolist()

@@ -548,3 +548,119 @@ def test_sigma_hat_closed_forms():
     assert oracle.sigma_hat(1000, 64, 64) == 1000.0
     assert oracle.sigma_hat(1000, 0, 64) == 0.0
     assert oracle.sigma_hat(4847571, 12345, 65536) == 4847571 * 12345 / 65536
+
+
+# ---------------------------------------------------------------- coin keying, independent (C-1, C-3, C-6)
+
+def _py_philox2x32_10(x0, x1, key):
+    """Philox2x32-10 written from Salmon et al. (SC'11) in plain Python integers -- shares no
+    code with oracle.c; pinned by the Random123 KAT vectors below before it is used."""
+    M, W = 0xD256D193, 0x9E3779B9
+    for r in range(10):
+        if r:
+            key = (key + W) & 0xFFFFFFFF
+        p = M * x0
+        x0, x1 = ((p >> 32) ^ key ^ x1) & 0xFFFFFFFF, p & 0xFFFFFFFF
+    return x0, x1
+
+
+def _py_key(seed, tag):
+    return _py_philox2x32_10(seed & 0xFFFFFFFF, seed >> 32, tag)[0]
+
+
+def test_python_philox_kat():
+    for c0, c1, k, o0, o1 in load("philox_kat.json")["philox2x32_10"]:
+        assert _py_philox2x32_10(int(c0, 16), int(c1, 16), int(k, 16)) == (int(o0, 16), int(o1, 16))
+
+
+def _py_lt_walk(row_ptr, col, thr, seed, s, ctr_order="v_s"):
+    """Reverse LT walk of sample s (reading C-6) with coins keyed per reading C-1:
+    r = Philox(ctr = {v, lo32(s)}, key = k_LT)[0] >> 1; start per reading C-3. The reverse rows
+    are built here from the forward CSR in forward-position order (reading C-4)."""
+    n = len(row_ptr) - 1
+    rows = [[] for _ in range(n)]
+    for u in range(n):
+        for ef in range(int(row_ptr[u]), int(row_ptr[u + 1])):
+            rows[int(col[ef])].append((u, int(thr[ef])))
+    k_lt, k_st = _py_key(seed, oracle.TAG_LT), _py_key(seed, oracle.TAG_START)
+    w0, w1 = _py_philox2x32_10(s & 0xFFFFFFFF, s >> 32, k_st)
+    v = ((w1 << 32 | w0) * n) >> 64
+    seen = [v]
+    while True:
+        ctr = (v, s & 0xFFFFFFFF) if ctr_order == "v_s" else (s & 0xFFFFFFFF, v)
+        r = _py_philox2x32_10(ctr[0], ctr[1], k_lt)[0] >> 1
+        lo, nxt = 0, None
+        for u, t in rows[v]:
+            if lo <= r < lo + t:
+                nxt = u
+                break
+            lo += t
+        if nxt is None or nxt in seen:
+            return sorted(seen)
+        seen.append(nxt)
+        v = nxt
+
+
+@pytest.mark.parametrize("trial", range(4))
+def test_lt_coin_keying_independent(trial):
+    """The oracle's LT walks equal walks computed with an independent Philox and the coin key
+    of reading C-1 (ctr = {v, lo32(s)}, key = k_LT, TAG_LT = 0x4C540001); the swapped counter
+    order gives different walks, so the check discriminates the keying, not just the law."""
+    rng = np.random.default_rng(900 + trial)
+    n = int(rng.integers(20, 60))
+    row_ptr, col = graphgen.random_graph(n, int(rng.integers(2 * n, 6 * n)), seed=910 + trial)
+    thr = graphgen.weights_lt(n, col, seed=920 + trial)
+    g = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT)
+    seed = 0x1234_5678_9ABC + trial
+    differs = 0
+    for s in range(120):
+        mem = g.sample_one(seed, s)[0].tolist()
+        assert mem == _py_lt_walk(row_ptr, col, thr, seed, s)
+        differs += mem != _py_lt_walk(row_ptr, col, thr, seed, s, ctr_order="s_v")
+    assert differs > 10
+
+
+def test_ic_coin_keying_independent():
+    """IC coins of the oracle equal Philox(ctr = {e, lo32(s)}, key = k_IC)[0] >> 1 < thr computed
+    with the independent Philox (reading C-1/C-2), for random (s, e, thr) incl. 64-bit seeds."""
+    rng = np.random.default_rng(5)
+    for _ in range(400):
+        seed = int(rng.integers(0, 1 << 63))
+        s, e, t = int(rng.integers(0, 1 << 32)), int(rng.integers(0, 1 << 32)), int(rng.integers(0, Q31 + 1))
+        want = (_py_philox2x32_10(e, s & 0xFFFFFFFF, _py_key(seed, oracle.TAG_IC))[0] >> 1) < t
+        assert oracle.ic_edge_live(s, e, t, seed) == want
+
+
+# ---------------------------------------------------------------- full-size store (SURVEY §8(c) step 3)
+
+@pytest.mark.parametrize("which", ["C1", "C2s"])
+def test_store_equals_lists_group_work_and_greedy(which):
+    """The list / bitset RRR store gives the same sizes, digests, member lists, E_logical, per-group
+    E_phys / levels / frontier sizes (level-mask counting vs or_group_work's sort) and greedy
+    seeds / gains (count-maintaining greedy vs the naive recount and CELF) -- whichever
+    representation each sample takes (all lists, all bitsets, the n/32 default)."""
+    cfg = graphgen.CONFIGS["C1"] if which == "C1" else graphgen.scaled(graphgen.CONFIGS["C2"], 1 << 13, theta=640 + 17)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = oracle.Graph(row_ptr, col, w_q31=thr)
+    theta = cfg.theta
+    sz, dg, el, off, mem = g.sample_many(cfg.seed, np.arange(theta, dtype=np.uint64), members=True)
+    ref_seeds, ref_gains = oracle.greedy(cfg.n, off, mem, cfg.k)
+    lazy_seeds, lazy_gains = oracle.greedy(cfg.n, off, mem, cfg.k, lazy=True)
+    assert np.array_equal(ref_seeds, lazy_seeds) and np.array_equal(ref_gains, lazy_gains)
+    works = [g.group_work(cfg.seed, a, min(a + 64, theta)) for a in range(0, theta, 64)]
+    for list_max in (0, 1, 1 << 30):
+        S = oracle.Store(g, cfg.seed, 0, theta, 64, list_max=list_max)
+        assert np.array_equal(S.sizes, sz) and np.array_equal(S.digests, dg) and S.e_logical == int(el.sum())
+        for i in (0, 1, theta // 2, theta - 1):
+            assert np.array_equal(S.members(i), mem[off[i]:off[i + 1]])
+        assert S.e_phys.tolist() == [w["e_phys"] for w in works]
+        assert S.levels.tolist() == [w["levels"] for w in works]
+        for gi, w in enumerate(works):
+            assert S.frontier[gi, :w["levels"]].tolist() == w["frontier"].tolist()
+            assert not S.frontier[gi, w["levels"]:].any()
+        seeds, gains = S.greedy(cfg.k)
+        assert np.array_equal(seeds, ref_seeds) and np.array_equal(gains, ref_gains)
+    S = oracle.Store(g, cfg.seed, 0, theta, 64)
+    seeds, gains = S.greedy(cfg.n)  # exhaustion: every set covered, then smallest unselected ids
+    r_seeds, r_gains = oracle.greedy(cfg.n, off, mem, cfg.n)
+    assert np.array_equal(seeds, r_seeds) and np.array_equal(gains, r_gains)
