@@ -540,6 +540,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.ctl = ctl.as<Ctl>();
     a.theta = S.theta;
     a.k_ic = stream_key(S.seed, kTagIC);
+    for (int r = 0; r < 10; ++r) a.ic_keys[r] = a.k_ic + (uint32_t)r * kPhiloxW;
     a.k_lt = stream_key(S.seed, kTagLT);
     a.k_start = stream_key(S.seed, kTagStart);
     a.wide = wide ? 1 : 0;
@@ -605,7 +606,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
                 cur ^= 1;
             }
             launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>(),
-                            a.wide != 0);
+                            a.wide != 0, a.touched != nullptr);
             launch_next_batch(a, st);
         }
         BPT_CUDA(cudaStreamSynchronize(st));

@@ -205,6 +205,7 @@ struct BatchArgs {
     Ctl* ctl;
     uint64_t theta;           // global sample count (bits of samples >= theta stay 0)
     uint32_t k_ic, k_lt, k_start;
+    uint32_t ic_keys[10];     // Philox key schedule of k_ic: ic_keys[r] = k_ic + r * W (reading C-1)
     // wide fusion (IC, 64 colours): the slots_max = kWide blocks of a
     // batch share one frontier. Working masks vertex-major VN[v * kWide + b]; one frontier entry
     // per vertex with kWide masks; vflag[v] = v already queued for the next level.
@@ -216,6 +217,9 @@ struct BatchArgs {
     // ORs and marks every vertex whose N it makes non-empty in touched[slot * tile_words + v / 32];
     // the compaction scans the bitmap (1,024-vertex tiles) instead of a queue of first setters
     uint32_t* touched;        // nullptr: queue mode
+    // union layout (bitmap mode): the working masks are U[slot][n] = V | N (gathered by the
+    // expansion, 8 B per vertex) followed by V[slot][n] (read / written by the compaction only),
+    // in the VN allocation; new colours of a touched vertex = U & ~V
     uint32_t tiles;           // 1,024-vertex tiles per slot (tile_words = 32 * tiles)
     int lt_persist;           // LT fused loop: one cooperative launch per batch
     int lt_blocks_per_sm;     // ... with this many blocks per SM
@@ -230,10 +234,10 @@ constexpr uint32_t kWide = BPT_WIDE_BLOCKS;  // blocks (x 64 colours) per wide f
 constexpr uint32_t kUnitWide = BPT_UNIT_WIDE;  // work items per wide expansion unit (windows of 32)
 // k_store.cu
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog, bool wide);
+                     cudaStream_t st, unsigned long long* d_elog, bool wide, bool umode);
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
-                     bool wide);
+                     bool wide, bool umode);
 // k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph
 void launch_init(const BatchArgs& a, cudaStream_t st);
 void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,

@@ -77,6 +77,14 @@ __device__ __forceinline__ uint2 ld_stream(const uint2* p) {
                  : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_first()));
     return r;
 }
+// coherent (L2) load with evict-last: U is OR-merged by other warps during the same launch (a stale
+// value only skips fewer coins)
+__device__ __forceinline__ uint2 ld_keep_u64(const unsigned long long* p) {
+    uint2 r;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_last()));
+    return r;
+}
 __device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p) {
     ulonglong2 r;
     asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
@@ -137,7 +145,7 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
         if (a.touched) {  // bitmap mode: mark the start, the compaction of level 0 finds it
-            atomicOr(&a.VN[(size_t)slot * a.n + start].y, 1ull << bit);
+            atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + start, 1ull << bit);
             atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (start >> 5)], 1u << (start & 31));
             a.lv[0].any = 1;
             continue;
@@ -231,7 +239,13 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
                 const uint32_t v = (uint32_t)r[it];
                 const uint32_t slot = (uint32_t)(r[it] >> 32) & ((1u << 26) - 1u);
                 ulonglong2* p = &a.VN[(size_t)slot * a.n + v];
-                if (a.colors == 64) {
+                if (bitmap) {  // union layout: new = U & ~V, V = U
+                    unsigned long long* U = reinterpret_cast<unsigned long long*>(a.VN);
+                    const size_t iu = (size_t)slot * a.n + v, iv = (size_t)a.slots_max * a.n + iu;
+                    const unsigned long long u = LDX(&U[iu]);
+                    mask[it] = u & ~LDX(&U[iv]);
+                    U[iv] = u;
+                } else if (a.colors == 64) {
                     const ulonglong2 x = LDX(p);
                     mask[it] = x.y;
                     *p = make_ulonglong2(x.x | x.y, 0ull);
@@ -519,11 +533,11 @@ __device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, ui
 
 // One kUnitIC-item unit. kWhole: all items valid (every unit but the last of a level), so no
 // per-lane predication is needed on the loads.
-template <bool kWhole, bool kC64, bool kBm, bool kCoh>
+template <bool kWhole, bool kC64, bool kCoh>
 __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln, WarpScratch& W, int lane,
                                                uint32_t le_mask, uint32_t unit, uint32_t rem,
                                                uint32_t jc0, uint64_t gblk0, unsigned long long& coins,
-                                               unsigned long long& atoms, bool& any_pass) {
+                                               unsigned long long& atoms) {
     const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
     // ---- entry of every item: jc0 contains item 0; the compaction marked every entry start in
     //      the unit's kUnitIC-bit mask (the unit's own mask is cleared here for the next level)
@@ -546,7 +560,6 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
     uint2 rc[kWinIC];
     uint32_t vidx[kWinIC];
     uint64_t live[kWinIC];
-    bool nzero[kWinIC];  // N[u] was still empty when gathered (bitmap mode: this edge marks u)
 #pragma unroll
     for (int w = 0; w < kWinIC; ++w) ent[w] = LDX(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
 #pragma unroll
@@ -562,7 +575,6 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         vidx[w] = ent[w].y * a.n + rc[w].x;
         const ulonglong2 vn = kCoh ? ld_keep_cg(&a.VN[vidx[w]]) : ld_keep(&a.VN[vidx[w]]);
         live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
-        nzero[w] = vn.y == 0;
         if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
     }
     // ---- coin tasks of the whole unit, flattened into one list
@@ -635,23 +647,6 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
         __syncwarp();
         if (lane == 0) coins += ntask;
     }
-    if constexpr (kBm) {
-        // ---- merges (Listing 1 line 14) without a return value: fire-and-forget ORs into N[u].
-        //      An edge that found N[u] empty also marks u in the touched bitmap: the first OR to
-        //      land on N[u] in this level came from such an edge (N is empty at level start), so
-        //      every vertex with a non-empty N is marked; the compaction scans the bitmap.
-#pragma unroll
-        for (int w = 0; w < kWinIC; ++w) {
-            if (pass[w]) {
-                ++atoms;
-                atomicOr(&a.VN[vidx[w]].y, pass[w]);
-                if (nzero[w])
-                    atomicOr(&a.touched[(size_t)ent[w].y * a.tiles * 32 + (rc[w].x >> 5)], 1u << (rc[w].x & 31));
-                any_pass = true;
-            }
-        }
-        return;
-    }
     // ---- merges (Listing 1 line 14) of the windows issued together
     unsigned long long old[kWinIC];
 #pragma unroll
@@ -697,7 +692,7 @@ __device__ __forceinline__ void expand_unit_ic(const BatchArgs& a, LevelRec* Ln,
 #ifndef BPT_EXPAND_MINB
 #define BPT_EXPAND_MINB 5
 #endif
-template <bool kC64, bool kBm, bool kCoh>
+template <bool kC64, bool kCoh>
 __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_t* __restrict__ tstart,
                                                cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
@@ -732,20 +727,15 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     const uint32_t nfull = (uint32_t)(total / kUnitIC);
     const uint32_t nwarps = active * kWarps;
     unsigned long long coins = 0, atoms = 0;
-    bool any_pass = false;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = LDX(&tstart[unit]);
         if (unit < nfull)
-            expand_unit_ic<true, kC64, kBm, kCoh>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
+            expand_unit_ic<true, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms);
         else
-            expand_unit_ic<false, kC64, kBm, kCoh>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
-                                        jc0, gblk0, coins, atoms, any_pass);
+            expand_unit_ic<false, kC64, kCoh>(a, Ln, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC),
+                                        jc0, gblk0, coins, atoms);
     }
-    if constexpr (kBm) {
-        if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
-    } else {
-        warp_flush(a, Ln, W, lane);
-    }
+    warp_flush(a, Ln, W, lane);
     unsigned long long ct = block_sum_ull(coins, red);
     if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
     unsigned long long at = block_sum_ull(atoms, red);
@@ -753,140 +743,156 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
     finish_expand(a, h_level, use_cond, active);
 }
 
-// kBm: touched-bitmap mode (64 colours; a.touched != nullptr), else the first-setter queue
-template <bool kC64, bool kBm>
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
+// the first-setter queue form (BPT_FLAG_QUEUE with 64 colours, and every C < 64 run); C < 64 gets
+// 64 registers (4 blocks per SM): its slice handling spills at 48
+template <bool kC64>
+__global__ void __launch_bounds__(kThreads, kC64 ? BPT_EXPAND_MINB : 4) k_expand_ic(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                               cudaGraphConditionalHandle h_level, int use_cond) {
     count_self(a.ctl);
     if (!a.ctl->cont) return;
-    static_assert(kC64 || !kBm, "the touched bitmap needs 64-colour groups");
-    expand_ic_body<kC64, kBm, false>(a, tstart, h_level, use_cond);
+    expand_ic_body<kC64, false>(a, tstart, h_level, use_cond);
 }
 
 // ------------------------------------------------------------------------ IC expansion (product)
 // The product's IC expansion (64 colours, touched-bitmap frontier), Listing 1 lines 9-15
-// (P:168-174). Work units of kUnitIC = 32 * kWinIC consecutive reverse-edge reads (items) per
-// warp, kWinIC windows of 32 lanes; the entry of every item from the unit's first entry (tstart)
+// (P:168-174). Work units of kUnitBm = 32 * kWinBm consecutive reverse-edge reads (items) per
+// warp, kWinBm windows of 32 lanes; the entry of every item from the unit's first entry (tstart)
 // and a popcount of the entry-start bitmap; the windows' loads (entry, {src, thr} record,
-// {V, N}[u]) issued together; live = mask & ~(V | N) (N: colours another edge already merged into
-// u this level -- a stale N only skips fewer coins). Measured at the heavy levels (C2): 11% of
-// items carry a live colour, ~7 on average, so the live (item, colour) pairs are flattened into
-// one task list per unit and evaluated 32 at a time: the owner lane by a 5-step search of the
-// lanes' exclusive task prefix, the window by the owner's packed window prefix, the colour by a
-// rank select in the owner's live mask; one 16-byte shared load brings {edge id, thr, live}.
-// Passing colours are OR-merged per item in shared memory, then into N[u] by one fire-and-forget
-// OR per item; u is marked in the touched bitmap when its N was empty at the gather (the first OR
-// of a level into N[u] comes from such an item, so every vertex with a non-empty N is marked).
+// U[u]) issued together; live = mask & ~U[u] with U = V | N the union of the visited colours and
+// the colours another edge already merged into u this level (a stale U only skips fewer coins).
+// Union layout: the expansion gathers and ORs 8 B per vertex (U: 38.8 MB per block on C2, so it
+// stays L2-resident next to the streamed records); the compaction alone reads V.
+// Measured at the heavy levels (C2): ~11% of the items carry a live colour, ~7 live colours each.
+// So the live items are first compacted (ballot) into a per-warp list, and everything after the
+// gather works on that list, one live item per lane: its (item, colour) coin tasks are flattened
+// and evaluated 32 at a time (owner lane by a 5-step search of the exclusive task prefix, colour
+// by a rank select in the owner's live mask, one 16-byte shared load per task, the Philox key
+// schedule read from the kernel parameters), the passing colours OR-merged per item in shared
+// memory and then into U[u] by one fire-and-forget OR per item, and u is marked in the touched
+// bitmap (the compaction finds the new colours as U & ~V).
+#ifndef BPT_WIN_BM
+#define BPT_WIN_BM 4
+#endif
+constexpr int kWinBm = BPT_WIN_BM;   // 32-lane windows per warp work unit (4: measured 4% faster than 3)
+constexpr int kUnitBm = 32 * kWinBm;
 struct BmScratch {
-    uint4 item[kWinIC][32];                 // live items: {edge id, thr, live lo, live hi}
-    unsigned long long pass[kWinIC][32];    // live items: passing colours (ATOMS.OR on 32-bit halves)
-    uint32_t sb[kWinIC][32];                // live items: global id of colour 0 of the item's block
-    uint32_t excl[32];                      // exclusive prefix of the lanes' task counts
-    uint32_t cum[32];                       // per-lane window prefix: c0 | (c0+c1) << 8 | (c0+c1+c2) << 16
+    uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
+    uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
+    unsigned long long pass[32];            // passing colours of the chunk's live items
+    uint32_t excl[32];                      // exclusive prefix of the chunk's task counts
 };
+
+// Philox2x32-10 (reading C-1) with the key schedule k + r * W precomputed in the kernel parameters
+__device__ __forceinline__ uint32_t philox_ks0(uint32_t x0, uint32_t x1, const uint32_t (&ks)[10]) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p = (uint64_t)kPhiloxM * (uint64_t)x0;
+        const uint32_t hi = (uint32_t)(p >> 32), lo = (uint32_t)p;
+        x0 = hi ^ ks[r] ^ x1;
+        x1 = lo;
+    }
+    return x0;
+}
 
 template <bool kWhole>
 __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, int lane, uint32_t le_mask,
                                                uint32_t unit, uint32_t rem, uint32_t jc0, uint64_t gblk0,
                                                unsigned long long& coins, unsigned long long& atoms,
                                                bool& any_pass) {
-    const uint32_t t0l = unit * (uint32_t)kUnitIC;  // mod 2^32: edge ids are t + delta (mod 2^32)
-    uint32_t mw[kWinIC];
+    const uint32_t t0l = unit * (uint32_t)kUnitBm;  // mod 2^32: edge ids are t + delta (mod 2^32)
+    uint32_t mw[kWinBm];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) mw[w] = __ldg(&a.umask[(size_t)unit * kWinIC + w]);
+    for (int w = 0; w < kWinBm; ++w) mw[w] = __ldg(&a.umask[(size_t)unit * kWinBm + w]);
     __syncwarp();
-    if (lane < kWinIC) a.umask[(size_t)unit * kWinIC + lane] = 0;
+    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;
     mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
-    uint32_t jl[kWinIC];
+    uint32_t jl[kWinBm];
     uint32_t before = jc0;
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
+    for (int w = 0; w < kWinBm; ++w) {
         jl[w] = before + __popc(mw[w] & le_mask);
         before += __popc(mw[w]);
     }
-    uint4 ent[kWinIC];
-    uint2 rc[kWinIC];
+    uint4 ent[kWinBm];
+    uint2 rc[kWinBm];
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
+    for (int w = 0; w < kWinBm; ++w) ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
+    for (int w = 0; w < kWinBm; ++w) {
         const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
         rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
     }
-    uint32_t vidx[kWinIC], tword[kWinIC], tbits = 0, c[kWinIC], tot = 0;
-    uint64_t live[kWinIC];
+    // ---- gather of U[u] = V[u] | N[u] (union layout), live colours, compacted list of live items
+    const uint32_t lt_mask = le_mask >> 1;  // lanes below this one
+    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
+    uint32_t nlive = 0;
 #pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
-        vidx[w] = ent[w].y * a.n + rc[w].x;
-        const ulonglong2 vn = ld_keep(&a.VN[vidx[w]]);
-        live[w] = (((uint64_t)ent[w].w << 32) | ent[w].z) & ~(vn.x | vn.y);
-        if (!kWhole && 32u * w + lane >= rem) live[w] = 0;
-        tword[w] = vn.y == 0 ? ent[w].y * a.tiles * 32 + (rc[w].x >> 5) : ~0u;
-        tbits |= (rc[w].x & 31u) << (5 * w);
-        c[w] = __popcll(live[w]);
-        tot += c[w];
-    }
-    const uint32_t incl = warp_incl_scan_u32(tot, lane);
-    const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-    if (ntask == 0) return;
-    uint32_t cm = 0, run = 0;
-#pragma unroll
-    for (int w = 0; w < 3; ++w) {
-        if (w < kWinIC - 1) run += c[w];
-        cm |= (w < kWinIC - 1 ? run : 0xffu) << (8 * w);
-    }
-#pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
-        if (live[w]) {
-            W.item[w][lane] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, (uint32_t)live[w],
-                                         (uint32_t)(live[w] >> 32));
-            W.sb[w][lane] = (uint32_t)(64ull * (gblk0 + ent[w].y));
-            W.pass[w][lane] = 0;
+    for (int w = 0; w < kWinBm; ++w) {
+        const uint32_t vidx = ent[w].y * a.n + rc[w].x;
+        const uint2 uu = ld_keep_u64(&U[vidx]);
+        uint32_t lo = ent[w].z & ~uu.x;
+        uint32_t hi = ent[w].w & ~uu.y;
+        if (!kWhole && 32u * w + lane >= rem) lo = hi = 0;
+        const bool lv = (lo | hi) != 0;
+        const uint32_t bal = __ballot_sync(kFull, lv);
+        if (lv) {
+            const uint32_t pos = nlive + __popc(bal & lt_mask);
+            W.A[pos] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, lo, hi);
+            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,
+                                  ent[w].y * a.tiles * 32 + (rc[w].x >> 5), rc[w].x & 31u);
         }
+        nlive += __popc(bal);
     }
-    W.excl[lane] = incl - tot;
-    W.cum[lane] = cm;
+    if (nlive == 0) return;
     __syncwarp();
-    for (uint32_t b = 0; b < ntask; b += 32) {
-        const uint32_t k = b + lane;
-        if (k < ntask) {
-            uint32_t o = 0;  // owner lane = largest lane with excl <= k
+    // ---- coins and merges, one chunk of <= 32 live items at a time (one live item per lane)
+    for (uint32_t c0 = 0; c0 < nlive; c0 += 32) {
+        const uint32_t j = c0 + lane;
+        const bool has = j < nlive;
+        uint32_t cnt = 0;
+        if (has) {
+            const uint4 it = W.A[j];
+            cnt = __popc(it.z) + __popc(it.w);
+            W.pass[lane] = 0;
+        }
+        const uint32_t incl = warp_incl_scan_u32(cnt, lane);
+        const uint32_t ntask = __shfl_sync(kFull, incl, 31);
+        W.excl[lane] = incl - cnt;
+        __syncwarp();
+        for (uint32_t b = 0; b < ntask; b += 32) {
+            const uint32_t k = b + lane;
+            if (k < ntask) {
+                uint32_t o = 0;  // owner = largest lane with excl <= k
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1)
-                if (W.excl[o + step] <= k) o += step;
-            uint32_t r = k - W.excl[o];
-            const uint32_t cmo = W.cum[o];
-            uint32_t w = 0, base = 0;  // window of the task: last window whose prefix <= r
-#pragma unroll
-            for (int q = 0; q < kWinIC - 1; ++q) {
-                const uint32_t pq = (cmo >> (8 * q)) & 0xffu;
-                if (r >= pq) { w = q + 1; base = pq; }
+                for (int step = 16; step > 0; step >>= 1)
+                    if (W.excl[o + step] <= k) o += step;
+                const uint4 it = W.A[c0 + o];
+                const uint32_t bit = nth_set_bit64(((uint64_t)it.w << 32) | it.z, k - W.excl[o]);
+                const uint32_t x = philox_ks0(it.x, W.B[c0 + o].x + bit, a.ic_keys);
+                if ((x >> 1) < it.y)
+                    atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
-            const uint4 it = W.item[w][o];
-            const uint32_t bit = nth_set_bit64(((uint64_t)it.w << 32) | it.z, r - base);
-            const uint32_t x = philox2x32_10(it.x, W.sb[w][o] + bit, a.k_ic).x;
-            if ((x >> 1) < it.y)
-                atomicOr(reinterpret_cast<uint32_t*>(&W.pass[w][o]) + (bit >> 5), 1u << (bit & 31));
         }
-    }
-    if (lane == 0) coins += ntask;
-    __syncwarp();
-#pragma unroll
-    for (int w = 0; w < kWinIC; ++w) {
-        if (live[w]) {
-            const unsigned long long pass = W.pass[w][lane];
+        if (lane == 0) coins += ntask;
+        __syncwarp();
+        if (has) {
+            const unsigned long long pass = W.pass[lane];
             if (pass) {
+                const uint4 bb = W.B[j];
                 ++atoms;
-                atomicOr(&a.VN[vidx[w]].y, pass);
-                if (tword[w] != ~0u) atomicOr(&a.touched[tword[w]], 1u << ((tbits >> (5 * w)) & 31u));
+                atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + bb.y, pass);
+                atomicOr(&a.touched[bb.z], 1u << bb.w);
                 any_pass = true;
             }
         }
+        __syncwarp();
     }
-    __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_bm(BatchArgs a, const uint32_t* __restrict__ tstart,
+#ifndef BPT_BM_MINB
+#define BPT_BM_MINB 4  // 64 registers: no spills; 4 x 8 warps per SM (measured: -4% vs 5 blocks at 48)
+#endif
+__global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                               cudaGraphConditionalHandle h_level, int use_cond) {
     count_self(a.ctl);
     if (!a.ctl->cont) return;
@@ -900,7 +906,7 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_bm(BatchAr
     const uint64_t total = packed & kEdgeMask;
     const bool idle = nq == 0 || L->overflow;
     const uint32_t active =
-        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kUnitIC * kWarps - 1) / ((uint64_t)kUnitIC * kWarps)));
+        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kUnitBm * kWarps - 1) / ((uint64_t)kUnitBm * kWarps)));
     if (blockIdx.x >= active) return;
     if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
     if (idle) {
@@ -912,165 +918,18 @@ __global__ void __launch_bounds__(kThreads, BPT_EXPAND_MINB) k_expand_bm(BatchAr
     __shared__ unsigned long long red[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
-    const uint32_t nunits = (uint32_t)((total + kUnitIC - 1) / kUnitIC);
-    const uint32_t nfull = (uint32_t)(total / kUnitIC);
+    const uint32_t nunits = (uint32_t)((total + kUnitBm - 1) / kUnitBm);
+    const uint32_t nfull = (uint32_t)(total / kUnitBm);
     const uint32_t nwarps = active * kWarps;
     unsigned long long coins = 0, atoms = 0;
     bool any_pass = false;
     for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = __ldg(&tstart[unit]);
         if (unit < nfull)
-            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitIC, jc0, gblk0, coins, atoms, any_pass);
+            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitBm, jc0, gblk0, coins, atoms, any_pass);
         else
-            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitIC), jc0, gblk0,
+            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, gblk0,
                                   coins, atoms, any_pass);
-    }
-    if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
-    unsigned long long ct = block_sum_ull(coins, red);
-    if (threadIdx.x == 0 && ct) atomicAdd(&((LevelRec*)L)->coins, ct);
-    unsigned long long at = block_sum_ull(atoms, red);
-    if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
-    finish_expand(a, h_level, use_cond, active);
-}
-
-// ------------------------------------------------------------------------ IC expansion, lane chunks
-// The product's IC expansion (64 colours, touched-bitmap frontier): Listing 1 lines 9-15
-// with each lane owning kLcK CONSECUTIVE work items (reverse-edge reads) of a
-// 32 * kLcK-item warp unit, so the per-item work is a handful of instructions:
-//   * entry lookup once per lane (tstart + a popcount of the unit's entry-start bits), a new
-//     entry record only where one starts inside the lane's chunk (entries average ~30-40 items at
-//     the heavy levels);
-//   * per item: the {src, thr} record, the {V, N}[u] gather (kLcP items per phase in flight per
-//     lane), live = mask & ~(V | N);
-//   * coins lane-locally: every live colour c of the item draws coin(s_c, e) (readings C-1/C-2);
-//     lanes of one entry see similar live counts, so the warp's loop runs ~the lanes' common count;
-//   * merges with one fire-and-forget OR into N[u] per passing item; u is marked in the touched
-//     bitmap when its N was empty at the gather (the first OR of a level into N[u] comes from such
-//     an item, so every vertex with a non-empty N is marked).
-// No shared memory: the whole L1 caches the hub vertices' {V, N} sectors and the records.
-#ifndef BPT_LC_K
-#define BPT_LC_K 8
-#endif
-constexpr int kLcK = BPT_LC_K;      // items per lane
-#ifndef BPT_LC_P
-#define BPT_LC_P 4
-#endif
-constexpr int kLcP = BPT_LC_P;      // items per phase (loads in flight per lane)
-constexpr int kLcUnit = 32 * kLcK;  // items per warp unit
-#ifdef BPT_EXPAND_LC
-constexpr bool kBmLc = true;        // bitmap mode expands with k_expand_lc (experiment)
-#else
-constexpr bool kBmLc = false;       // bitmap mode expands with k_expand_ic<true, true>
-#endif
-static_assert(kLcK % kLcP == 0 && kLcK <= 8, "a lane's entry-start bits are one byte");
-
-__device__ __forceinline__ uint2 ld_rec_l1(const uint2* p) {  // L1-allocating (the lanes' chunks share lines)
-    uint2 r;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
-                 : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_first()));
-    return r;
-}
-
-template <bool kWhole>
-__device__ __forceinline__ void expand_unit_lc(const BatchArgs& a, int lane, uint32_t unit, uint32_t rem, uint32_t jc0,
-                                               uint64_t gblk0, unsigned long long& coins, unsigned long long& atoms,
-                                               bool& any_pass) {
-    constexpr uint32_t kWords = kLcUnit / 32;
-    const uint32_t t0 = unit * (uint32_t)kLcUnit;  // mod 2^32: edge ids are t + delta (mod 2^32)
-    const uint32_t p0 = (uint32_t)kLcK * lane;     // the lane's first item in the unit
-    // ---- entry-start bits of the lane's items (item 0 of the unit is in jc0)
-    const uint32_t wv = __ldg(&a.umask[(size_t)unit * kWords + (p0 >> 5)]);
-    __syncwarp();
-    if (lane < (int)kWords) a.umask[(size_t)unit * kWords + lane] = 0;  // cleared for the next level
-    uint32_t bits = (wv >> (p0 & 31)) & ((1u << kLcK) - 1u);
-    if (lane == 0) bits &= ~1u;
-    const uint32_t cnt = __popc(bits);
-    const uint32_t j0 = jc0 + warp_incl_scan_u32(cnt, lane) - cnt;  // entry of the item before the chunk
-#pragma unroll
-    for (int ph = 0; ph < kLcK / kLcP; ++ph) {
-        uint32_t e[kLcP], thr[kLcP], sb[kLcP], vidx[kLcP], tword[kLcP], tbits = 0;
-        uint64_t live[kLcP];
-        uint2 rc[kLcP];
-        uint4 ent = __ldg(&a.q[j0 + __popc(bits & ((2u << (kLcP * ph)) - 1u))]);
-#pragma unroll
-        for (int ii = 0; ii < kLcP; ++ii) {
-            const int i = kLcP * ph + ii;
-            if (ii > 0 && ((bits >> i) & 1u)) ent = __ldg(&a.q[j0 + __popc(bits & ((2u << i) - 1u))]);
-            const bool ok = kWhole || p0 + i < rem;
-            e[ii] = t0 + p0 + i + ent.x;
-            rc[ii] = ld_rec_l1(&a.rec[ok ? e[ii] : 0u]);  // items past the level's end: masked below
-            vidx[ii] = ent.y * a.n;
-            sb[ii] = (uint32_t)(64ull * (gblk0 + ent.y));
-            live[ii] = ok ? (((uint64_t)ent.w << 32) | ent.z) : 0ull;
-            tword[ii] = ent.y * a.tiles * 32;
-        }
-#pragma unroll
-        for (int ii = 0; ii < kLcP; ++ii) {
-            vidx[ii] += rc[ii].x;
-            thr[ii] = rc[ii].y;
-            const ulonglong2 vn = ld_keep(&a.VN[vidx[ii]]);
-            live[ii] &= ~(vn.x | vn.y);
-            tword[ii] = vn.y == 0 ? tword[ii] + (rc[ii].x >> 5) : ~0u;
-            tbits |= (rc[ii].x & 31u) << (5 * ii);
-        }
-#pragma unroll
-        for (int ii = 0; ii < kLcP; ++ii) {
-            uint64_t m = live[ii], pass = 0;
-            coins += __popcll(m);
-            while (m) {
-                const uint32_t c = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const uint32_t x = philox2x32_10(e[ii], sb[ii] + c, a.k_ic).x;
-                if ((x >> 1) < thr[ii]) pass |= 1ull << c;
-            }
-            if (pass) {
-                ++atoms;
-                atomicOr(&a.VN[vidx[ii]].y, pass);
-                if (tword[ii] != ~0u) atomicOr(&a.touched[tword[ii]], 1u << ((tbits >> (5 * ii)) & 31u));
-                any_pass = true;
-            }
-        }
-    }
-}
-
-#ifndef BPT_LC_MINB
-#define BPT_LC_MINB 4
-#endif
-__global__ void __launch_bounds__(kThreads, BPT_LC_MINB) k_expand_lc(BatchArgs a, const uint32_t* __restrict__ tstart,
-                                                              cudaGraphConditionalHandle h_level, int use_cond) {
-    count_self(a.ctl);
-    if (!a.ctl->cont) return;
-    Ctl* ctl = a.ctl;
-    const uint32_t level = ctl->level;
-    const uint64_t gblk0 = ctl->gblk0;
-    const LevelRec* L = &a.lv[level];
-    LevelRec* Ln = &a.lv[level + 1];
-    const unsigned long long packed = L->packed;
-    const uint64_t nq = packed >> kPackShift;
-    const uint64_t total = packed & kEdgeMask;
-    const bool idle = nq == 0 || L->overflow;
-    const uint32_t active =
-        idle ? 1u : (uint32_t)umin64(gridDim.x, umax64(1, (total + (uint64_t)kLcUnit * kWarps - 1) / ((uint64_t)kLcUnit * kWarps)));
-    if (blockIdx.x >= active) return;
-    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
-    if (idle) {
-        finish_expand(a, h_level, use_cond, active);
-        return;
-    }
-    __shared__ unsigned long long red[kWarps];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t nunits = (uint32_t)((total + kLcUnit - 1) / kLcUnit);
-    const uint32_t nfull = (uint32_t)(total / kLcUnit);
-    const uint32_t nwarps = active * kWarps;
-    unsigned long long coins = 0, atoms = 0;
-    bool any_pass = false;
-    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
-        const uint32_t jc0 = __ldg(&tstart[unit]);
-        if (unit < nfull)
-            expand_unit_lc<true>(a, lane, unit, kLcUnit, jc0, gblk0, coins, atoms, any_pass);
-        else
-            expand_unit_lc<false>(a, lane, unit, (uint32_t)(total - (uint64_t)unit * kLcUnit), jc0, gblk0, coins, atoms,
-                                  any_pass);
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
     unsigned long long ct = block_sum_ull(coins, red);
@@ -1977,7 +1836,6 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 
 int g_expand_grid = 0;
 int g_expand_grid_w = 0;
-int g_expand_grid_t = 0;
 int g_expand_grid_b = 0;
 int g_expand_grid_lt = 0;
 int g_levels_per_sm_lt = 0;  // co-resident blocks per SM of the cooperative LT loop
@@ -2032,27 +1890,25 @@ void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, ui
 }
 
 uint32_t expand_unit(int model, bool bitmap) {
-    return model == BPT_IC ? (bitmap && kBmLc ? (uint32_t)kLcUnit : (uint32_t)kUnitIC) : kTile;
+    return model == BPT_IC ? (bitmap ? (uint32_t)kUnitBm : (uint32_t)kUnitIC) : kTile;
 }
 
 int expand_grid() {
     if (!g_expand_grid) {
         int per_sm = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_lt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemTile)));
-        for (void* f : {(void*)k_expand_ic<true, true>, (void*)k_expand_ic<true, false>, (void*)k_expand_ic<false, false>})
+        for (void* f : {(void*)k_expand_ic<true>, (void*)k_expand_ic<false>})
             BPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(sizeof(WarpScratch) * kWarps)));
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true, true>, kThreads,
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_ic<true>, kThreads,
                                                                sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
-        int per_sm_t = 0, per_sm_b = 0;
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_expand_lc, kThreads, 0));
+        int per_sm_b = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_bm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(BmScratch) * kWarps)));
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_expand_bm, kThreads,
                                                                sizeof(BmScratch) * kWarps));
         g_expand_grid_b = num_sms() * (per_sm_b > 0 ? per_sm_b : 1);
-        g_expand_grid_t = num_sms() * (per_sm_t > 0 ? per_sm_t : 1);
         int per_sm_w = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(WarpScratchW) * kWarps)));
@@ -2111,12 +1967,11 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
     k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model, a.touched != nullptr));
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
     if (a.model == BPT_IC && a.touched)
-        kBmLc ? k_expand_lc<<<g_expand_grid_t, kThreads, 0, st>>>(a, tstart, h0, 0)
-              : k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC && a.colors == 64)
-        k_expand_ic<true, false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
-        k_expand_ic<false, false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        k_expand_ic<false><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else
         k_expand_lt<<<g_expand_grid_lt, kThreads, sizeof(SmemTile), st>>>(a, tstart, h0, 0);
     if (ev1) BPT_CUDA(cudaEventRecord(ev1, st));
@@ -2181,7 +2036,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         coop.cooperative = 1;
         BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
         cudaGraphNode_t n_store;
-        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0);
+        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched != nullptr);
         void* nb_args[] = {&args, &h_batch, &one};
         add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
         cudaGraphExec_t exec;
@@ -2209,17 +2064,16 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),
                      sizeof(WarpScratchW) * kWarps, exp_args)
         : a.model == BPT_IC && a.touched
-        ? (kBmLc ? add_kernel(lbody, &n_cmp, (void*)k_expand_lc, dim3(g_expand_grid_t), dim3(kThreads), 0, exp_args)
-                 : add_kernel(lbody, &n_cmp, (void*)k_expand_bm, dim3(g_expand_grid_b), dim3(kThreads),
-                              sizeof(BmScratch) * kWarps, exp_args))
+        ? add_kernel(lbody, &n_cmp, (void*)k_expand_bm, dim3(g_expand_grid_b), dim3(kThreads),
+                     sizeof(BmScratch) * kWarps, exp_args)
         : a.model == BPT_IC
-        ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true, false> : (void*)k_expand_ic<false, false>,
+        ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
     // the expansion's last block advances the level and sets the loop condition
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
-    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0);
+    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched != nullptr);
     void* nb_args[] = {&args, &h_batch, &one};
     add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
 

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
                                                           unsigned long long* __restrict__ elog_total,
                                                           uint32_t* __restrict__ count0, int single_slot,
-                                                          uint32_t vstride, uint64_t sstride) {
+                                                          uint32_t vstride, uint64_t sstride, int umode) {
     constexpr int kW = kFinThreads / 32;
     __shared__ unsigned long long s_mask[kW][32];
     __shared__ uint32_t s_size[kW][64];
@@ -47,6 +47,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     // working mask of vertex v of this block: W[v * vstride] (slot-major: vstride 1, sstride n;
     // wide vertex-major: vstride kWide, sstride 1)
     ulonglong2* W = VN + (size_t)blockIdx.y * sstride;
+    // union layout: U[slot][n] then V[slot][n]; sstride = n, gridDim.y = slots_max
+    unsigned long long* UV = reinterpret_cast<unsigned long long*>(VN) + (size_t)blockIdx.y * n;
+    const size_t slots_max_n = (size_t)gridDim.y * n;
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -58,7 +61,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const uint64_t v = base + 32ull * u + lane;
-            m[u] = v < v_end ? W[v * vstride].x : 0ull;  // N is 0 after the last level
+            // N is 0 after the last level (union layout: U == V, V after the U block)
+            m[u] = v < v_end ? (umode ? UV[slots_max_n + v] : W[v * vstride].x) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -66,7 +70,12 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
             if (v < v_end) {
                 V[v] = m[u];
                 if (m[u]) {
-                    W[v * vstride] = make_ulonglong2(0ull, 0ull);
+                    if (umode) {
+                        UV[v] = 0ull;
+                        UV[slots_max_n + v] = 0ull;
+                    } else {
+                        W[v * vstride] = make_ulonglong2(0ull, 0ull);
+                    }
                     const uint32_t pc = __popcll(m[u]);
                     // occurrences (A7 round 0): one block owns v when the batch has one slot
                     if (single_slot) count0[v] += pc;
@@ -263,13 +272,13 @@ void compute_digests(const Samples& S, cudaStream_t st) {
 }
 
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog, bool wide) {
+                     cudaStream_t st, unsigned long long* d_elog, bool wide, bool umode) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
                                              S.sizes.as<uint32_t>(), d_elog,
                                              S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0,
-                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n);
+                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n, umode ? 1 : 0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
 }
@@ -277,7 +286,7 @@ void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t 
 // graph node for the finaliser (device-resident batch loop)
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
-                     bool wide) {
+                     bool wide, bool umode) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     uint64_t* store = S.store.as<uint64_t>();
@@ -288,8 +297,9 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     int single = slots_max == 1 ? 1 : 0;
     uint32_t vstride = wide ? kWide : 1u;
     uint64_t sstride = wide ? 1 : (uint64_t)n;
+    int um = umode ? 1 : 0;
     void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog,
-                        &count0, &single, &vstride, &sstride};
+                        &count0, &single, &vstride, &sstride, &um};
     cudaKernelNodeParams p{};
     p.func = (void*)k_finalize;
     p.gridDim = grid;

@@ -1,0 +1,83 @@
+"""Like-for-like DRAM traffic of the IC expansion (roofline `traffic`), for bench.py.
+
+Runs batch 0 of the bench's C2 step -- the first 64-sample group (samples 0..63, the bench's first
+sampling seed), batch_groups = 1 exactly as bench.py launches it -- through the host-driven level
+loop, and writes every level's counters to gpurun_out/traffic_levels.json. Run it under
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \\
+      -k regex:k_expand --csv --log-file gpurun_out/traffic_ncu.csv python scripts/traffic_capture.py
+then `python scripts/traffic_capture.py --summarize` (here, no GPU) pairs launch i with level i and
+writes profiles/expand_traffic.json: per launch the DRAM bytes next to the algorithmic bytes of the
+SAME launch (DESIGN.md §6 byte model), and their sums."""
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "gpurun_out")
+
+
+def alg_bytes(rows):
+    """DESIGN.md §6 per-level byte model (same as bpt_samples_info.expand_bytes): 16 B per reverse-edge
+    read, 8 B per atomicOr, 24 B per frontier entry, 8 B per vertex discovered for the next level."""
+    out = []
+    for i, r in enumerate(rows):
+        batch, level, raw, kept, work, vc, coins, atomics = r
+        raw_next = rows[i + 1][2] if i + 1 < len(rows) and rows[i + 1][0] == batch else 0
+        out.append(16.0 * work + 8.0 * atomics + 24.0 * kept + 8.0 * raw_next)
+    return out
+
+
+def capture():
+    import torch
+    import graphgen
+    import paper_2311_10201_b200 as bpt
+    cfg = graphgen.CONFIGS["C2"]
+    torch.cuda.set_device(0)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    s = g.sample(64, colors=64, seed=cfg.seed, batch_groups=1, profile=True, poll_levels=64)
+    rows = s.level_stats().tolist()
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "traffic_levels.json"), "w") as f:
+        json.dump({"rows": rows, "info": s.info}, f)
+    print(json.dumps({"levels": len(rows), "e_phys": s.info["e_phys"]}))
+
+
+def summarize():
+    lv = json.load(open(os.path.join(OUT, "traffic_levels.json")))
+    rows = lv["rows"]
+    alg = alg_bytes(rows)
+    launches = {}
+    for r in csv.DictReader(l for l in open(os.path.join(OUT, "traffic_ncu.csv")) if not l.startswith("==")):
+        key = (r["ID"], r["Kernel Name"])
+        d = launches.setdefault(key, {"name": r["Kernel Name"]})
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                 "msecond": 1e-3}.get(unit, 1)
+        d[r["Metric Name"]] = v * scale
+    seq = [launches[k] for k in sorted(launches, key=lambda k: int(k[0]))]
+    per = []
+    for i, d in enumerate(seq):
+        a = alg[i] if i < len(alg) else 0.0  # launches after the last level are no-ops (pipelined polling)
+        per.append({"level": i, "dram_bytes": d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0),
+                    "algorithmic_bytes": a, "edges": rows[i][4] if i < len(rows) else 0,
+                    "us": d.get("gpu__time_duration.sum", 0) * 1e6})
+    dram = sum(p["dram_bytes"] for p in per)
+    algs = sum(p["algorithmic_bytes"] for p in per)
+    n = len(per)
+    res = {"source": "scripts/traffic_capture.py under ncu (dram__bytes_read/write.sum per launch), bench step batch 0 "
+                     "(C2, samples 0..63, bench seed, batch_groups = 1, host-driven level loop)",
+           "kernel": seq[0]["name"] if seq else None, "launches": n,
+           "dram_bytes_per_launch": dram / n if n else None, "algorithmic_bytes_per_launch": algs / n if n else None,
+           "dram_over_algorithmic": dram / algs if algs else None, "per_launch": per}
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", "expand_traffic.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps({k: v for k, v in res.items() if k != "per_launch"}, indent=1))
+
+
+if __name__ == "__main__":
+    summarize() if "--summarize" in sys.argv else capture()
