@@ -43,7 +43,8 @@ UNIT = "RRR sets/s"
 CFG = graphgen.CONFIGS["C2"]
 EXTRACT_SAMPLES = 64
 PER_MEMBER_BYTES_LT = "24 B per RRR member (8 B row bounds + 8 B chosen in-edge record + 8 B visited-set insertion)"
-PER_EDGE_BYTES = "16 B per reverse-edge read (8 B {src,thr} record + 8 B V[u] gather) + 8 B per atomicOr + 24 B per frontier entry + 8 B per enqueued entry"
+PER_EDGE_BYTES = ("16 B per reverse-edge read (8 B {src,thr} record + 8 B U[u] = V|N gather) + 8 B per atomicOr "
+                  "+ 24 B per frontier entry + 8 B per vertex discovered for the next level")
 
 
 def parse():
@@ -140,15 +141,15 @@ def measured_peak_hbm() -> tuple[float, str]:
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def ncu_traffic_per_launch(name: str):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def ncu_traffic(name: str) -> dict:
+    """DRAM read+write bytes per launch of the dominant kernel from a committed ncu capture, with the
+    algorithmic bytes of the SAME launches (scripts/traffic_capture.py)."""
     p = os.path.join(ROOT, "profiles", name)
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch"), d.get("source")
+            return json.load(f)
     except Exception:
-        return None, None, None
+        return {}
 
 
 # ------------------------------------------------------------------ CPU oracle baseline
@@ -284,6 +285,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     clocks.start()
     clocks.wait_first()
     launches0 = bpt.kernel_launch_count()
+    graph0 = bpt.graph_kernel_count()
     barrier()
     torch.cuda.synchronize()
     clocks.mark()
@@ -298,7 +300,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    launches = bpt.kernel_launch_count() - launches0
+    host_launches = bpt.kernel_launch_count() - launches0
+    graph_kernels = bpt.graph_kernel_count() - graph0
+    launches = host_launches + graph_kernels
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64)
     if world > 1:
@@ -381,16 +385,32 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return
     peak, peak_src = measured_peak_hbm()
+    # the co-binding integer-ALU roof of the coins: Philox2x32-10 evaluations per second
+    # measured on this device, against the coins the expansion evaluated per step
+    pc, pms = bpt.bench_philox(256)
+    coins = float(pinfo["coins"])
+    alu = {"philox_calls_per_s": pc / (pms / 1000.0), "coins_per_step": coins,
+           "coins_per_edge_read": coins / float(pinfo["e_phys"]) if pinfo["e_phys"] else None,
+           "coin_roof_ms_per_step": 1000.0 * coins / (pc / (pms / 1000.0)),
+           "coin_roof_share_of_expansion": (1000.0 * coins / (pc / (pms / 1000.0))) / ms_expand if ms_expand else None}
+    prof = ncu_traffic("expand_ncu_summary.json") if cfg.model == "IC" else {}
+    for key in ("inst_per_edge_read", "issue_active_pct", "warps_active_pct", "l2_hit_pct", "source"):
+        if key in prof:
+            alu["ncu_" + key] = prof[key]
     achieved = expand_bytes / (ms_expand / 1000.0) / 1e9 if ms_expand > 0 else None
     if cfg.model == "IC":
-        traffic, alg_ncu, traffic_src = ncu_traffic_per_launch("expand_traffic.json")
-        kernel, per_unit = "k_expand_ic (A3 fused frontier expansion)", PER_EDGE_BYTES
+        tr = ncu_traffic("expand_traffic.json")
+        kernel, per_unit = "k_expand_bm (A3 fused frontier expansion)", PER_EDGE_BYTES
     else:  # LT: one reverse walk per sample into the sparse member-list store
-        traffic, alg_ncu, traffic_src = ncu_traffic_per_launch("walk_lt_traffic.json")
+        tr = ncu_traffic("walk_lt_traffic.json")
         kernel, per_unit = "k_walk_lt_sparse (A3' LT reverse walks, sparse store)", PER_MEMBER_BYTES_LT
+    traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_algorithmic_per_launch": tr.get("algorithmic_bytes_per_launch"),
+                "traffic_over_algorithmic": tr.get("dram_over_algorithmic"),
+                "traffic_launches": tr.get("launches"),
                 "algorithmic_bytes_per_launch": expand_bytes / expand_launches if expand_launches else None,
                 "launches_per_step": expand_launches, "ms_expand_per_step": ms_expand,
                 "ms_expand_per_step_timed_region": ms_expand_timed,
@@ -399,7 +419,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "timing": "CUDA events around every expansion launch of one extra step run right after the "
                           "timed region (host-driven loop); the timed steps themselves run the graph loop and "
                           "report the device %globaltimer span of every launch (achieved_timed_region)",
-                "peak_source": peak_src, "per_unit": per_unit, "traffic_source": traffic_src}
+                "peak_source": peak_src, "per_unit": per_unit, "traffic_source": tr.get("source"),
+                "alu": alu}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, row_ptr, col, thr, args.cpu_samples or None)
@@ -425,6 +446,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "wide_fusion": wide,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
+        "gpu_launches_breakdown": {"host_launches": int(host_launches), "graph_kernel_executions": int(graph_kernels),
+                                   "note": "graph kernels count themselves on the device (Ctl::kernels_run)"},
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

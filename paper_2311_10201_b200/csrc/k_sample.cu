@@ -796,15 +796,15 @@ __device__ __forceinline__ uint32_t philox_ks0(uint32_t x0, uint32_t x1, const u
 
 template <bool kWhole>
 __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, int lane, uint32_t le_mask,
-                                               uint32_t unit, uint32_t rem, uint32_t jc0, uint64_t gblk0,
-                                               unsigned long long& coins, unsigned long long& atoms,
-                                               bool& any_pass) {
+                                               uint32_t unit, uint32_t rem, uint32_t jc0, uint32_t mword,
+                                               uint64_t gblk0, unsigned long long& coins,
+                                               unsigned long long& atoms, bool& any_pass) {
     const uint32_t t0l = unit * (uint32_t)kUnitBm;  // mod 2^32: edge ids are t + delta (mod 2^32)
+    // entry-start words of the unit (prefetched one unit ahead: lane w holds word w)
     uint32_t mw[kWinBm];
 #pragma unroll
-    for (int w = 0; w < kWinBm; ++w) mw[w] = __ldg(&a.umask[(size_t)unit * kWinBm + w]);
-    __syncwarp();
-    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;
+    for (int w = 0; w < kWinBm; ++w) mw[w] = __shfl_sync(kFull, mword, w);
+    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;  // cleared for the next level
     mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
     uint32_t jl[kWinBm];
     uint32_t before = jc0;
@@ -923,13 +923,26 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     const uint32_t nwarps = active * kWarps;
     unsigned long long coins = 0, atoms = 0;
     bool any_pass = false;
-    for (uint32_t unit = blockIdx.x * kWarps + wid; unit < nunits; unit += nwarps) {
-        const uint32_t jc0 = __ldg(&tstart[unit]);
+    // the unit's first entry and entry-start words are loaded one unit ahead (one fewer dependent
+    // round trip per unit)
+    uint32_t unit = blockIdx.x * kWarps + wid;
+    uint32_t nx_t = 0, nx_m = 0;
+    if (unit < nunits) {
+        nx_t = __ldg(&tstart[unit]);
+        nx_m = lane < kWinBm ? a.umask[(size_t)unit * kWinBm + lane] : 0u;
+    }
+    for (; unit < nunits; unit += nwarps) {
+        const uint32_t jc0 = nx_t, mword = nx_m;
+        const uint32_t nxt = unit + nwarps;
+        if (nxt < nunits) {
+            nx_t = __ldg(&tstart[nxt]);
+            nx_m = lane < kWinBm ? a.umask[(size_t)nxt * kWinBm + lane] : 0u;
+        }
         if (unit < nfull)
-            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitBm, jc0, gblk0, coins, atoms, any_pass);
+            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass);
         else
-            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, gblk0,
-                                  coins, atoms, any_pass);
+            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, mword,
+                                  gblk0, coins, atoms, any_pass);
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
     unsigned long long ct = block_sum_ull(coins, red);
