@@ -456,13 +456,15 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     S.store.alloc((size_t)S.blocks * n * 8);  // fully written by the finaliser, no memset
 
     // ---- batch plan
-    // IC: one block per batch keeps the working masks L2-resident; LT: as many as fit (fewer,
-    // longer levels: LT frontiers are thin, per-level overhead dominates)
-    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? 1 : 2048);
     // wide fusion (IC, 64 colours): kWide blocks share one frontier (k_sample.cu "wide fusion")
     const bool wide = S.model == BPT_IC && C == 64 && !opt.batch_groups && (opt.flags & BPT_FLAG_WIDE);
     // touched-bitmap frontier (IC, 64 colours; k_sample.cu "A4: compaction")
     const bool bitmap = S.model == BPT_IC && C == 64 && !wide && !(opt.flags & BPT_FLAG_QUEUE);
+    // IC: a few 64-sample blocks per batch -- the union-layout masks U (8 B per vertex and block) of
+    // 4 blocks are gathered at ~85% L2 hits, and 4x fewer batches cut the per-level and per-batch
+    // fixed costs (C2, theta = 8192: 253 vs 283 ms); the queue form keeps one block
+    // ({V, N} pairs, 16 B). LT: as many as fit (fewer, longer levels: LT frontiers are thin).
+    uint64_t want = opt.batch_groups ? opt.batch_groups : (S.model == BPT_IC ? (bitmap ? 4 : 1) : 2048);
     if (wide) want = kWide;
     uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
     const uint32_t tile = wide ? kUnitWide : expand_unit(S.model, bitmap);
@@ -550,6 +552,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.touched = bitmap ? touched.as<uint32_t>() : nullptr;
     a.tiles = (uint32_t)tiles;
     a.lt_persist = (opt.flags & BPT_FLAG_LT_LEVELS) ? 0 : 1;
+    a.m = g.m;
+    a.umask_words = S.model == BPT_IC ? umask.bytes / 4 : 0;
+    a.tstart_cap = ts_cap;
     a.lt_blocks_per_sm = 1;
 
     const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
@@ -623,6 +628,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     BPT_CUDA(cudaMemcpyAsync(c_host, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
     const Ctl cf = *c_host;
+    if (const uint32_t bad = checks_read_reset())
+        fail(BPT_ECUDA, "device bounds check failed (bits " + std::to_string(bad) + "; k_sample.cu BPT_CHECK ids)");
     if (cf.error == 1) fail(BPT_ENOMEM, "frontier queue overflow; lower batch_groups");
     if (cf.error == 2) fail(BPT_ENOMEM, "level loop exceeded " + std::to_string(kMaxLevels) + " levels");
     const uint32_t rows = (uint32_t)umin64(cf.stats_used, stats_cap);

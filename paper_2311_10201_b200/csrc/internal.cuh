@@ -23,6 +23,18 @@ void check_cuda(cudaError_t e, const char* what);
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
+// Device bounds checks (diagnostic build -DBPT_CHECKS; compute-sanitizer is not available on the
+// GPU pool): a failed check records its id in a device flag instead of trapping, and the API call
+// that ran the kernels fails with BPT_ECUDA naming the check.
+#ifdef BPT_CHECKS
+#define BPT_CHECK(cond, id) \
+    do { if (!(cond)) ::bpt::check_failed(id); } while (0)
+#else
+#define BPT_CHECK(cond, id) do { } while (0)
+#endif
+__device__ void check_failed(uint32_t id);
+uint32_t checks_read_reset();  // host: failed-check bits since the last call (0 in normal builds)
+
 extern uint64_t g_launches;        // kernel launches issued by the host (<<<>>> and cudaGraphLaunch)
 extern uint64_t g_graph_kernels;   // kernel executions inside CUDA graphs, counted on the device
 inline void count_launch(uint64_t k = 1) { g_launches += k; }
@@ -222,6 +234,9 @@ struct BatchArgs {
     // in the VN allocation; new colours of a touched vertex = U & ~V
     uint32_t tiles;           // 1,024-vertex tiles per slot (tile_words = 32 * tiles)
     int lt_persist;           // LT fused loop: one cooperative launch per batch
+    uint64_t m;               // edges (bounds of rec[], checked in BPT_CHECKS builds)
+    uint64_t umask_words;     // words of umask[]
+    uint64_t tstart_cap;      // entries of tstart[]
     int lt_blocks_per_sm;     // ... with this many blocks per SM
 };
 #ifndef BPT_WIDE_BLOCKS

@@ -106,6 +106,26 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
+}  // namespace
+
+__device__ unsigned int g_check_bits;
+__device__ void check_failed(uint32_t id) {
+    if (!(atomicOr(&g_check_bits, 1u << (id & 31)) & (1u << (id & 31))))
+        printf("[bpt] device bounds check %u failed (block %d thread %d)\n", id, blockIdx.x, threadIdx.x);
+}
+uint32_t checks_read_reset() {
+#ifdef BPT_CHECKS
+    unsigned int h = 0, z = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&h, g_check_bits, 4);
+    cudaMemcpyToSymbol(g_check_bits, &z, 4);
+    return h;
+#else
+    return 0;
+#endif
+}
+
+namespace {
 // every kernel of the sampling graph counts its own execution (launch evidence)
 __device__ __forceinline__ void count_self(Ctl* c) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&c->kernels_run, 1ull);
@@ -144,6 +164,7 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), a.k_start);
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
+        BPT_CHECK(start < a.n, 11);
         if (a.touched) {  // bitmap mode: mark the start, the compaction of level 0 finds it
             atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + start, 1ull << bit);
             atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (start >> 5)], 1u << (start & 31));
@@ -176,9 +197,11 @@ constexpr uint32_t kCompTile = kThreads * kCompItems;
 // Touched-bitmap mode (IC, 64 colours): the items are the vertices of 1,024-vertex tiles of each
 // slot; item i of a tile is discovered iff its bit in the bitmap the expansion set is on (bits
 // are cleared as they are read). Same per-item work as a queue entry from then on.
-template <bool kCoh>
-__device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __restrict__ tstart, uint64_t tstart_cap,
-                                             uint32_t unit) {
+// kUnit: work items per expansion unit (a compile-time constant: the unit divisions below are
+// multiplications then -- as a runtime 64-bit divisor they were a quarter of the kernel's instructions)
+template <bool kCoh, uint32_t kUnit>
+__device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __restrict__ tstart, uint64_t tstart_cap) {
+    constexpr uint64_t unit = kUnit;
     LevelRec* L = &a.lv[LDX(&a.ctl->level)];
     const bool bitmap = a.touched != nullptr;
     const uint64_t nraw = bitmap ? (uint64_t)LDX(&a.ctl->slots) * a.tiles * kCompTile : umin64(LDX(&L->raw), a.raw_cap);
@@ -310,9 +333,11 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
                 // IC entries carry delta = rowstart - off (mod 2^32): edge id e = t + delta for
                 // work item t; LT entries carry the vertex itself
                 const uint32_t x = a.model == BPT_IC ? rs[it] - (uint32_t)off : v;
+                BPT_CHECK(qi < a.q_cap && v < a.n && slot < a.slots_max, 9);
                 a.q[qi] = make_uint4(x, slot, (uint32_t)mask[it], (uint32_t)(mask[it] >> 32));
                 if (a.model != BPT_IC) a.qoff[qi] = off;  // IC finds entries via tstart + umask
                 if (a.umask && off / unit < tstart_cap) {
+                    BPT_CHECK((off >> 5) < a.umask_words, 10);
                     if ((off >> 5) != mword) {
                         if (mbits) atomicOr(&a.umask[mword], mbits);
                         mword = off >> 5;
@@ -359,11 +384,12 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
 }
 
 
+template <uint32_t kUnit>
 __global__ void __launch_bounds__(kThreads, 5) k_compact(BatchArgs a, uint32_t* __restrict__ tstart,
-                                                      uint64_t tstart_cap, uint32_t unit) {
+                                                      uint64_t tstart_cap) {
     count_self(a.ctl);
     if (!a.ctl->cont) return;
-    compact_body<false>(a, tstart, tstart_cap, unit);
+    compact_body<false, kUnit>(a, tstart, tstart_cap);
 }
 
 // ------------------------------------------------------------------------ A3: expansion
@@ -779,7 +805,6 @@ struct BmScratch {
     uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
     uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
     unsigned long long pass[32];            // passing colours of the chunk's live items
-    uint32_t excl[32];                      // exclusive prefix of the chunk's task counts
 };
 
 // Philox2x32-10 (reading C-1) with the key schedule k + r * W precomputed in the kernel parameters
@@ -794,8 +819,27 @@ __device__ __forceinline__ uint32_t philox_ks0(uint32_t x0, uint32_t x1, const u
     return x0;
 }
 
+// position of the r-th (0-based) set bit of the 64-bit mask hi:lo: the 32-bit half by one popcount,
+// the byte by SWAR byte popcounts and their prefix sums (compared with r in all bytes at once), the
+// bit inside the byte from a 256-entry table of packed 3-bit positions (shared memory)
+__device__ __forceinline__ uint32_t rank_select64(uint32_t lo, uint32_t hi, uint32_t r, const uint32_t* sel8) {
+    const uint32_t c = __popc(lo);
+    const bool upper = r >= c;
+    const uint32_t w = upper ? hi : lo;
+    if (upper) r -= c;
+    uint32_t t = w - ((w >> 1) & 0x55555555u);
+    t = (t & 0x33333333u) + ((t >> 2) & 0x33333333u);
+    t = (t + (t >> 4)) & 0x0f0f0f0fu;
+    const uint32_t pre = t * 0x01010101u;                             // byte i: set bits in bytes 0..i
+    const uint32_t ge = (((r | 0x80u) * 0x01010101u) - pre) & 0x00808080u;  // bytes i < 3 with pre_i <= r
+    const uint32_t byte = __popc(ge);
+    const uint32_t before = byte ? (pre >> (8 * byte - 8)) & 0xffu : 0u;
+    const uint32_t v = (w >> (8 * byte)) & 0xffu;
+    return (upper ? 32u : 0u) + 8u * byte + ((sel8[v] >> (3 * (r - before))) & 7u);
+}
+
 template <bool kWhole>
-__device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, int lane, uint32_t le_mask,
+__device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane, uint32_t le_mask,
                                                uint32_t unit, uint32_t rem, uint32_t jc0, uint32_t mword,
                                                uint64_t gblk0, unsigned long long& coins,
                                                unsigned long long& atoms, bool& any_pass) {
@@ -815,11 +859,17 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
     }
     uint4 ent[kWinBm];
     uint2 rc[kWinBm];
+    BPT_CHECK((uint64_t)unit * kWinBm + kWinBm <= a.umask_words, 1);
 #pragma unroll
-    for (int w = 0; w < kWinBm; ++w) ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
+    for (int w = 0; w < kWinBm; ++w) {
+        BPT_CHECK(((kWhole || 32u * w + lane < rem) ? jl[w] : jc0) < a.q_cap, 2);
+        ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
+    }
 #pragma unroll
     for (int w = 0; w < kWinBm; ++w) {
         const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        BPT_CHECK((uint32_t)(t0l + i + ent[w].x) < a.m, 3);
+        BPT_CHECK(ent[w].y < a.slots_max, 4);
         rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
     }
     // ---- gather of U[u] = V[u] | N[u] (union layout), live colours, compacted list of live items
@@ -829,6 +879,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
 #pragma unroll
     for (int w = 0; w < kWinBm; ++w) {
         const uint32_t vidx = ent[w].y * a.n + rc[w].x;
+        BPT_CHECK(rc[w].x < a.n, 5);
         const uint2 uu = ld_keep_u64(&U[vidx]);
         uint32_t lo = ent[w].z & ~uu.x;
         uint32_t hi = ent[w].w & ~uu.y;
@@ -837,6 +888,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
         const uint32_t bal = __ballot_sync(kFull, lv);
         if (lv) {
             const uint32_t pos = nlive + __popc(bal & lt_mask);
+            BPT_CHECK(pos < (uint32_t)kUnitBm, 6);
             W.A[pos] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, lo, hi);
             W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,
                                   ent[w].y * a.tiles * 32 + (rc[w].x >> 5), rc[w].x & 31u);
@@ -857,17 +909,21 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
         }
         const uint32_t incl = warp_incl_scan_u32(cnt, lane);
         const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-        W.excl[lane] = incl - cnt;
+        const uint32_t excl = incl - cnt;
         __syncwarp();
         for (uint32_t b = 0; b < ntask; b += 32) {
+            // owner of task b + i = (lanes with excl <= b + i) - 1 (every live item has >= 1 task, so the
+            // excl of the live lanes strictly increase): the lanes below the window by one ballot, the
+            // ranges starting inside it by one OR-reduction -- no search
+            const uint32_t below = __popc(__ballot_sync(kFull, has && excl < b));
+            const uint32_t d = excl - b;
+            const uint32_t starts = __reduce_or_sync(kFull, (has && d < 32u) ? (1u << d) : 0u);
+            const uint32_t o = (below + __popc(starts & le_mask) - 1u) & 31u;
+            const uint32_t eo = __shfl_sync(kFull, excl, o);
             const uint32_t k = b + lane;
             if (k < ntask) {
-                uint32_t o = 0;  // owner = largest lane with excl <= k
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1)
-                    if (W.excl[o + step] <= k) o += step;
                 const uint4 it = W.A[c0 + o];
-                const uint32_t bit = nth_set_bit64(((uint64_t)it.w << 32) | it.z, k - W.excl[o]);
+                const uint32_t bit = rank_select64(it.z, it.w, k - eo, sel8);
                 const uint32_t x = philox_ks0(it.x, W.B[c0 + o].x + bit, a.ic_keys);
                 if ((x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
@@ -880,6 +936,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             if (pass) {
                 const uint4 bb = W.B[j];
                 ++atoms;
+                BPT_CHECK(bb.y < a.slots_max * a.n && bb.z < (uint64_t)a.slots_max * a.tiles * 32 && bb.w < 32, 7);
                 atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + bb.y, pass);
                 atomicOr(&a.touched[bb.z], 1u << bb.w);
                 any_pass = true;
@@ -916,6 +973,14 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
     __shared__ unsigned long long red[kWarps];
+    __shared__ uint32_t sel8[256];  // bit positions of every byte value, 3 bits each (rank_select64)
+    {
+        uint32_t t = 0;
+        for (uint32_t p = 0, j = 0; p < 8; ++p)
+            if ((threadIdx.x >> p) & 1u) t |= p << (3 * j++);
+        sel8[threadIdx.x] = t;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
     const uint32_t nunits = (uint32_t)((total + kUnitBm - 1) / kUnitBm);
@@ -933,15 +998,16 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     }
     for (; unit < nunits; unit += nwarps) {
         const uint32_t jc0 = nx_t, mword = nx_m;
+        BPT_CHECK(unit < a.tstart_cap, 8);
         const uint32_t nxt = unit + nwarps;
         if (nxt < nunits) {
             nx_t = __ldg(&tstart[nxt]);
             nx_m = lane < kWinBm ? a.umask[(size_t)nxt * kWinBm + lane] : 0u;
         }
         if (unit < nfull)
-            expand_unit_bm<true>(a, W, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass);
+            expand_unit_bm<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass);
         else
-            expand_unit_bm<false>(a, W, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, mword,
+            expand_unit_bm<false>(a, W, sel8, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, mword,
                                   gblk0, coins, atoms, any_pass);
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
@@ -982,6 +1048,7 @@ __global__ void k_init_w(BatchArgs a, cudaGraphConditionalHandle h_level, int us
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), a.k_start);
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
+        BPT_CHECK(start < a.n, 11);
         const unsigned long long old = atomicOr(&a.VN[(size_t)start * kWide + b].y, 1ull << bit);
         if (old == 0 && atomicOr(&a.vflag[start], 1u) == 0) {
             const unsigned pos = atomicAdd(&a.lv[0].raw, 1u);
@@ -1813,7 +1880,7 @@ __global__ void __launch_bounds__(kThreads) k_levels_lt(BatchArgs a, uint32_t* _
                                                       uint64_t tstart_cap) {
     count_self(a.ctl);
     while (__ldcg(&a.ctl->cont)) {
-        compact_body<true>(a, tstart, tstart_cap, kTile);
+        compact_body<true, kTile>(a, tstart, tstart_cap);
         grid_barrier(a.ctl);
         expand_lt_body<true>(a, tstart, (cudaGraphConditionalHandle)0, 0);
         grid_barrier(a.ctl);
@@ -1902,6 +1969,13 @@ void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, ui
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_lists");
 }
 
+// the compaction instance whose unit matches the expansion of this batch
+using CompactFn = void (*)(BatchArgs, uint32_t*, uint64_t);
+static CompactFn compact_kernel(const BatchArgs& a) {
+    if (a.model != BPT_IC) return k_compact<kTile>;
+    return a.touched ? k_compact<kUnitBm> : k_compact<kUnitIC>;
+}
+
 uint32_t expand_unit(int model, bool bitmap) {
     return model == BPT_IC ? (bitmap ? (uint32_t)kUnitBm : (uint32_t)kUnitIC) : kTile;
 }
@@ -1936,7 +2010,7 @@ int expand_grid() {
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pl, k_levels_lt, kThreads, sizeof(SmemTile)));
         g_levels_per_sm_lt = per_sm_pl > 0 ? per_sm_pl : 1;
         int per_sm_c = 0;
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact, kThreads, 0));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, k_compact<kUnitBm>, kThreads, 0));
         g_compact_grid = num_sms() * (per_sm_c > 0 ? per_sm_c : 1);
     }
     return g_expand_grid;
@@ -1977,7 +2051,7 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
         ::bpt::check_cuda(cudaGetLastError(), "launch wide level kernels");
         return;
     }
-    k_compact<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap, expand_unit(a.model, a.touched != nullptr));
+    compact_kernel(a)<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap);
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
     if (a.model == BPT_IC && a.touched)
         k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
@@ -2066,12 +2140,11 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     cudaGraphNode_t n_level;
     BPT_CUDA(cudaGraphAddNode(&n_level, body, &n_init, 1, &cl));
     cudaGraph_t lbody = cl.conditional.phGraph_out[0];
-    uint32_t unit = expand_unit(a.model, a.touched != nullptr);
-    void* cmp_args[] = {&args, &tstart, &tstart_cap, &unit};
+    void* cmp_args[] = {&args, &tstart, &tstart_cap};
     void* cmpw_args[] = {&args, &tstart, &tstart_cap};
     cudaGraphNode_t n_cmp = a.wide
         ? add_kernel(lbody, nullptr, (void*)k_compact_w, dim3(g_compact_grid), dim3(kThreads), 0, cmpw_args)
-        : add_kernel(lbody, nullptr, (void*)k_compact, dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
+        : add_kernel(lbody, nullptr, (void*)compact_kernel(a), dim3(g_compact_grid), dim3(kThreads), 0, cmp_args);
     void* exp_args[] = {&args, &tstart, &h_level, &one};
     cudaGraphNode_t n_exp = a.wide
         ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),

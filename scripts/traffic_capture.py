@@ -1,8 +1,8 @@
 """Like-for-like DRAM traffic of the IC expansion (roofline `traffic`), for bench.py.
 
-Runs batch 0 of the bench's C2 step -- the first 64-sample group (samples 0..63, the bench's first
-sampling seed), batch_groups = 1 exactly as bench.py launches it -- through the host-driven level
-loop, and writes every level's counters to gpurun_out/traffic_levels.json. Run it under
+Runs batch 0 of the bench's C2 step -- its first four 64-sample blocks (samples 0..255, the bench's
+first sampling seed, the automatic batch of 4 blocks exactly as bench.py launches it) -- through the
+host-driven level loop, and writes every level's counters to gpurun_out/traffic_levels.json. Run it under
   ncu --set full -k regex:k_expand_bm -o gpurun_out/traffic_full python scripts/traffic_capture.py
 then `python scripts/traffic_capture.py --summarize` (here, no GPU) pairs launch i with level i and
 writes profiles/expand_traffic.json (per launch the DRAM bytes next to the algorithmic bytes of the
@@ -37,7 +37,7 @@ def capture():
     torch.cuda.set_device(0)
     row_ptr, col, thr = graphgen.make_graph(cfg)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
-    s = g.sample(64, colors=64, seed=cfg.seed, batch_groups=1, profile=True, poll_levels=1)
+    s = g.sample(256, colors=64, seed=cfg.seed, profile=True, poll_levels=1)  # batch 0 = 4 blocks
     rows = s.level_stats().tolist()
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, "traffic_levels.json"), "w") as f:
@@ -87,8 +87,8 @@ def summarize():
     edges = sum(p["edges"] for p in per)
     us = sum(p["us"] for p in per) or 1.0
     wavg = lambda k: sum((p[k] or 0) * p["us"] for p in per) / us  # time-weighted
-    src = ("ncu --set full of every k_expand_bm launch of batch 0 of the bench step (C2, samples 0..63, bench seed, "
-           "batch_groups = 1, host-driven level loop; scripts/traffic_capture.py)")
+    src = ("ncu --set full of every k_expand_bm launch of batch 0 of the bench step (C2, samples 0..255 = 4 blocks, "
+           "bench seed, automatic batch, host-driven level loop; scripts/traffic_capture.py)")
     res = {"source": src, "kernel": seq[0].get("Kernel Name") if seq else None, "launches": n,
            "dram_bytes_per_launch": dram / n if n else None, "algorithmic_bytes_per_launch": algs / n if n else None,
            "dram_over_algorithmic": dram / algs if algs else None, "per_launch": per}
