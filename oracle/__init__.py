@@ -62,6 +62,8 @@ def lib():
     L.or_sample_many.restype = _i
     L.or_group_work.argtypes = [_p, _u64, _u64, _u64, _p, _p, _p, _p, _u32]
     L.or_group_work.restype = _i
+    L.or_group_work_ids.argtypes = [_p, _u64, _p, _u64, _p, _p, _p, _p, _u32]
+    L.or_group_work_ids.restype = _i
     L.or_greedy.argtypes = [_u32, _u64, _p, _p, _u32, _i, _p, _p]
     L.or_greedy.restype = _i
     L.or_sigma_hat.argtypes = [_u32, _u64, _u64]
@@ -178,6 +180,17 @@ class Graph:
         mem = np.empty(int(offsets[-1]), dtype=np.uint32)
         lib().or_sample_many(self._h, seed, _ptr(ids), cnt, t, None, None, None, _ptr(offsets), _ptr(mem))
         return sizes, digests, elog, offsets, mem
+
+    def group_work_ids(self, seed: int, ids, cap: int = 4096):
+        """group_work of a traversal group of arbitrary sample ids."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        ep = np.zeros(1, dtype=np.uint64)
+        el = np.zeros(1, dtype=np.uint64)
+        lv = np.zeros(1, dtype=np.uint32)
+        fr = np.zeros(cap, dtype=np.uint64)
+        lib().or_group_work_ids(self._h, seed, _ptr(ids), ids.shape[0], _ptr(ep), _ptr(el), _ptr(lv), _ptr(fr), cap)
+        return {"e_phys": int(ep[0]), "e_logical": int(el[0]), "levels": int(lv[0]),
+                "frontier": fr[: int(lv[0])].copy()}
 
     def group_work(self, seed: int, s0: int, s1: int, cap: int = 4096):
         ep = np.zeros(1, dtype=np.uint64)

@@ -324,14 +324,29 @@ int or_sample_many(const or_graph* g, uint64_t seed, const uint64_t* ids, uint64
  * Outputs: *e_phys, *e_logical (sum of the unfused reads), *levels (number of non-empty
  * levels), frontier[0..levels) (if frontier != NULL and levels <= cap).
  * ---------------------------------------------------------------------------------- */
+/* The same for a traversal group of arbitrary sample ids (slots sorted by
+ * start vertex form groups of non-consecutive samples; the definition is unchanged). */
+int or_group_work_ids(const or_graph* g, uint64_t seed, const uint64_t* ids, uint64_t count,
+                      uint64_t* e_phys, uint64_t* e_logical, uint32_t* levels, uint64_t* frontier, uint32_t cap);
+
 int or_group_work(const or_graph* g, uint64_t seed, uint64_t s0, uint64_t s1,
                   uint64_t* e_phys, uint64_t* e_logical, uint32_t* levels, uint64_t* frontier, uint32_t cap) {
+    uint64_t* ids = (uint64_t*)malloc((s1 > s0 ? s1 - s0 : 1) * sizeof(uint64_t));
+    for (uint64_t s = s0; s < s1; s++) ids[s - s0] = s;
+    int r = or_group_work_ids(g, seed, ids, s1 > s0 ? s1 - s0 : 0, e_phys, e_logical, levels, frontier, cap);
+    free(ids);
+    return r;
+}
+
+int or_group_work_ids(const or_graph* g, uint64_t seed, const uint64_t* ids, uint64_t count,
+                      uint64_t* e_phys, uint64_t* e_logical, uint32_t* levels, uint64_t* frontier, uint32_t cap) {
     or_keys k = keys_of(seed);
     or_scratch w; scratch_init(&w, g->n);
     uint64_t npairs = 0, cap_pairs = 1024;
     uint64_t* pairs = (uint64_t*)malloc(cap_pairs * sizeof(uint64_t));
     uint64_t elog_total = 0, lt_total = 0;
-    for (uint64_t s = s0; s < s1; s++) {
+    for (uint64_t i = 0; i < count; i++) {
+        uint64_t s = ids[i];
         uint64_t el = 0;
         uint32_t size = run_sample(g, &k, s, &w, &el);
         elog_total += el; lt_total += size;

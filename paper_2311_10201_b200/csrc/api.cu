@@ -539,6 +539,16 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.stats_cap = stats_cap;
     a.slots_max = (uint32_t)slots;
     a.blocks = S.blocks;
+    // sorted start vertices (IC touched-bitmap form; k_order.cu)
+    S.sorted = bitmap && !(opt.flags & BPT_FLAG_UNSORTED);
+    if (S.sorted) {
+        S.slot_sample.alloc(nlocal * 4);
+        S.sample_slot.alloc(nlocal * 4);
+        sort_slots(g.roff.as<uint32_t>(), n, S.s0, nlocal, stream_key(S.seed, kTagStart), S.slot_sample.as<uint32_t>(),
+                   S.sample_slot.as<uint32_t>(), st);
+    }
+    a.slot_sample = S.sorted ? S.slot_sample.as<uint32_t>() : nullptr;
+    a.nlocal = nlocal;
     a.ctl = ctl.as<Ctl>();
     a.theta = S.theta;
     a.k_ic = stream_key(S.seed, kTagIC);
@@ -1005,6 +1015,13 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
             BPT_CUDA(cudaMemcpyAsync(members, S.list_mem.as<uint32_t>() + b, total * 4, cudaMemcpyDefault, st));
             BPT_CUDA(cudaStreamSynchronize(st));
         } else if (total) {
+            Samples& M = const_cast<Samples&>(S);
+            if (M.sorted && M.h_sample_slot.empty()) {  // sample -> slot map on the host, once per handle
+                M.h_sample_slot.resize(M.s1 - M.s0);
+                BPT_CUDA(cudaMemcpyAsync(M.h_sample_slot.data(), M.sample_slot.p, (M.s1 - M.s0) * 4,
+                                         cudaMemcpyDeviceToHost, st));
+                BPT_CUDA(cudaStreamSynchronize(st));
+            }
             DevBuf tmp;
             uint32_t* dm = members;
             if (!is_device_ptr(members)) { tmp.alloc(total * 4); dm = tmp.as<uint32_t>(); }

@@ -154,6 +154,13 @@ struct Samples {
     // lists (list_off, list_mem); the selection uses a vertex -> samples index built on demand
     bool sparse = false;
     DevBuf inv_off, inv_s;
+    // sorted start vertices (k_order.cu): the traversal slots (64 * local block + bit) hold the
+    // samples in start order; store, per-slot kernels and selection work in slot order, every
+    // per-sample output is mapped through these (identity when `sorted` is false)
+    bool sorted = false;
+    DevBuf slot_sample;   // u32[nlocal]: global sample id of local slot j
+    DevBuf sample_slot;   // u32[nlocal]: local slot of local sample i
+    std::vector<uint32_t> h_sample_slot;  // host copy, on demand (extraction)
     // multi-rank sparse selection: every rank's lists gathered once (offsets over all ranks'
     // samples, padded members, global occurrence counts)
     DevBuf g_off, g_mem, g_count0;
@@ -234,6 +241,9 @@ struct BatchArgs {
     // in the VN allocation; new colours of a touched vertex = U & ~V
     uint32_t tiles;           // 1,024-vertex tiles per slot (tile_words = 32 * tiles)
     int lt_persist;           // LT fused loop: one cooperative launch per batch
+    const uint32_t* slot_sample;  // sorted start vertices: global sample id of each local slot (nullptr:
+                                  // slot 64 * local block + bit holds sample 64 * global block + bit)
+    uint64_t nlocal;          // local samples
     uint64_t m;               // edges (bounds of rec[], checked in BPT_CHECKS builds)
     uint64_t umask_words;     // words of umask[]
     uint64_t tstart_cap;      // entries of tstart[]
@@ -285,6 +295,9 @@ void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, 
 void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
                           uint32_t k_start, uint32_t k_lt, const uint32_t* sizes, const uint64_t* off,
                           uint32_t* members, cudaStream_t st);
+// k_order.cu: sorted start vertices
+void sort_slots(const uint32_t* roff, uint32_t n, uint64_t s0, uint64_t nlocal, uint32_t k_start,
+                uint32_t* slot_sample, uint32_t* sample_slot, cudaStream_t st);
 cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, const StoreHook& h);
 // k_select.cu
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st);

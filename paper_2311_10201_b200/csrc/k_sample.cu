@@ -165,6 +165,18 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
         const uint64_t r64 = ((uint64_t)w.y << 32) | w.x;
         const uint32_t start = (uint32_t)__umul64hi(r64, (uint64_t)a.n);
         BPT_CHECK(start < a.n, 11);
+        if (a.touched && a.slot_sample) {  // sorted start vertices: the slot holds another sample
+            const uint64_t li = 64ull * (a.ctl->blk0 + slot) + bit;
+            if (li >= a.nlocal) continue;
+            const uint32_t ss = a.slot_sample[li];
+            const uint2 w2 = philox2x32_10(ss, 0u, a.k_start);
+            const uint32_t st2 = (uint32_t)__umul64hi(((uint64_t)w2.y << 32) | w2.x, (uint64_t)a.n);
+            BPT_CHECK(st2 < a.n, 12);
+            atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + st2, 1ull << bit);
+            atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (st2 >> 5)], 1u << (st2 & 31));
+            a.lv[0].any = 1;
+            continue;
+        }
         if (a.touched) {  // bitmap mode: mark the start, the compaction of level 0 finds it
             atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + start, 1ull << bit);
             atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (start >> 5)], 1u << (start & 31));
@@ -890,7 +902,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             const uint32_t pos = nlive + __popc(bal & lt_mask);
             BPT_CHECK(pos < (uint32_t)kUnitBm, 6);
             W.A[pos] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, lo, hi);
-            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,
+            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,  // colour-0 sample / slot
                                   ent[w].y * a.tiles * 32 + (rc[w].x >> 5), rc[w].x & 31u);
         }
         nlive += __popc(bal);
@@ -924,7 +936,8 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             if (k < ntask) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select64(it.z, it.w, k - eo, sel8);
-                const uint32_t x = philox_ks0(it.x, W.B[c0 + o].x + bit, a.ic_keys);
+                const uint32_t sid = W.B[c0 + o].x + bit;  // slot index (sorted) or sample id
+                const uint32_t x = philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys);
                 if ((x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
@@ -955,7 +968,9 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     if (!a.ctl->cont) return;
     Ctl* ctl = a.ctl;
     const uint32_t level = ctl->level;
-    const uint64_t gblk0 = ctl->gblk0;
+    // colour 0 of slot k is sample 64 * (gblk0 + k) -- or, with sorted start vertices, local slot
+    // 64 * (blk0 + k), mapped through slot_sample
+    const uint64_t gblk0 = a.slot_sample ? ctl->blk0 : ctl->gblk0;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
     const unsigned long long packed = L->packed;

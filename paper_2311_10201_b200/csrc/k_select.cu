@@ -192,6 +192,12 @@ static bool build_lists(const Samples& S, cudaStream_t st) {
     if (nlocal == 0 || bytes > free_b / 4 || bytes * 8 > S.store.bytes) return M.lists_ok = false;
     std::vector<uint32_t> sz(nlocal);
     BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
+    if (S.sorted) {  // the lists follow the store: one per slot (the slot's sample's size)
+        std::vector<uint32_t> slot_sample(nlocal), by_slot(nlocal);
+        BPT_CUDA(cudaMemcpy(slot_sample.data(), S.slot_sample.p, nlocal * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t j = 0; j < nlocal; ++j) by_slot[j] = sz[slot_sample[j] - S.s0];
+        sz.swap(by_slot);
+    }
     std::vector<uint64_t> off(nlocal + 1, 0);
     for (uint64_t i = 0; i < nlocal; ++i) off[i + 1] = off[i] + sz[i];
     M.list_off.alloc((nlocal + 1) * 8);

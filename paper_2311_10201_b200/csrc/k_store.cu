@@ -1,6 +1,9 @@
 // k_store.cu -- A5 RRR store finalisation (sizes, digests, E_logical, occurrence counts)
 // and A6 RRR extraction (Listing 1 lines 18-21: "for vertex v, for colour c,
 // if visited[v].c: RRRset(c).add(v)") as an ordered, atomic-free mask -> list transpose.
+#include <cstring>
+#include <map>
+
 #include "internal.cuh"
 
 namespace bpt {
@@ -34,7 +37,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
                                                           uint64_t nlocal, uint32_t* __restrict__ sizes,
                                                           unsigned long long* __restrict__ elog_total,
                                                           uint32_t* __restrict__ count0, int single_slot,
-                                                          uint32_t vstride, uint64_t sstride, int umode) {
+                                                          uint32_t vstride, uint64_t sstride, int umode,
+                                                          const uint32_t* __restrict__ slot_sample, uint64_t s0) {
     constexpr int kW = kFinThreads / 32;
     __shared__ unsigned long long s_mask[kW][32];
     __shared__ uint32_t s_size[kW][64];
@@ -110,8 +114,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
         const int c = threadIdx.x;
         uint32_t S = 0;
         for (int q = 0; q < kW; ++q) S += s_size[q][c];
-        const uint64_t li = 64ull * blk + c;  // local sample index
-        if (li < nlocal && S) atomicAdd(&sizes[li], S);
+        const uint64_t li = 64ull * blk + c;  // local slot = local sample index unless start-sorted
+        if (li < nlocal && S) atomicAdd(&sizes[slot_sample ? slot_sample[li] - s0 : li], S);
     }
     if (threadIdx.x == 0) {
         unsigned long long E = 0;
@@ -125,7 +129,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
 // over vertices [r*chunk, (r+1)*chunk) of local block g.
 __global__ void __launch_bounds__(kFinThreads) k_digests(const uint64_t* __restrict__ store, uint32_t n,
                                                          uint64_t chunk, uint64_t nlocal,
-                                                         unsigned long long* __restrict__ digests) {
+                                                         unsigned long long* __restrict__ digests,
+                                                         const uint32_t* __restrict__ slot_sample, uint64_t s0) {
     constexpr int kW = kFinThreads / 32;
     __shared__ unsigned long long s_mask[kW][32];
     __shared__ unsigned long long s_mix[kW][32];
@@ -160,8 +165,8 @@ __global__ void __launch_bounds__(kFinThreads) k_digests(const uint64_t* __restr
         const int c = threadIdx.x;
         unsigned long long D = 0;
         for (int q = 0; q < kW; ++q) D += s_dig[q][c];
-        const uint64_t li = 64ull * blk + c;
-        if (li < nlocal && D) atomicAdd(&digests[li], D);
+        const uint64_t li = 64ull * blk + c;  // local slot (relative to this launch's first block)
+        if (li < nlocal && D) atomicAdd(&digests[slot_sample ? slot_sample[li] - s0 : li], D);
     }
 }
 
@@ -170,8 +175,8 @@ __global__ void __launch_bounds__(kFinThreads) k_digests(const uint64_t* __restr
 constexpr int kExRounds = 32;
 constexpr uint32_t kExTile = 32 * kExRounds;
 
-// pass 1: per-(colour, tile) member counts, colour-major; colours outside [c_lo, c_hi) = 0
-__global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint32_t c_lo, uint32_t c_hi,
+// pass 1: per-(colour, tile) member counts, colour-major; colours outside the requested set cm = 0
+__global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint64_t cm,
                                 uint32_t ntiles, uint32_t* __restrict__ tcnt) {
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -181,39 +186,43 @@ __global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint
         const uint64_t v = tile * kExTile + (uint64_t)r * 32 + lane;
         const uint64_t m = v < n ? V[v] : 0ull;
         if (!__any_sync(kFull, m != 0)) continue;
-        for (uint32_t c = c_lo; c < c_hi; ++c) {
+        for (uint64_t mm = cm; mm; mm &= mm - 1) {
+            const uint32_t c = __ffsll((long long)mm) - 1;
             const uint32_t b = __ballot_sync(kFull, (m >> c) & 1ull);
             if (lane == (int)(c & 31)) { if (c < 32) cnt_lo += __popc(b); else cnt_hi += __popc(b); }
         }
     }
-    if (lane >= (int)c_lo && lane < (int)c_hi) tcnt[(uint64_t)lane * ntiles + tile] = cnt_lo;
-    else tcnt[(uint64_t)lane * ntiles + tile] = 0;
+    tcnt[(uint64_t)lane * ntiles + tile] = ((cm >> lane) & 1ull) ? cnt_lo : 0;
     const uint32_t c2 = lane + 32;
-    tcnt[(uint64_t)c2 * ntiles + tile] = (c2 >= c_lo && c2 < c_hi) ? cnt_hi : 0;
+    tcnt[(uint64_t)c2 * ntiles + tile] = ((cm >> c2) & 1ull) ? cnt_hi : 0;
 }
 
-// pass 2: ordered scatter; tpos = exclusive colour-major scan of tcnt (position inside the
-// group's output slab, colours in ascending order, vertices ascending within a colour)
-__global__ void k_extract_write(const uint64_t* __restrict__ V, uint32_t n, uint32_t c_lo, uint32_t c_hi,
-                                uint32_t ntiles, const uint32_t* __restrict__ tpos, uint64_t out_base,
+// pass 2: ordered scatter; tpos = exclusive colour-major scan of tcnt; colour c's members go to
+// cbase[c] + (its members in earlier tiles) + rank, vertices ascending (reading C-10)
+__global__ void k_extract_write(const uint64_t* __restrict__ V, uint32_t n, uint64_t cm,
+                                uint32_t ntiles, const uint32_t* __restrict__ tpos, const uint64_t* __restrict__ cbase,
                                 uint32_t* __restrict__ members) {
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     if (tile >= ntiles) return;
-    uint32_t pos_lo = tpos[(uint64_t)lane * ntiles + tile];
-    uint32_t pos_hi = tpos[(uint64_t)(lane + 32) * ntiles + tile];
+    // positions relative to the colour's first tile, plus the caller's offset of that colour's sample
+    uint64_t pos_lo = ((cm >> lane) & 1ull) ? cbase[lane] + tpos[(uint64_t)lane * ntiles + tile] -
+                                                  tpos[(uint64_t)lane * ntiles] : 0;
+    uint64_t pos_hi = ((cm >> (lane + 32)) & 1ull) ? cbase[lane + 32] + tpos[(uint64_t)(lane + 32) * ntiles + tile] -
+                                                         tpos[(uint64_t)(lane + 32) * ntiles] : 0;
     const uint32_t lt = (1u << lane) - 1u;
     for (int r = 0; r < kExRounds; ++r) {
         const uint64_t v = tile * kExTile + (uint64_t)r * 32 + lane;
         const uint64_t m = v < n ? V[v] : 0ull;
         if (!__any_sync(kFull, m != 0)) continue;
-        for (uint32_t c = c_lo; c < c_hi; ++c) {
+        for (uint64_t mm = cm; mm; mm &= mm - 1) {
+            const uint32_t c = __ffsll((long long)mm) - 1;
             const bool has = (m >> c) & 1ull;
             const uint32_t b = __ballot_sync(kFull, has);
             if (!b) continue;
             const uint32_t src_lane = c & 31;
-            const uint32_t p = __shfl_sync(kFull, c < 32 ? pos_lo : pos_hi, src_lane);
-            if (has) members[out_base + p + __popc(b & lt)] = (uint32_t)v;
+            const uint64_t p = __shfl_sync(kFull, c < 32 ? pos_lo : pos_hi, src_lane);
+            if (has) members[p + __popc(b & lt)] = (uint32_t)v;
             if (lane == (int)src_lane) { if (c < 32) pos_lo += __popc(b); else pos_hi += __popc(b); }
         }
     }
@@ -265,7 +274,8 @@ void compute_digests(const Samples& S, cudaStream_t st) {
         const uint64_t nb = umin64(65535, S.blocks - b0);
         k_digests<<<dim3((unsigned)ranges, (unsigned)nb), kFinThreads, 0, st>>>(
             S.store.as<uint64_t>() + (size_t)b0 * S.n, S.n, chunk, nlocal - 64 * b0,
-            S.digests.as<unsigned long long>() + 64 * b0);
+            S.sorted ? S.digests.as<unsigned long long>() : S.digests.as<unsigned long long>() + 64 * b0,
+            S.sorted ? S.slot_sample.as<uint32_t>() + 64 * b0 : nullptr, S.s0);
         count_launch();
     }
     ::bpt::check_cuda(cudaGetLastError(), "launch k_digests");
@@ -278,7 +288,8 @@ void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t 
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
                                              S.sizes.as<uint32_t>(), d_elog,
                                              S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0,
-                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n, umode ? 1 : 0);
+                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n, umode ? 1 : 0,
+                                             S.sorted ? S.slot_sample.as<uint32_t>() : nullptr, S.s0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
 }
@@ -298,8 +309,10 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     uint32_t vstride = wide ? kWide : 1u;
     uint64_t sstride = wide ? 1 : (uint64_t)n;
     int um = umode ? 1 : 0;
+    const uint32_t* slot_sample = S.sorted ? S.slot_sample.as<uint32_t>() : nullptr;
+    uint64_t s0 = S.s0;
     void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog,
-                        &count0, &single, &vstride, &sstride, &um};
+                        &count0, &single, &vstride, &sstride, &um, (void*)&slot_sample, &s0};
     cudaKernelNodeParams p{};
     p.func = (void*)k_finalize;
     p.gridDim = grid;
@@ -313,18 +326,31 @@ void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint6
                    cudaStream_t st) {
     const uint32_t n = S.n;
     const uint32_t ntiles = (uint32_t)((n + kExTile - 1) / kExTile);
-    DevBuf tcnt((uint64_t)64 * ntiles * 4), tmp(scan_temp_bytes((uint64_t)64 * ntiles));
-    const uint64_t lfirst = first - S.s0, llast = lfirst + count;  // local sample indices
-    for (uint64_t blk = lfirst / 64; blk * 64 < llast; ++blk) {
-        const uint32_t c_lo = (uint32_t)(umax64(lfirst, blk * 64) - blk * 64);
-        const uint32_t c_hi = (uint32_t)(umin64(llast, blk * 64 + 64) - blk * 64);
-        const uint64_t out_base = h_offsets[blk * 64 + c_lo - lfirst];
-        const uint64_t* V = S.store.as<uint64_t>() + (size_t)blk * n;
-        const unsigned grid = (unsigned)(((uint64_t)ntiles * 32 + 255) / 256);
-        k_extract_count<<<grid, 256, 0, st>>>(V, n, c_lo, c_hi, ntiles, tcnt.as<uint32_t>());
+    const uint64_t lfirst = first - S.s0;  // local sample index of `first`
+    // the store's blocks holding the requested samples: per block the colour (slot bit) set and
+    // each colour's output offset (slots are the samples themselves unless start-sorted)
+    struct Blk { uint64_t mask = 0; uint64_t base[64]; };
+    std::map<uint64_t, Blk> blocks;
+    for (uint64_t i = 0; i < count; ++i) {
+        const uint64_t slot = S.sorted ? S.h_sample_slot[lfirst + i] : lfirst + i;
+        Blk& b = blocks[slot / 64];
+        b.mask |= 1ull << (slot % 64);
+        b.base[slot % 64] = h_offsets[i];
+    }
+    std::vector<uint64_t> hbase(blocks.size() * 64, 0);
+    size_t bi = 0;
+    for (auto& kv : blocks) memcpy(&hbase[64 * bi++], kv.second.base, sizeof(kv.second.base));
+    DevBuf tcnt((uint64_t)64 * ntiles * 4), tmp(scan_temp_bytes((uint64_t)64 * ntiles)), dbase(hbase.size() * 8);
+    BPT_CUDA(cudaMemcpyAsync(dbase.p, hbase.data(), hbase.size() * 8, cudaMemcpyHostToDevice, st));
+    const unsigned grid = (unsigned)(((uint64_t)ntiles * 32 + 255) / 256);
+    bi = 0;
+    for (auto& kv : blocks) {
+        const uint64_t* V = S.store.as<uint64_t>() + (size_t)kv.first * n;
+        k_extract_count<<<grid, 256, 0, st>>>(V, n, kv.second.mask, ntiles, tcnt.as<uint32_t>());
         count_launch();
         exclusive_scan_u32(tcnt.as<uint32_t>(), tcnt.as<uint32_t>(), (uint64_t)64 * ntiles, tmp.p, st);
-        k_extract_write<<<grid, 256, 0, st>>>(V, n, c_lo, c_hi, ntiles, tcnt.as<uint32_t>(), out_base, d_members);
+        k_extract_write<<<grid, 256, 0, st>>>(V, n, kv.second.mask, ntiles, tcnt.as<uint32_t>(),
+                                              dbase.as<uint64_t>() + 64 * bi++, d_members);
         count_launch();
         ::bpt::check_cuda(cudaGetLastError(), "launch k_extract_write");
     }

@@ -46,7 +46,9 @@ def test_c2_full_theta(bpt, c2):
     sample's size and digest, seeds / gains / sigma_hat of k = 50, E_logical, and per group the
     E_phys and the per-level frontier sizes equal the oracle's."""
     cfg, row_ptr, col, thr, gold, g = c2
-    s = g.sample(cfg.theta, colors=64, seed=cfg.seed)
+    # consecutive-sample groups here (the golden group work is of those groups); the default
+    # sorted start vertices are checked in test_c2_full_sorted_start_vertices
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED)
     assert np.array_equal(s.sizes(0, cfg.theta), gold["sizes"])
     assert np.array_equal(s.digests(0, cfg.theta), gold["digests"])
     info = s.info
@@ -84,10 +86,44 @@ def test_c2_full_theta(bpt, c2):
     s.close()
 
 
+def test_c2_full_sorted_start_vertices(bpt, c2):
+    """The bench's launch configuration (sorted start vertices, the default): all 65,536 sizes and
+    digests, seeds, gains, sigma_hat and E_logical equal the oracle's; the groups differ, so E_phys
+    equals the oracle's group work of the sorted groups (golden c2_sorted_oracle.npz) and is below
+    the consecutive-group value."""
+    cfg, row_ptr, col, thr, gold, g = c2
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed)
+    assert np.array_equal(s.sizes(0, cfg.theta), gold["sizes"])
+    assert np.array_equal(s.digests(0, cfg.theta), gold["digests"])
+    info = s.info
+    assert info["e_logical"] == int(gold["e_logical"])
+    assert info["e_phys"] < int(gold["e_phys"].sum())
+    sgold = os.path.join(GOLD, "c2_sorted_oracle.npz")
+    if os.path.exists(sgold):
+        sg = np.load(sgold)
+        assert info["e_phys"] == int(sg["e_phys"].sum())
+        B = info["batch_groups"]
+        rows = s.level_stats()
+        nb = (len(sg["e_phys"]) + B - 1) // B
+        want = np.zeros(nb, np.uint64)
+        np.add.at(want, np.arange(len(sg["e_phys"])) // B, sg["e_phys"])
+        assert np.array_equal(_per_batch(rows, 4, nb), want)
+    seeds, gains, sigma = s.select_seeds(cfg.k)
+    assert np.array_equal(seeds, gold["seeds"]) and np.array_equal(gains, gold["gains"])
+    assert sigma == float(gold["sigma"])
+    og = oracle.Graph(row_ptr, col, w_q31=thr)
+    ids = np.array([0, 63, 4097, cfg.theta - 1], dtype=np.uint64)
+    _, _, _, off, mem = og.sample_many(cfg.seed, ids, members=True)
+    for j, i in enumerate(ids):
+        o, m = s.extract(int(i), 1)
+        assert np.array_equal(m, mem[off[j]:off[j + 1]])
+    s.close()
+
+
 def test_c2_full_graph_theta_2048(bpt, c2):
     """The C2 graph with theta = 2,048 (32 groups): sizes, digests, seeds, gains, sigma_hat."""
     cfg, row_ptr, col, thr, gold, g = c2
-    s = g.sample(2048, colors=64, seed=cfg.seed)
+    s = g.sample(2048, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED)
     assert np.array_equal(s.sizes(0, 2048), gold["sizes"][:2048])
     assert np.array_equal(s.digests(0, 2048), gold["digests"][:2048])
     assert s.info["e_phys"] == int(gold["e_phys"][:32].sum())

@@ -34,6 +34,21 @@ def oracle_all(row_ptr, col, thr, model, theta, seed, colors=64, k=None, threads
     return out
 
 
+def sorted_slots(row_ptr, col, n, theta, seed, s0=0):
+    """Traversal order of the samples [s0, theta) under sorted start vertices (include/bpt.h
+    BPT_FLAG_UNSORTED): start in-degree descending, then start id, then
+    sample id -- computed here from the oracle's start vertices and the forward CSR."""
+    ids = np.arange(s0, theta, dtype=np.int64)
+    starts = np.array([oracle.start_vertex(int(s), n, seed) for s in ids], dtype=np.int64)
+    indeg = np.bincount(col.astype(np.int64), minlength=n)
+    return ids[np.lexsort((ids, starts, -indeg[starts]))]
+
+
+def group_e_phys(og, seed, order, group):
+    """E_phys of traversal groups of `group` consecutive samples of `order`."""
+    return [og.group_work_ids(seed, order[i:i + group]) for i in range(0, len(order), group)]
+
+
 def check_full(bpt, s, ref, theta):
     assert np.array_equal(s.sizes(0, theta), ref["sizes"])
     assert np.array_equal(s.digests(0, theta), ref["digests"])
@@ -261,8 +276,11 @@ def test_c1_full_parity(bpt, colors):
         assert sigma == oracle.sigma_hat(cfg.n, int(ref["gains"].sum()), cfg.theta)
         info = s.info
         # exact work counters: E_phys = sum over traversal groups of the
-        # distinct (v, level) pairs weighted by in-degree; E_logical = unfused reads
-        e_phys = sum(ref["g"].group_work(cfg.seed, a, a + colors)["e_phys"] for a in range(0, cfg.theta, colors))
+        # distinct (v, level) pairs weighted by in-degree; E_logical = unfused reads. With 64
+        # colours the groups are 64 samples in sorted start order (BPT_FLAG_UNSORTED off)
+        order = (sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed) if colors == 64
+                 else np.arange(cfg.theta))
+        e_phys = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, colors))
         assert info["e_phys"] == e_phys
         assert info["e_logical"] == int(ref["elog"].sum())
         assert info["members"] == int(ref["sizes"].sum())
@@ -272,20 +290,23 @@ def test_c1_full_parity(bpt, colors):
 
 
 def test_c1_level_structure_per_group(bpt):
-    """batch_groups = 1: each batch is one 64-colour group; its per-level frontier sizes and
-    edge reads equal the oracle's level sets."""
+    """batch_groups = 1: each batch is one 64-colour group -- 64 samples in sorted start order by
+    default, 64 consecutive samples with BPT_FLAG_UNSORTED; its per-level frontier sizes and edge
+    reads equal the oracle's level sets of the same group."""
     cfg = graphgen.CONFIGS["C1"]
     row_ptr, col, thr = graphgen.make_graph(cfg)
     og = oracle.Graph(row_ptr, col, w_q31=thr)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
-    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, batch_groups=1, poll_levels=1)
-    rows = s.level_stats()
-    for b in range(cfg.theta // 64):
-        w = og.group_work(cfg.seed, 64 * b, 64 * b + 64)
-        r = rows[rows[:, 0] == b]
-        assert r[:, 2].tolist() == w["frontier"].tolist()
-        assert int(r[:, 4].sum()) == w["e_phys"]
-        assert len(r) == w["levels"]
+    order = sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed)
+    for flags, groups in ((0, order), (bpt.FLAG_UNSORTED, np.arange(cfg.theta))):
+        s = g.sample(cfg.theta, colors=64, seed=cfg.seed, batch_groups=1, poll_levels=1, flags=flags)
+        rows = s.level_stats()
+        for b in range(cfg.theta // 64):
+            w = og.group_work_ids(cfg.seed, groups[64 * b:64 * b + 64])
+            r = rows[rows[:, 0] == b]
+            assert r[:, 2].tolist() == w["frontier"].tolist()
+            assert int(r[:, 4].sum()) == w["e_phys"]
+            assert len(r) == w["levels"]
 
 
 # ------------------------------------------------------------------ ragged and edge cases
@@ -364,7 +385,8 @@ def test_level_loop_variants(bpt, model):
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr)
-        variants = [0, bpt.FLAG_QUEUE]
+        # consecutive-sample groups in both forms (equal work counters), then the default sorted slots
+        variants = [bpt.FLAG_UNSORTED, bpt.FLAG_QUEUE, 0]
     else:
         cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 12, theta=2048)
         row_ptr, col, thr = graphgen.make_graph(cfg)
@@ -392,6 +414,8 @@ def test_level_loop_variants(bpt, model):
             s.close()
         infos.append(rows)
     assert infos[0] == infos[1]
+    if model == "IC":  # sorted start vertices: other groups, same sets (E_logical, members)
+        assert [r[3:5] for r in infos[2]] == [r[3:5] for r in infos[0]]
     if model == "LT":  # walks: same work counters as the fused loop (E_phys = E_logical = sum |RR|)
         for walk in infos[2:]:
             assert [r[2:5] for r in infos[0]] == walk
@@ -622,3 +646,42 @@ def test_empty_rank_shard_selection(bpt):
     s = gl.sample(64, seed=cfg.seed, shard=(2, 0))
     seeds, gains, _ = s.select_seeds(cfg.k)
     assert int(gains.sum()) == 0
+
+
+# ------------------------------------------------------------------ sorted start vertices
+
+def test_sorted_start_slots(bpt, c2_small):
+    """Samples assigned to traversal slots in start order (in-degree descending, start id, sample
+    id): RRR sets, sizes, digests, ragged-range extraction, occurrences, seeds and gains
+    are identical to the oracle's (coins keyed by sample id, reading C-1); E_phys equals the
+    oracle's group work of the sorted groups and is lower than with consecutive groups; per
+    rank shard the samples are sorted inside the shard."""
+    cfg, row_ptr, col, thr, ref = c2_small
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    srt = g.sample(cfg.theta, seed=cfg.seed)
+    uns = g.sample(cfg.theta, seed=cfg.seed, flags=bpt.FLAG_UNSORTED)
+    for s in (srt, uns):
+        check_full(bpt, s, ref, cfg.theta)
+        for first, count in ((5, 300), (cfg.theta - 77, 77), (1000, 1)):
+            off, mem = s.extract(first, count)
+            o0 = ref["offsets"]
+            assert np.array_equal(mem, ref["members"][o0[first]:o0[first + count]])
+        seeds, gains, _ = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+    assert np.array_equal(srt.occurrences(), uns.occurrences())
+    order = sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed)
+    B = srt.info["batch_groups"]
+    want = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64))
+    assert srt.info["e_phys"] == want
+    assert srt.info["e_phys"] < uns.info["e_phys"]
+    assert srt.info["e_logical"] == uns.info["e_logical"] == int(ref["elog"].sum())
+    rows = srt.level_stats()
+    ws = group_e_phys(ref["g"], cfg.seed, order, 64)
+    for b in range(len(ws) // B):  # per batch of B slots: the sum of its groups' edge reads
+        assert int(rows[rows[:, 0] == b][:, 4].sum()) == sum(w["e_phys"] for w in ws[B * b:B * b + B])
+    for W, r in ((3, 1), (3, 2)):
+        s0, s1 = graphgen.shard_range(cfg.theta, W, r)
+        sh = g.sample(cfg.theta, seed=cfg.seed, shard=(W, r))
+        assert np.array_equal(sh.digests(s0, s1 - s0), ref["digests"][s0:s1])
+        order = sorted_slots(row_ptr, col, cfg.n, s1, cfg.seed, s0=s0)
+        assert sh.info["e_phys"] == sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64))
