@@ -70,6 +70,8 @@ def lib():
     L.or_sigma_hat.restype = ctypes.c_double
     L.or_store_build.argtypes = [_p, _u64, _u64, _u64, _u32, _i, _u32]
     L.or_store_build.restype = _p
+    L.or_store_build_ids.argtypes = [_p, _u64, _u64, _p, _u64, _u32, _i, _u32, _i]
+    L.or_store_build_ids.restype = _p
     L.or_store_free.argtypes = [_p]
     L.or_store_free.restype = None
     L.or_store_info.argtypes = [_p, _p, _p, _p, _p, _p, _p]
@@ -208,10 +210,14 @@ class Store:
     that runs on it -- so full-size configs fit host memory (C2: ~20 GB instead of ~190 GB)."""
 
     def __init__(self, graph: "Graph", seed: int, s0: int, count: int, colors: int = 64,
-                 threads: int | None = None, list_max: int = 0):
+                 threads: int | None = None, list_max: int = 0, ids=None, keep: bool = True):
+        """ids: sample ids in traversal order (groups of `colors` consecutive ids; default s0 ...);
+        keep=False: sizes, digests and group work only (no sets, no greedy)."""
         self.graph, self.count, self.colors, self.n = graph, count, colors, graph.n
         self.ngroups = (count + colors - 1) // colors
-        h = lib().or_store_build(graph._h, seed, s0, count, colors, threads or default_threads(), list_max)
+        self._ids = None if ids is None else np.ascontiguousarray(ids, dtype=np.uint64)
+        h = lib().or_store_build_ids(graph._h, seed, s0, _ptr(self._ids), count, colors, threads or default_threads(),
+                                     list_max, int(keep))
         if not h:
             raise ValueError("oracle store: IC only, and BFS levels must stay below 64")
         self._h = h

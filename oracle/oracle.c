@@ -508,6 +508,8 @@ double or_sigma_hat(uint32_t n, uint64_t covered, uint64_t theta) {
 typedef struct {
     uint32_t n, colors;
     uint64_t s0, count, ngroups;
+    const uint64_t* ids;   /* sample ids in traversal order (NULL: s0, s0 + 1, ...) */
+    int keep;              /* keep the sets (lists / bitsets); 0: sizes, digests and group work only */
     uint32_t list_max;
     uint32_t* size;        /* [count] */
     uint64_t* digest;      /* [count] */
@@ -540,7 +542,7 @@ static void* store_worker(void* arg) {
         uint32_t ntouched = 0;
         for (uint64_t i = a; i < b; i++) {
             uint64_t el = 0;
-            uint32_t size = run_sample(g, &J->k, S->s0 + i, &w, &el);
+            uint32_t size = run_sample(g, &J->k, S->ids ? S->ids[i] : S->s0 + i, &w, &el);
             el_sum += el;
             uint64_t d = 0;
             for (uint32_t j = 0; j < size; j++) {
@@ -551,6 +553,7 @@ static void* store_worker(void* arg) {
                 lvmask[v] |= 1ULL << L;
             }
             S->size[i] = size; S->digest[i] = d;
+            if (!S->keep) continue;
             if (size <= S->list_max) {
                 uint32_t* l = (uint32_t*)malloc((size ? size : 1) * sizeof(uint32_t));
                 memcpy(l, w.queue, (size_t)size * sizeof(uint32_t));
@@ -589,12 +592,13 @@ void or_store_free(or_store* S) {
     free(S->e_phys); free(S->levels); free(S->frontier); free(S);
 }
 
-/* samples [s0, s0 + count), groups of `colors`; list_max = 0 selects n/32 */
-or_store* or_store_build(const or_graph* g, uint64_t seed, uint64_t s0, uint64_t count, uint32_t colors,
-                         int nthreads, uint32_t list_max) {
+/* samples [s0, s0 + count) -- or ids[0 .. count) in that order if ids != NULL --, traversal groups
+ * of `colors` consecutive entries; list_max = 0 selects n/32; keep = 0 keeps no sets */
+or_store* or_store_build_ids(const or_graph* g, uint64_t seed, uint64_t s0, const uint64_t* ids, uint64_t count,
+                             uint32_t colors, int nthreads, uint32_t list_max, int keep) {
     if (colors == 0 || g->model != 0) return NULL;
     or_store* S = (or_store*)calloc(1, sizeof(or_store));
-    S->n = g->n; S->colors = colors; S->s0 = s0; S->count = count;
+    S->n = g->n; S->colors = colors; S->s0 = s0; S->count = count; S->ids = ids; S->keep = keep;
     S->ngroups = (count + colors - 1) / colors;
     S->list_max = list_max ? list_max : g->n / 32;
     S->size = (uint32_t*)calloc(count ? count : 1, sizeof(uint32_t));
@@ -615,7 +619,13 @@ or_store* or_store_build(const or_graph* g, uint64_t seed, uint64_t s0, uint64_t
     free(th);
     pthread_mutex_destroy(&J.mu);
     if (atomic_load(&J.fail)) { or_store_free(S); return NULL; }
+    S->ids = NULL;  /* not retained */
     return S;
+}
+
+or_store* or_store_build(const or_graph* g, uint64_t seed, uint64_t s0, uint64_t count, uint32_t colors,
+                         int nthreads, uint32_t list_max) {
+    return or_store_build_ids(g, seed, s0, NULL, count, colors, nthreads, list_max, 1);
 }
 
 void or_store_info(const or_store* S, uint32_t* sizes, uint64_t* digests, uint64_t* e_phys, uint32_t* levels,

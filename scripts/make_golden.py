@@ -7,6 +7,8 @@ C-ABI results on the same seeded inputs against these files.
       per-level frontier sizes of every 64-sample traversal group, E_logical, greedy seeds and
       gains for k = 50 at theta = 65,536 and at theta = 2,048 (the first 32 groups), sigma_hat.
       ~40 min on 8 cores, ~20 GB (SURVEY §8(c) oracle step 3 store: lists / bitsets).
+  python scripts/make_golden.py C2S  -> tests/golden/c2_sorted_oracle.npz
+      per-group E_phys / levels / frontier sizes of the C2 step under sorted start vertices.
   python scripts/make_golden.py C4   -> tests/golden/c4_shard7_oracle.npz
       64 sample ids of the last of 8 rank shards of configs[3] (theta = 131,072), spread over the
       shard and over all 64 colour slots: sizes, digests, and the member lists of two of them.
@@ -51,6 +53,28 @@ def c2():
     print(f"done {time.time() - t0:.0f} s", flush=True)
 
 
+def c2_sorted():
+    """Group work of the C2 step under sorted start vertices (include/bpt.h BPT_FLAG_UNSORTED off):
+    the order is start in-degree descending, start id, sample id -- computed from the oracle's
+    start vertices and the forward CSR."""
+    cfg = graphgen.CONFIGS["C2"]
+    t0 = time.time()
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = oracle.Graph(row_ptr, col, w_q31=thr)
+    ids = np.arange(cfg.theta, dtype=np.int64)
+    starts = np.array([oracle.start_vertex(int(s), cfg.n, cfg.seed) for s in ids], dtype=np.int64)
+    indeg = np.bincount(col.astype(np.int64), minlength=cfg.n)
+    order = ids[np.lexsort((ids, starts, -indeg[starts]))]
+    S = oracle.Store(g, cfg.seed, 0, cfg.theta, 64, ids=order, keep=False)
+    np.savez_compressed(
+        os.path.join(GOLD, "c2_sorted_oracle.npz"),
+        citation=np.array("BASELINE.json configs[1] (C2) with sorted start vertices (P:430; SURVEY 8(f) NEXT #3): "
+                          "E_phys / levels / frontier sizes per 64-sample group of the sorted order, oracle/ only "
+                          "(scripts/make_golden.py C2S); P:239-241"),
+        order=order.astype(np.uint32), e_phys=S.e_phys, levels=S.levels, frontier=S.frontier.astype(np.uint32))
+    print(f"done {time.time() - t0:.0f} s, e_phys {int(S.e_phys.sum())}", flush=True)
+
+
 def c4_shard_ids(theta=131072, world=8, rank=7, count=64):
     nb = (theta + 63) // 64
     b0, b1 = rank * nb // world, (rank + 1) * nb // world
@@ -83,4 +107,4 @@ def c4():
 
 
 if __name__ == "__main__":
-    {"C2": c2, "C4": c4}[sys.argv[1]]()
+    {"C2": c2, "C2S": c2_sorted, "C4": c4}[sys.argv[1]]()

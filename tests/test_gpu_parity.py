@@ -82,12 +82,18 @@ def test_launch_evidence_counts(bpt):
     row_ptr, col, thr = graphgen.make_graph(cfg)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
     h0, d0 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
-    s = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1)
+    s = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1, flags=bpt.FLAG_UNSORTED)
     h1, d1 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
     info = s.info
     assert h1 - h0 == 1  # the graph launch
     assert d1 - d0 == 3 * info["batches"] + 2 * info["levels_total"]
     assert info["kernel_launches"] == (h1 - h0) + (d1 - d0)
+    # sorted start vertices add the slot sort: key kernel, log2(N)(log2(N)+1)/2 bitonic steps, maps
+    h1, d1 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
+    s = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1)
+    lg = (cfg.theta - 1).bit_length()
+    assert bpt.kernel_launch_count() - h1 == 1 + 2 + lg * (lg + 1) // 2
+    assert bpt.graph_kernel_count() - d1 == 3 * s.info["batches"] + 2 * s.info["levels_total"]
     p = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1, profile=True)
     assert bpt.graph_kernel_count() == d1  # profile mode launches directly
     assert bpt.kernel_launch_count() - h1 >= 3 * p.info["batches"] + 2 * p.info["levels_total"]
