@@ -94,6 +94,7 @@ def test_launch_evidence_counts(bpt):
     lg = (cfg.theta - 1).bit_length()
     assert bpt.kernel_launch_count() - h1 == 1 + 2 + lg * (lg + 1) // 2
     assert bpt.graph_kernel_count() - d1 == 3 * s.info["batches"] + 2 * s.info["levels_total"]
+    h1, d1 = bpt.kernel_launch_count(), bpt.graph_kernel_count()
     p = g.sample(cfg.theta, seed=cfg.seed, batch_groups=1, profile=True)
     assert bpt.graph_kernel_count() == d1  # profile mode launches directly
     assert bpt.kernel_launch_count() - h1 >= 3 * p.info["batches"] + 2 * p.info["levels_total"]
