@@ -1,9 +1,9 @@
 """Like-for-like DRAM traffic of the IC expansion (roofline `traffic`), for bench.py.
 
-Runs batch 0 of the bench's C2 step -- its first four 64-sample blocks (samples 0..255, the bench's
-first sampling seed, the automatic batch of 4 blocks exactly as bench.py launches it) -- through the
-host-driven level loop, and writes every level's counters to gpurun_out/traffic_levels.json. Run it under
-  ncu --set full -k regex:k_expand_bm -o gpurun_out/traffic_full python scripts/traffic_capture.py
+Runs the bench's C2 sampling call (theta = 65,536, the bench's first sampling seed, sorted start
+vertices, the automatic batch of 4 blocks exactly as bench.py launches it) through the host-driven
+level loop, and writes batch 0's level counters to gpurun_out/traffic_levels.json. Run it under
+  ncu --set full -k regex:k_expand_bm -c 16 -o gpurun_out/traffic_full python scripts/traffic_capture.py
 then `python scripts/traffic_capture.py --summarize` (here, no GPU) pairs launch i with level i and
 writes profiles/expand_traffic.json (per launch the DRAM bytes next to the algorithmic bytes of the
 SAME launch, DESIGN.md §6 byte model, and their sums) and profiles/expand_ncu_summary.json
@@ -37,8 +37,10 @@ def capture():
     torch.cuda.set_device(0)
     row_ptr, col, thr = graphgen.make_graph(cfg)
     g = bpt.Graph(row_ptr, col, w_q31=thr)
-    s = g.sample(256, colors=64, seed=cfg.seed, profile=True, poll_levels=1)  # batch 0 = 4 blocks
-    rows = s.level_stats().tolist()
+    # the whole bench sampling call (sorted start vertices over all theta samples), host-driven so
+    # every expansion launch is a direct launch; ncu captures the first ones = batch 0's levels
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, profile=True, poll_levels=1)
+    rows = [r for r in s.level_stats().tolist() if r[0] == 0]
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, "traffic_levels.json"), "w") as f:
         json.dump({"rows": rows, "info": s.info}, f)
@@ -71,7 +73,7 @@ def summarize():
     lv = json.load(open(os.path.join(OUT, "traffic_levels.json")))
     rows = lv["rows"]
     alg = alg_bytes(rows)
-    seq = _ncu_rows(os.path.join(OUT, "traffic_full.ncu-rep"))
+    seq = _ncu_rows(os.path.join(OUT, "traffic_full.ncu-rep"))[:len(rows)]  # batch 0's levels
     per = []
     for i, d in enumerate(seq):
         a = alg[i] if i < len(alg) else 0.0  # launches after the last level are no-ops (pipelined polling)
@@ -87,8 +89,8 @@ def summarize():
     edges = sum(p["edges"] for p in per)
     us = sum(p["us"] for p in per) or 1.0
     wavg = lambda k: sum((p[k] or 0) * p["us"] for p in per) / us  # time-weighted
-    src = ("ncu --set full of every k_expand_bm launch of batch 0 of the bench step (C2, samples 0..255 = 4 blocks, "
-           "bench seed, automatic batch, host-driven level loop; scripts/traffic_capture.py)")
+    src = ("ncu --set full of every k_expand_bm launch of batch 0 of the bench's sampling call (C2, theta 65,536, "
+           "bench seed, sorted start vertices, 4 blocks per batch, host-driven level loop; scripts/traffic_capture.py)")
     res = {"source": src, "kernel": seq[0].get("Kernel Name") if seq else None, "launches": n,
            "dram_bytes_per_launch": dram / n if n else None, "algorithmic_bytes_per_launch": algs / n if n else None,
            "dram_over_algorithmic": dram / algs if algs else None, "per_launch": per}
