@@ -813,6 +813,10 @@ __global__ void __launch_bounds__(kThreads, kC64 ? BPT_EXPAND_MINB : 4) k_expand
 #endif
 constexpr int kWinBm = BPT_WIN_BM;   // 32-lane windows per warp work unit (4: measured 4% faster than 3)
 constexpr int kUnitBm = 32 * kWinBm;
+#ifndef BPT_HEAVY
+#define BPT_HEAVY 24
+#endif
+constexpr int kHeavy = BPT_HEAVY;  // live colours from which an item's coins are drawn warp-wide
 struct BmScratch {
     uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
     uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
@@ -914,14 +918,39 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
         const uint32_t j = c0 + lane;
         const bool has = j < nlive;
         uint32_t cnt = 0;
+        uint4 mine = make_uint4(0, 0, 0, 0);
         if (has) {
-            const uint4 it = W.A[j];
-            cnt = __popc(it.z) + __popc(it.w);
-            W.pass[lane] = 0;
+            mine = W.A[j];
+            cnt = __popc(mine.z) + __popc(mine.w);
         }
-        const uint32_t incl = warp_incl_scan_u32(cnt, lane);
+        // heavy items (>= kHeavy live colours; the sorted groups' hub rows): the whole warp draws
+        // the item's coins by bit POSITION -- lanes l and l + 32 -- with no decode at all, and the
+        // passing colours come back as two ballots
+        const bool heavy = cnt >= (uint32_t)kHeavy;
+        unsigned long long hpass = 0;
+        for (uint32_t hb = __ballot_sync(kFull, heavy); hb; hb &= hb - 1) {
+            const uint32_t hj = __ffs(hb) - 1;
+            const uint4 it = W.A[c0 + hj];  // broadcast
+            const uint32_t sb = W.B[c0 + hj].x;
+            bool p0 = false, p1 = false;
+            if ((it.z >> lane) & 1u) {
+                const uint32_t sid = sb + lane;
+                p0 = (philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys) >> 1) < it.y;
+            }
+            if ((it.w >> lane) & 1u) {
+                const uint32_t sid = sb + 32 + lane;
+                p1 = (philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys) >> 1) < it.y;
+            }
+            const uint32_t lo = __ballot_sync(kFull, p0), hi = __ballot_sync(kFull, p1);
+            if (lane == (int)hj) hpass = ((unsigned long long)hi << 32) | lo;
+        }
+        if (has) W.pass[lane] = hpass;
+        // light items: their (item, colour) tasks flattened, 32 per round; a heavy item keeps one
+        // dummy task so the owners' exclusive prefixes stay strictly increasing
+        const uint32_t lcnt = heavy ? 1u : cnt;
+        const uint32_t incl = warp_incl_scan_u32(lcnt, lane);
         const uint32_t ntask = __shfl_sync(kFull, incl, 31);
-        const uint32_t excl = incl - cnt;
+        const uint32_t excl = incl - lcnt;
         __syncwarp();
         for (uint32_t b = 0; b < ntask; b += 32) {
             // owner of task b + i = (lanes with excl <= b + i) - 1 (every live item has >= 1 task, so the
@@ -932,8 +961,9 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             const uint32_t starts = __reduce_or_sync(kFull, (has && d < 32u) ? (1u << d) : 0u);
             const uint32_t o = (below + __popc(starts & le_mask) - 1u) & 31u;
             const uint32_t eo = __shfl_sync(kFull, excl, o);
+            const bool oheavy = __shfl_sync(kFull, heavy, o);
             const uint32_t k = b + lane;
-            if (k < ntask) {
+            if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select64(it.z, it.w, k - eo, sel8);
                 const uint32_t sid = W.B[c0 + o].x + bit;  // slot index (sorted) or sample id
@@ -942,7 +972,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
         }
-        if (lane == 0) coins += ntask;
+        coins += __reduce_add_sync(kFull, cnt) * (lane == 0);
         __syncwarp();
         if (has) {
             const unsigned long long pass = W.pass[lane];
@@ -1629,7 +1659,13 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
 // Sparse LT store: the visited set of a walk is a per-thread open-addressing hash set in local
 // memory (2,048 slots; a walk longer than 1,536 vertices is reported, the dense store handles
 // those), so no dense n x blocks bitmap exists at all.
-constexpr uint32_t kWalkHash = 2048, kWalkMax = 1536;
+#ifndef BPT_WALK_HASH_BITS
+#define BPT_WALK_HASH_BITS 11
+#endif
+// per-thread visited set of a walk: 2^bits u32 slots, walks up to 3/4 of that (longer ones move
+// the call to the dense-store walks); the set is cleared once per walk
+constexpr uint32_t kWalkHashBits = BPT_WALK_HASH_BITS;
+constexpr uint32_t kWalkHash = 1u << kWalkHashBits, kWalkMax = kWalkHash / 4 * 3;
 
 // Register cap for the sparse walks: at 7 blocks per SM ptxas fits the walk in 32 registers, so
 // 8 blocks x 256 threads are resident per SM and C3's 262,144 walks (1,024 blocks) start in ONE
@@ -1662,7 +1698,7 @@ __global__ void __launch_bounds__(256, BPT_WALK_MINB) k_walk_lt_sparse(uint32_t 
                 x = ht[h];
             }
         };
-        auto home = [](uint32_t u) -> uint32_t { return (u * 0x9E3779B1u) >> 21; };
+        auto home = [](uint32_t u) -> uint32_t { return (u * 0x9E3779B1u) >> (32 - kWalkHashBits); };
         auto insert = [&](uint32_t u) -> bool { const uint32_t h = home(u); return insert_at(u, h, ht[h]); };
         const uint2 w = philox2x32_10((uint32_t)s, (uint32_t)(s >> 32), k_start);
         uint32_t v = (uint32_t)__umul64hi(((uint64_t)w.y << 32) | w.x, (uint64_t)n);
