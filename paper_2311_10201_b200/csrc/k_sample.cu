@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, kC64 ? BPT_EXPAND_MINB : 4) k_expand
 constexpr int kWinBm = BPT_WIN_BM;   // 32-lane windows per warp work unit (4: measured 4% faster than 3)
 constexpr int kUnitBm = 32 * kWinBm;
 #ifndef BPT_HEAVY
-#define BPT_HEAVY 24
+#define BPT_HEAVY 32
 #endif
 constexpr int kHeavy = BPT_HEAVY;  // live colours from which an item's coins are drawn warp-wide
 struct BmScratch {
