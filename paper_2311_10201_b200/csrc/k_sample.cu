@@ -821,6 +821,7 @@ struct BmScratch {
     uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
     uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
     unsigned long long pass[32];            // passing colours of the chunk's live items
+    uint2 cum[32];                          // byte prefix popcounts of the chunk's live masks
 };
 
 // Philox2x32-10 (reading C-1) with the key schedule k + r * W precomputed in the kernel parameters
@@ -852,6 +853,27 @@ __device__ __forceinline__ uint32_t rank_select64(uint32_t lo, uint32_t hi, uint
     const uint32_t before = byte ? (pre >> (8 * byte - 8)) & 0xffu : 0u;
     const uint32_t v = (w >> (8 * byte)) & 0xffu;
     return (upper ? 32u : 0u) + 8u * byte + ((sel8[v] >> (3 * (r - before))) & 7u);
+}
+
+// byte prefix popcounts of the 64-bit mask hi:lo -- byte i of .x = set bits in bytes 0..i, of .y =
+// set bits in bytes 0..4+i -- computed once per live item, then every rank select of its tasks is a
+// SIMD byte compare and one table lookup
+__device__ __forceinline__ uint2 byte_prefix64(uint32_t lo, uint32_t hi) {
+    auto bytes = [](uint32_t w) {
+        uint32_t t = w - ((w >> 1) & 0x55555555u);
+        t = (t & 0x33333333u) + ((t >> 2) & 0x33333333u);
+        return (t + (t >> 4)) & 0x0f0f0f0fu;
+    };
+    return make_uint2(bytes(lo) * 0x01010101u, bytes(hi) * 0x01010101u + (uint32_t)__popc(lo) * 0x01010101u);
+}
+__device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, uint2 cum, uint32_t r,
+                                                    const uint32_t* sel8) {
+    const uint32_t rr = (r | 0x80u) * 0x01010101u;  // r + 128 in every byte (r < 64, prefixes <= 64)
+    const uint32_t byte = __popc((rr - cum.x) & 0x80808080u) + __popc((rr - cum.y) & 0x00808080u);
+    const uint64_t c64 = ((uint64_t)cum.y << 32) | cum.x;
+    const uint32_t before = byte ? (uint32_t)(c64 >> (8 * byte - 8)) & 0xffu : 0u;
+    const uint32_t v = (uint32_t)((((uint64_t)hi << 32) | lo) >> (8 * byte)) & 0xffu;
+    return 8u * byte + ((sel8[v] >> (3 * (r - before))) & 7u);
 }
 
 template <bool kWhole>
@@ -944,7 +966,10 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             const uint32_t lo = __ballot_sync(kFull, p0), hi = __ballot_sync(kFull, p1);
             if (lane == (int)hj) hpass = ((unsigned long long)hi << 32) | lo;
         }
-        if (has) W.pass[lane] = hpass;
+        if (has) {
+            W.pass[lane] = hpass;
+            W.cum[lane] = byte_prefix64(mine.z, mine.w);
+        }
         // light items: their (item, colour) tasks flattened, 32 per round; a heavy item keeps one
         // dummy task so the owners' exclusive prefixes stay strictly increasing
         const uint32_t lcnt = heavy ? 1u : cnt;
@@ -965,7 +990,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
             const uint32_t k = b + lane;
             if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
-                const uint32_t bit = rank_select64(it.z, it.w, k - eo, sel8);
+                const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
                 const uint32_t sid = W.B[c0 + o].x + bit;  // slot index (sorted) or sample id
                 const uint32_t x = philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys);
                 if ((x >> 1) < it.y)
