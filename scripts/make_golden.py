@@ -24,7 +24,7 @@ sys.path.insert(0, ROOT)
 import graphgen  # noqa: E402
 import oracle  # noqa: E402
 
-GOLD = os.path.join(ROOT, "tests", "golden")
+GOLD = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "tests", "golden")  # optional output dir
 
 
 def c2():
