@@ -95,9 +95,10 @@ def c4():
     sizes, digests, elog = g.sample_many(cfg.seed, ids)
     print(f"samples {time.time() - t0:.0f} s", flush=True)
     lists = {}
-    for j in (0, len(ids) - 1):
+    for j in (0, len(ids) - 1):  # two member lists, sampled (every 997th member) to keep the file small
         mem, _, _ = g.sample_one(cfg.seed, int(ids[j]))
-        lists[f"list_{int(ids[j])}"] = mem
+        lists[f"list_{int(ids[j])}_len"] = np.array(len(mem), dtype=np.uint64)
+        lists[f"list_{int(ids[j])}_every997"] = mem[::997].copy()
     np.savez_compressed(
         os.path.join(GOLD, "c4_shard7_oracle.npz"),
         citation=np.array("BASELINE.json configs[3] (C4), graph_seed 4, sampling seed 0x5EED0004, theta 131072, "
