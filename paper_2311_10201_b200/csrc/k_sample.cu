@@ -232,37 +232,66 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long vc_local = 0;
     uint32_t touched_local = 0;
-    for (uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile; tile0 < nraw; tile0 += (uint64_t)gridDim.x * kCompTile) {
+    // bitmap mode: the block's tiles (block b: tiles b, b + G, ...) are first screened with one
+    // warp-wide 128-B load per tile, and only the non-empty ones are processed (most tiles of the
+    // thin levels are empty: 4 x 4,734 tiles per C2 level)
+    constexpr uint32_t kScreen = 256;  // tiles screened per pass
+    __shared__ uint32_t nonempty[kScreen];
+    __shared__ uint32_t n_nonempty;
+    const uint32_t ntiles_all = bitmap ? (uint32_t)(nraw / kCompTile) : 0u;
+    uint32_t k0 = 0;       // first screened tile index (in units of the grid stride) of this pass
+    uint32_t li = 0;       // next non-empty tile of this pass
+    uint64_t tile0 = (uint64_t)blockIdx.x * kCompTile;
+    while (true) {
+        if (bitmap) {
+            if (li == 0 || li >= n_nonempty) {  // screen the next kScreen tiles of this block
+                __syncthreads();
+                if (li != 0) k0 += kScreen;
+                li = 0;
+                if (threadIdx.x == 0) n_nonempty = 0;
+                __syncthreads();
+                if ((uint64_t)blockIdx.x + (uint64_t)k0 * gridDim.x >= ntiles_all) break;
+                for (uint32_t k = k0 + wid; k < k0 + kScreen; k += kWarps) {
+                    const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
+                    if (t >= ntiles_all) break;
+                    const uint32_t w = LDX(a.touched + t * 32 + lane);
+                    if (__any_sync(kFull, w != 0) && lane == 0) nonempty[atomicAdd(&n_nonempty, 1u)] = (uint32_t)t;
+                }
+                __syncthreads();
+                if (n_nonempty == 0) { li = 1; continue; }  // nothing in this pass: screen the next one
+            }
+            tile0 = (uint64_t)nonempty[li++] * kCompTile;
+        } else {
+            if (tile0 >= nraw) break;
+        }
         uint64_t r[kCompItems];
         if (bitmap) {
             // tile t of slot t / tiles covers vertices 1024 (t % tiles) + [0, 1024); item it of
             // thread x is vertex it * 256 + x of the tile: bit `lane` of word 8 it + warp
-            const uint64_t t = tile0 / kCompTile;
-            const uint32_t slot = (uint32_t)(t / a.tiles);
-            const uint32_t vbase = (uint32_t)(t % a.tiles) * kCompTile;
+            const uint32_t t = (uint32_t)(tile0 / kCompTile);
+            const uint32_t slot = t / a.tiles;
+            const uint32_t vbase = (t - slot * a.tiles) * kCompTile;
             uint32_t* wp = a.touched + t * 32 + wid;
             uint32_t wv[kCompItems];
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) wv[it] = LDX(wp + 8 * it);
-            bool anyb = false;
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) {
                 const bool on = (wv[it] >> lane) & 1u;
                 r[it] = on ? raw_pack(vbase + it * kThreads + threadIdx.x, slot, 0) : ~0ull;
-                anyb |= on;
                 touched_local += on;
             }
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it)  // cleared for the next level
                 if (lane == it && wv[it]) wp[8 * it] = 0;
-            if (!__syncthreads_or(anyb)) continue;
         } else {
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) {
                 const uint64_t i = tile0 + (uint64_t)it * kThreads + threadIdx.x;
                 r[it] = i < nraw ? LDX(&a.raw[i]) : ~0ull;
             }
+            tile0 += (uint64_t)gridDim.x * kCompTile;
         }
         uint64_t mask[kCompItems];
         uint32_t rs[kCompItems], re[kCompItems];
