@@ -356,7 +356,7 @@ static bool run_lt_walks_sparse(Samples& S, const bpt_sample_opts& opt, cudaStre
     }
     const double t_alloc = since();
     WalkTimer tm(st);
-    launch_walk_lt_sparse(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), (uint32_t)g.m, S.s0, nlocal, stream_key(S.seed, kTagStart),
+    launch_walk_lt_sparse(g, S.s0, nlocal, stream_key(S.seed, kTagStart),
                           stream_key(S.seed, kTagLT), S.sizes.as<uint32_t>(), S.count0.as<uint32_t>(),
                           totals.as<unsigned long long>(), rows.p ? rows.as<uint32_t>() : nullptr, st);
     tm.stop(st);

@@ -2,6 +2,7 @@
 // Not part of the ABI; the ABI is include/bpt.h.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cstddef>
 #include <string>
 #include <vector>
@@ -107,6 +108,14 @@ struct Graph {
     int model = 0;
     DevBuf roff;   // u32[n+1]
     DevBuf rec;    // uint2[m] {src, thr (IC) | cum (LT)}
+    // LT sparse walks: per-thread visited hash sets in global memory, entries tagged with a walk
+    // epoch so no set is ever cleared between walks (zeroed once; re-zeroed when the epochs wrap).
+    // Used under `walk_mu`; a call orders itself after the previous user by `walk_ev`.
+    mutable DevBuf walk_ht;
+    mutable uint32_t walk_epoch = 0;     // last epoch handed out
+    mutable std::mutex walk_mu;
+    mutable cudaEvent_t walk_ev = nullptr;
+    ~Graph() { if (walk_ev) cudaEventDestroy(walk_ev); }
 };
 
 // Per-level device record of one batch (zeroed at batch start).
@@ -283,7 +292,8 @@ void launch_walk_lt(uint64_t* store, uint32_t n, const uint32_t* roff, const uin
                     cudaStream_t st);
 // LT sparse store: walks with a per-thread visited hash set (no dense store); sizes, count0,
 // totals[0..1] as launch_walk_lt, totals[2] = 1 if a walk outgrew the hash set
-void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
+// `g`'s walk tables (Graph::walk_ht) hold the visited sets
+void launch_walk_lt_sparse(const Graph& g, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
                            unsigned long long* totals, uint32_t* rows, cudaStream_t st);
 // walk-order member rows (optional output of the sparse walk: stride walk_row_stride()) -> lists

@@ -1554,8 +1554,8 @@ __device__ __forceinline__ bool lt_pick(const uint32_t* __restrict__ roff, const
     for (int step = 0; hi - lo > 1; ++step) {
         uint32_t g;
         if (step < 4) {
-            g = lo + (uint32_t)((uint64_t)(r - clo) * (hi - lo) / (uint64_t)(chi - clo));
-            g = min(g, hi - 2);
+            // interpolation guess in f32 (any guess inside [lo, hi - 2] is correct; no 64-bit division)
+            g = lo + min((uint32_t)(__fdividef((float)(r - clo), (float)(chi - clo)) * (float)(hi - lo)), hi - lo - 2);
         } else {
             g = (lo + hi - 1) >> 1;
         }
@@ -1573,17 +1573,6 @@ __device__ __forceinline__ bool lt_pick(const uint32_t* __restrict__ roff, const
 // round trips depends on it) and one 64-B window of 8 records around it is loaded at once. The
 // answer is the first j in [lo, hi) with cum[j] > r (none if r >= cum[hi - 1]) exactly as in
 // lt_pick; when it is not inside the window the search continues on the side it lies.
-// The visited-set probe *slot (local memory) and the row bounds roff[u], roff[u + 1] in ONE asm
-// statement: the probe decides a branch, and without this the compiler sank the bound loads
-// below it (the probe and the bounds then ran as two DRAM round trips in series).
-__device__ __forceinline__ void ld_probe_and_bounds(const uint32_t* slot, const uint32_t* p, uint32_t& x,
-                                                    uint32_t& lo, uint32_t& hi) {
-    const uint32_t ls = (uint32_t)__cvta_generic_to_local(slot);
-    asm volatile("ld.local.u32 %0, [%3];\n\tld.global.nc.u32 %1, [%4];\n\tld.global.nc.u32 %2, [%4+4];"
-                 : "=r"(x), "=r"(lo), "=r"(hi)
-                 : "r"(ls), "l"(p)
-                 : "memory");
-}
 
 // lo, hi: the row bounds roff[v], roff[v + 1], loaded by the caller (ahead of time).
 __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, const uint2* __restrict__ rec,
@@ -1634,9 +1623,9 @@ __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, c
     }
     for (int step = 0; hi - lo > 1; ++step) {
         uint32_t gg;
-        if (step < 4) {
-            gg = lo + (uint32_t)((uint64_t)(r - clo) * (hi - lo) / (uint64_t)(chi - clo));
-            gg = min(gg, hi - 2);
+        if (step < 4) {  // interpolation guess in f32 (any guess inside [lo, hi - 2] is correct)
+            const float f = __fdividef((float)(r - clo), (float)(chi - clo)) * (float)(hi - lo);
+            gg = lo + min((uint32_t)f, hi - lo - 2);
         } else {
             gg = (lo + hi - 1) >> 1;
         }
@@ -1710,14 +1699,20 @@ __global__ void __launch_bounds__(256) k_walk_lt_lists(uint32_t n, const uint32_
     }
 }
 
-// Sparse LT store: the visited set of a walk is a per-thread open-addressing hash set in local
-// memory (2,048 slots; a walk longer than 1,536 vertices is reported, the dense store handles
-// those), so no dense n x blocks bitmap exists at all.
+// Sparse LT store: the visited set of a walk is a per-thread open-addressing hash set (2,048
+// slots; a walk longer than 1,536 vertices is reported, the dense store handles those), so no
+// dense n x blocks bitmap exists at all. The sets live in global memory (Graph::walk_ht, one
+// 8 KB region per thread, zeroed once) and every entry carries the epoch of the walk that wrote
+// it: entry = epoch << shift | (u + 1), n < 2^shift. A slot whose epoch is not the current walk's
+// is empty, so a set is never cleared between walks (round 1 cleared a local-memory set of 8 KB
+// per walk: 2.1 GB of stores per C3 call, 23x the walk's algorithmic DRAM bytes). Each call
+// takes a fresh range of epochs (one per walk of a thread); the host re-zeroes the tables when the
+// epochs wrap. shift = 32 (n >= 2^31): epoch 0, empty = 0, the tables cleared per walk.
 #ifndef BPT_WALK_HASH_BITS
 #define BPT_WALK_HASH_BITS 11
 #endif
 // per-thread visited set of a walk: 2^bits u32 slots, walks up to 3/4 of that (longer ones move
-// the call to the dense-store walks); the set is cleared once per walk
+// the call to the dense-store walks)
 constexpr uint32_t kWalkHashBits = BPT_WALK_HASH_BITS;
 constexpr uint32_t kWalkHash = 1u << kWalkHashBits, kWalkMax = kWalkHash / 4 * 3;
 
@@ -1728,26 +1723,49 @@ constexpr uint32_t kWalkHash = 1u << kWalkHashBits, kWalkMax = kWalkHash / 4 * 3
 #ifndef BPT_WALK_MINB
 #define BPT_WALK_MINB 7
 #endif
+struct WalkTab {
+    uint32_t* ht;       // [threads][kWalkHash]
+    uint32_t shift;     // n < 2^shift (32: no epoch bits)
+    uint32_t epoch0;    // epoch of a thread's first walk of this call (walk j: epoch0 + j)
+    uint32_t clear;     // 1: clear the thread's set before every walk (no epoch range left)
+};
+// The visited-set probe *slot (global walk table) and the row bounds roff[u], roff[u + 1] in ONE asm
+// statement: the probe decides a branch, and without this the compiler sank the bound loads
+// below it (the probe and the bounds then ran as two DRAM round trips in series).
+__device__ __forceinline__ void ld_probe_and_bounds_g(const uint32_t* slot, const uint32_t* p, uint32_t& x,
+                                                      uint32_t& lo, uint32_t& hi) {
+    asm volatile("ld.global.u32 %0, [%3];\n\tld.global.nc.u32 %1, [%4];\n\tld.global.nc.u32 %2, [%4+4];"
+                 : "=r"(x), "=r"(lo), "=r"(hi)
+                 : "l"(slot), "l"(p)
+                 : "memory");
+}
 __global__ void __launch_bounds__(256, BPT_WALK_MINB) k_walk_lt_sparse(uint32_t n, const uint32_t* __restrict__ roff,
                                                         const uint2* __restrict__ rec, uint32_t m, uint64_t s0,
                                                         uint64_t nlocal,
                                                         uint32_t k_start, uint32_t k_lt,
                                                         uint32_t* __restrict__ sizes, uint32_t* __restrict__ count0,
                                                         unsigned long long* __restrict__ totals,
-                                                        uint32_t* __restrict__ rows) {
+                                                        uint32_t* __restrict__ rows, WalkTab tab) {
     // rows (optional): member i of local sample l at rows[l * kWalkMax + i], in walk order
-    uint32_t ht[kWalkHash];
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint32_t* __restrict__ ht = tab.ht + tid * kWalkHash;
     unsigned long long members = 0;
     uint32_t longest = 0, too_long = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nlocal; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t epoch = tab.epoch0;
+    for (uint64_t i = tid; i < nlocal; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t s = s0 + i;
-#pragma unroll 8
-        for (uint32_t h = 0; h < kWalkHash; ++h) ht[h] = ~0u;
+        if (tab.clear) {
+            for (uint32_t h = 0; h < kWalkHash; h += 4) *reinterpret_cast<uint4*>(ht + h) = make_uint4(0, 0, 0, 0);
+        }
+        // slot value of u in this walk; a slot is empty unless its epoch is this walk's
+        const uint32_t etag = epoch << (tab.shift & 31), emask = tab.shift >= 32 ? 0u : ~0u << tab.shift;
+        auto empty = [&](uint32_t x) -> bool { return ((x & emask) != etag) | (x == 0u); };
         // insert u, whose home slot h was already read (x); false if u was already in the set
         auto insert_at = [&](uint32_t u, uint32_t h, uint32_t x) -> bool {
+            const uint32_t want = etag | (u + 1u);
             while (true) {
-                if (x == u) return false;
-                if (x == ~0u) { ht[h] = u; return true; }
+                if (x == want) return false;
+                if (empty(x)) { ht[h] = want; return true; }
                 h = (h + 1) & (kWalkHash - 1);
                 x = ht[h];
             }
@@ -1769,7 +1787,7 @@ __global__ void __launch_bounds__(256, BPT_WALK_MINB) k_walk_lt_sparse(uint32_t 
             // the bounds and coin are wasted only on the step that ends the walk)
             const uint32_t h = home(u);
             uint32_t x;
-            ld_probe_and_bounds(&ht[h], roff + u, x, lo, hi);
+            ld_probe_and_bounds_g(&ht[h], roff + u, x, lo, hi);
             // consumed on both sides of the branch below (never true for a validated CSR, where
             // roff[u] <= m): keeps the bound loads above the branch
             bad_bounds |= (lo > m) | (hi > m);
@@ -1785,6 +1803,7 @@ __global__ void __launch_bounds__(256, BPT_WALK_MINB) k_walk_lt_sparse(uint32_t 
         members += size;
         longest = max(longest, size);
         too_long |= bad_bounds;
+        if (!tab.clear) ++epoch;
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -1916,8 +1935,8 @@ __device__ __forceinline__ void expand_lt_body(const BatchArgs& a, const uint32_
                         for (int step = 0; hi2 - lo2 > 1; ++step) {
                             uint32_t g;
                             if (step < 4) {
-                                g = lo2 + (uint32_t)((uint64_t)(r - clo) * (hi2 - lo2) / (uint64_t)(chi - clo));
-                                g = min(g, hi2 - 2);
+                                // interpolation guess in f32 (any guess inside [lo, hi - 2] is correct; no 64-bit division)
+                                g = lo2 + min((uint32_t)(__fdividef((float)(r - clo), (float)(chi - clo)) * (float)(hi2 - lo2)), hi2 - lo2 - 2);
                             } else {
                                 g = (lo2 + hi2 - 1) >> 1;
                             }
@@ -2047,14 +2066,46 @@ void launch_rows_to_lists(const uint32_t* rows, const uint64_t* off, uint64_t nl
     ::bpt::check_cuda(cudaGetLastError(), "launch k_rows_to_lists");
 }
 
-void launch_walk_lt_sparse(uint32_t n, const uint32_t* roff, const uint2* rec, uint32_t m, uint64_t s0, uint64_t nlocal,
+void launch_walk_lt_sparse(const Graph& g, uint64_t s0, uint64_t nlocal,
                            uint32_t k_start, uint32_t k_lt, uint32_t* sizes, uint32_t* count0,
                            unsigned long long* totals, uint32_t* rows, cudaStream_t st) {
-    const unsigned grid = (unsigned)umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8);
-    k_walk_lt_sparse<<<grid ? grid : 1, 256, 0, st>>>(n, roff, rec, m, s0, nlocal, k_start, k_lt, sizes, count0, totals,
-                                                      rows);
+    const unsigned grid = (unsigned)umax64(1, umin64((nlocal + 255) / 256, (uint64_t)num_sms() * 8));
+    const uint64_t threads = (uint64_t)grid * 256;
+    const uint64_t walks = umax64(1, (nlocal + threads - 1) / threads);  // walks per thread
+    std::lock_guard<std::mutex> lock(g.walk_mu);
+    if (!g.walk_ev) ::bpt::check_cuda(cudaEventCreateWithFlags(&g.walk_ev, cudaEventDisableTiming), "walk event");
+    else ::bpt::check_cuda(cudaStreamWaitEvent(st, g.walk_ev, 0), "walk event wait");  // previous user of the tables
+    const size_t bytes = threads * kWalkHash * 4;
+    WalkTab tab{};
+    tab.shift = 32u - (uint32_t)__builtin_clz(g.n | 1u);  // n < 2^shift
+    if (tab.shift >= 31) tab.shift = 32;                    // no room for an epoch field
+    const uint64_t max_epoch = tab.shift >= 32 ? 0 : (1ull << (32 - tab.shift)) - 1;
+    if (g.walk_ht.bytes < bytes) {
+        g.walk_ht.reset();
+        g.walk_ht.alloc(bytes);
+        ::bpt::check_cuda(cudaMemsetAsync(g.walk_ht.p, 0, g.walk_ht.bytes, st), "walk table zero");
+        g.walk_epoch = 0;
+    }
+    if (max_epoch == 0 || walks > max_epoch) {
+        tab.clear = 1;  // every walk clears its set (epoch 0 or a single epoch, re-zeroed below)
+        ::bpt::check_cuda(cudaMemsetAsync(g.walk_ht.p, 0, g.walk_ht.bytes, st), "walk table zero");
+        g.walk_epoch = 0;
+        tab.epoch0 = max_epoch ? 1u : 0u;
+    } else {
+        if (g.walk_epoch + walks > max_epoch) {  // epochs wrap: stale tags could alias
+            ::bpt::check_cuda(cudaMemsetAsync(g.walk_ht.p, 0, g.walk_ht.bytes, st), "walk table zero");
+            g.walk_epoch = 0;
+        }
+        tab.epoch0 = g.walk_epoch + 1;
+        g.walk_epoch += (uint32_t)walks;
+    }
+    tab.ht = g.walk_ht.as<uint32_t>();
+    k_walk_lt_sparse<<<grid, 256, 0, st>>>(g.n, g.roff.as<uint32_t>(), g.rec.as<uint2>(), (uint32_t)g.m, s0, nlocal,
+                                           k_start, k_lt, sizes, count0, totals, rows, tab);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_walk_lt_sparse");
+    g.walk_ht.stream = st;
+    ::bpt::check_cuda(cudaEventRecord(g.walk_ev, st), "walk event record");
 }
 
 void launch_sort_lists(const uint64_t* off, uint32_t* members, uint64_t nlists, uint32_t* err, cudaStream_t st) {

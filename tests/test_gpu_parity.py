@@ -533,6 +533,23 @@ def test_lt_long_walks_fall_back_to_dense(bpt):
     assert ei.value.code == bpt.BPT_ENOMEM
 
 
+def test_lt_sparse_walk_table_epochs(bpt):
+    """The sparse walks' visited sets live in per-thread global tables tagged with a walk epoch
+    (never cleared between walks): theta > the walk launch's thread count (148 x 8 x 256) makes
+    every thread walk twice in one call (two epochs), and repeated calls on the same graph reuse
+    the tables with fresh epochs. Sizes and digests stay identical to the oracle each time."""
+    cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 11, theta=64)
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr, model=bpt.LT)
+    og = oracle.Graph(row_ptr, col, w_q31=thr, model=oracle.LT)
+    for theta, seed in [((1 << 19) + 77, 3), (4096, 4), ((1 << 19) + 77, 3)]:
+        sizes, digests, _ = og.sample_many(seed, np.arange(theta, dtype=np.uint64))
+        s = g.sample(theta, colors=64, seed=seed, sparse=True)
+        assert np.array_equal(s.sizes(0, theta), sizes)
+        assert np.array_equal(s.digests(0, theta), digests)
+        s.close()
+
+
 def test_lt_ragged_theta_and_ranges(bpt):
     cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 11, theta=64)
     row_ptr, col, thr = graphgen.make_graph(cfg)
