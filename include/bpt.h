@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BPT_ABI_VERSION 1
+#define BPT_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define BPT_API __attribute__((visibility("default")))
@@ -132,7 +132,8 @@ typedef struct {
     uint32_t flags;          /* BPT_FLAG_* */
     uint32_t shard_world;    /* test hook: sample only shard shard_rank of shard_world (0 = use the comm) */
     uint32_t shard_rank;
-    uint32_t reserved;
+    uint32_t pull_permille;  /* BPT_FLAG_PULL: levels whose push work is >= pull_permille / 1000 x m
+                                are pulled (0 = the default, 1000) */
 } bpt_sample_opts;
 #define BPT_FLAG_PROFILE 1u  /* time every expansion launch with CUDA events */
 /* Wide fusion (the paper fuses up to 1024 colours): IC with
@@ -164,6 +165,14 @@ typedef struct {
  * On by default; this flag keeps sample s in slot s (groups of consecutive samples, reading C-9).
  * RRR sets, sizes, digests and seeds are identical either way; E_phys / levels differ. */
 #define BPT_FLAG_UNSORTED 256u
+/* IC, 64 colours (touched-bitmap form): direction switching (P:544-545,
+ * P:529-531). A level whose push work (reverse-edge reads of the frontier, all slots of the batch)
+ * reaches ~m is expanded by PULL: every forward edge u -> w is read once for all slots of the
+ * batch, live = frontier(w) & ~visited(u), with the coin of the edge's canonical reverse id (same
+ * RRR sets, sizes, digests, seeds, E_phys and level structure as the push form; coins / merges
+ * differ). Needs 16 B per edge of forward records (built on first use, kept with the graph); falls
+ * back to push when they do not fit. */
+#define BPT_FLAG_PULL 512u
 
 BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
                       void* stream, bpt_samples** out);
@@ -189,6 +198,9 @@ typedef struct {
     double ms_expand;       /* expansion time: CUDA events per launch (BPT_FLAG_PROFILE), else device
                                %globaltimer spans of the launches; LT walks: the walk kernel */
     double expand_bytes;    /* algorithmic bytes moved by expansion launches */
+    uint64_t pull_levels;   /* levels expanded by pull (BPT_FLAG_PULL) */
+    uint64_t pull_edge_reads; /* forward-edge records read by those levels (e_phys counts the push
+                               form's reads of every level, the work the oracle defines) */
 } bpt_samples_info;
 
 BPT_API bpt_status bpt_samples_get_info(const bpt_samples* s, bpt_samples_info* out);
@@ -200,6 +212,10 @@ BPT_API bpt_status bpt_occurrences(const bpt_samples* s, uint32_t* counts);
 /* Per level of every batch: {batch, level, raw_entries, kept_entries, edges_or_tasks, vc_pairs,
  * coins, atomics} as 8 u64 per row, host buffer (coins / atomics are schedule-dependent). *rows = number of rows available (written if rows_out != NULL). */
 BPT_API bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_rows, uint64_t* rows_out);
+/* Expansion time of every bpt_level_stats row, ms as f32 (CUDA events around each expansion
+ * launch), host buffer; only samples drawn with BPT_FLAG_PROFILE have them (*rows = 0 otherwise).
+ * Measurement aid for the roofline; *rows = rows available. */
+BPT_API bpt_status bpt_level_times(const bpt_samples* s, float* out, uint64_t cap_rows, uint64_t* rows_out);
 
 /* ---------------------------------------------------------------------------------
  * A5/A6: per-sample results for global sample ids [first, first+count), which must lie

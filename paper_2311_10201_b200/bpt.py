@@ -34,6 +34,7 @@ FLAG_LT_REWALK = 32  # LT sparse store: member lists by a second walk
 FLAG_LT_LEVELS = 64  # LT fused: per-level launches instead of one cooperative launch per batch
 FLAG_QUEUE = 128  # IC 64 colours: first-setter queue instead of the touched bitmap
 FLAG_UNSORTED = 256  # IC 64 colours: sample s in slot s (no start-vertex sort)
+FLAG_PULL = 512  # IC 64 colours: pull expansion of the heavy levels (direction switching)
 _STATUS = {0: "BPT_OK", -1: "BPT_EINVAL", -2: "BPT_ENOMEM", -3: "BPT_ECUDA", -4: "BPT_ENCCL", -5: "BPT_ESTATE"}
 
 _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
@@ -41,7 +42,7 @@ _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c
 
 class bpt_sample_opts(ctypes.Structure):
     _fields_ = [("batch_groups", _u32), ("poll_levels", _u32), ("flags", _u32), ("shard_world", _u32),
-                ("shard_rank", _u32), ("reserved", _u32)]
+                ("shard_rank", _u32), ("pull_permille", _u32)]
 
 
 class bpt_samples_info(ctypes.Structure):
@@ -51,7 +52,8 @@ class bpt_samples_info(ctypes.Structure):
                 ("e_phys", _u64), ("e_logical", _u64), ("members", _u64), ("levels_total", _u64),
                 ("frontier_entries", _u64), ("coins", _u64), ("atomics", _u64), ("store_bytes", _u64),
                 ("kernel_launches", _u64), ("expand_launches", _u64),
-                ("ms_total", ctypes.c_double), ("ms_expand", ctypes.c_double), ("expand_bytes", ctypes.c_double)]
+                ("ms_total", ctypes.c_double), ("ms_expand", ctypes.c_double), ("expand_bytes", ctypes.c_double),
+                ("pull_levels", _u64), ("pull_edge_reads", _u64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -74,6 +76,7 @@ _SIGS = {
     "bpt_sample_ex": ([_p, _i, _u64, _u32, _u64, ctypes.POINTER(bpt_sample_opts), _p, ctypes.POINTER(_p)], _i),
     "bpt_samples_get_info": ([_p, ctypes.POINTER(bpt_samples_info)], _i),
     "bpt_level_stats": ([_p, _p, _u64, _p], _i),
+    "bpt_level_times": ([_p, _p, _u64, _p], _i),
     "bpt_occurrences": ([_p, _p], _i),
     "bpt_rrr_sizes": ([_p, _u64, _u64, _p], _i),
     "bpt_rrr_digests": ([_p, _u64, _u64, _p], _i),
@@ -214,10 +217,10 @@ def bpt_graph_free(h) -> None:
 
 
 def bpt_sample(graph, model: int, theta: int, colors: int, seed: int, stream=None, batch_groups: int = 0,
-               poll_levels: int = 0, flags: int = 0, shard: tuple[int, int] | None = None):
+               poll_levels: int = 0, flags: int = 0, shard: tuple[int, int] | None = None, pull_permille: int = 0):
     h = _p()
     sw, sr = shard if shard else (0, 0)
-    opts = bpt_sample_opts(batch_groups, poll_levels, flags, sw, sr, 0)
+    opts = bpt_sample_opts(batch_groups, poll_levels, flags, sw, sr, pull_permille)
     _check(_lib.bpt_sample_ex(graph, model, theta, colors, seed, ctypes.byref(opts), _stream(stream),
                               ctypes.byref(h)))
     return h
@@ -235,6 +238,15 @@ def bpt_level_stats(h) -> np.ndarray:
     out = np.zeros((rows.value, 8), dtype=np.uint64)  # batch, level, raw, kept, work, vc, coins, atomics
     if rows.value:
         _check(_lib.bpt_level_stats(h, _ptr(out), rows.value, None))
+    return out
+
+
+def bpt_level_times(h) -> np.ndarray:
+    rows = _u64()
+    _check(_lib.bpt_level_times(h, None, 0, ctypes.byref(rows)))
+    out = np.zeros(rows.value, dtype=np.float32)  # expansion ms per bpt_level_stats row (profile mode)
+    if rows.value:
+        _check(_lib.bpt_level_times(h, _ptr(out), rows.value, None))
     return out
 
 
@@ -341,9 +353,12 @@ class Graph:
 
     def sample(self, theta: int, colors: int = 64, seed: int = 0, stream=None, batch_groups: int = 0,
                poll_levels: int = 0, profile: bool = False, shard: tuple[int, int] | None = None,
-               wide: bool = False, sparse: bool = False, flags: int = 0) -> "Samples":
+               wide: bool = False, sparse: bool = False, flags: int = 0, pull: bool = False,
+               pull_permille: int = 0) -> "Samples":
         flags |= (FLAG_PROFILE if profile else 0) | (FLAG_WIDE if wide else 0) | (FLAG_SPARSE if sparse else 0)
-        h = bpt_sample(self._h, self.model, theta, colors, seed, stream, batch_groups, poll_levels, flags, shard)
+        flags |= FLAG_PULL if pull else 0
+        h = bpt_sample(self._h, self.model, theta, colors, seed, stream, batch_groups, poll_levels, flags, shard,
+                       pull_permille)
         return Samples(self, h)
 
     def close(self):
@@ -378,6 +393,9 @@ class Samples:
 
     def level_stats(self) -> np.ndarray:
         return bpt_level_stats(self._h)
+
+    def level_times(self) -> np.ndarray:
+        return bpt_level_times(self._h)
 
     def select_seeds(self, k: int, seeds=None, gains=None):
         return bpt_select_seeds(self._h, k, seeds, gains)

@@ -14,6 +14,10 @@
 #include "internal.cuh"
 
 namespace bpt {
+#ifndef BPT_PULL_ALPHA
+#define BPT_PULL_ALPHA 1.0
+#endif
+constexpr double kPullAlpha = BPT_PULL_ALPHA;  // pull levels: push work >= kPullAlpha * m
 
 // ------------------------------------------------------------------ errors
 thread_local std::string g_last_error;
@@ -481,6 +485,15 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     size_t free_b = 0, total_b = 0;
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
     free_b += cached_bytes();  // the pool's cached blocks are released if an allocation needs them
+    // pull expansion of the heavy levels (BPT_FLAG_PULL; touched-bitmap form): forward records
+    // (16 B per edge, cached on the graph) + vertex-major frontier masks + the previous level's
+    // touched words, when they fit beside the batch (else push only)
+    bool pull = bitmap && (opt.flags & BPT_FLAG_PULL) && g.m > 0;
+    if (pull) {
+        const uint64_t extra = (g.pull_rec.p ? 0 : g.m * 16 + g.m * 24) + (uint64_t)want * n * 8 + want * tiles * 128;
+        if (extra > free_b / 2) pull = false;
+        else free_b -= extra;
+    }
     uint64_t raw_cap = 0, q_cap = 0, ts_cap = 0;
     while (!wide && slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
     while (!wide && slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
@@ -494,10 +507,17 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
         elog(8);
     BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
-    DevBuf vflag, qd, qmask, touched;
+    DevBuf vflag, qd, qmask, touched, Fbuf, FBbuf;
     if (bitmap) {
         touched.alloc(slots * tiles * 128);
         BPT_CUDA(cudaMemsetAsync(touched.p, 0, touched.bytes, st));  // the compaction clears what it reads
+    }
+    if (pull) {
+        build_pull_records(g, st);
+        Fbuf.alloc(slots * (uint64_t)n * 8);
+        FBbuf.alloc(slots * tiles * 128);
+        BPT_CUDA(cudaMemsetAsync(Fbuf.p, 0, Fbuf.bytes, st));  // then kept exact by every compaction
+        BPT_CUDA(cudaMemsetAsync(FBbuf.p, 0, FBbuf.bytes, st));
     }
     if (wide) {
         vflag.alloc((uint64_t)n * 4 + 4);
@@ -566,9 +586,18 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.umask_words = S.model == BPT_IC ? umask.bytes / 4 : 0;
     a.tstart_cap = ts_cap;
     a.lt_blocks_per_sm = 1;
+    a.pull = pull ? g.pull_rec.as<uint4>() : nullptr;
+    a.pull_edges = pull ? g.m : 0;
+    // pull when the level's push work reaches kPullAlpha x m (the pull form reads m
+    // forward records for all slots of the batch, the push form ~1 record per unit of work)
+    a.pull_min_work = (uint64_t)std::max(1.0, (opt.pull_permille ? opt.pull_permille / 1000.0 : kPullAlpha) * (double)g.m);
+    a.F = pull ? Fbuf.as<unsigned long long>() : nullptr;
+    a.FB = pull ? FBbuf.as<uint32_t>() : nullptr;
 
     const bool profile = (opt.flags & BPT_FLAG_PROFILE) != 0;
     double ev_ms = 0;
+    std::vector<float> ev_each;        // profile mode: ms of every expansion launch, in launch order
+    std::vector<uint64_t> ev_batch0;   // ... index of the first launch of every batch
     uint64_t ev_launches = 0, polls = 0;
     double wait_ms = 0;
     if (!profile) {
@@ -594,7 +623,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         struct PollCleanup { cudaEvent_t* e; ~PollCleanup() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); } } pc{poll_ev};
         static thread_local Ctl* poll_host = nullptr;
         if (!poll_host) BPT_CUDA(cudaMallocHost(&poll_host, 2 * sizeof(Ctl)));
+        std::vector<uint64_t> batch_ev0(nbatches);  // first event of every batch
         for (uint64_t b = 0; b < nbatches; ++b) {
+            batch_ev0[b] = evs.size();
             launch_init(a, st);
             int cur = 0;
             bool have_prev = false, done = false;
@@ -625,12 +656,13 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
             launch_next_batch(a, st);
         }
         BPT_CUDA(cudaStreamSynchronize(st));
-        for (auto& e : evs) {
-            float ms = 0;
-            BPT_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
-            ev_ms += ms;
+        ev_each.resize(evs.size());
+        for (size_t i = 0; i < evs.size(); ++i) {
+            BPT_CUDA(cudaEventElapsedTime(&ev_each[i], evs[i].first, evs[i].second));
+            ev_ms += ev_each[i];
         }
         ev_launches = evs.size();
+        ev_batch0.swap(batch_ev0);
     }
     const auto t_loop = clk::now();
     unsigned long long h_elog = 0;
@@ -656,16 +688,27 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     I.e_logical = S.model == BPT_IC ? h_elog : cf.vc;
     I.levels_total = cf.levels_total;
     I.levels_max = cf.levels_max;
+    I.pull_levels = cf.pull_levels;
+    I.pull_edge_reads = cf.pull_reads;
     I.batch_groups = (uint32_t)slots;
     I.batches = (uint32_t)nbatches;
     I.store_bytes = S.store.bytes;
     S.level_rows.clear();
+    S.level_ms.clear();
     double bytes = 0;
     for (uint32_t i = 0; i < rows; ++i) {
         const LevelRec& r = R[i];
+        if (profile) {  // batch b's level L ran as launch ev_batch0[b] + L
+            const uint64_t b = r.pad >> 32, L = r.pad & 0xffffffffull;
+            const uint64_t e = b < ev_batch0.size() ? ev_batch0[b] + L : ~0ull;
+            S.level_ms.push_back(e < ev_each.size() ? ev_each[e] : 0.f);
+        }
         const uint64_t kept = r.packed >> kPackShift, work = r.packed & kEdgeMask;
         const uint64_t raw_next = (i + 1 < rows && (R[i + 1].pad >> 32) == (r.pad >> 32)) ? R[i + 1].raw : 0;
-        bytes += (S.model == BPT_IC ? 16.0 : 24.0) * work + 8.0 * r.atomics + 24.0 * kept + 8.0 * raw_next;
+        if (r.pull)  // 16 B forward record + the slots' F[w] words per edge, U[u] per vertex and slot, merges
+            bytes += (16.0 + 8.0 * slots) * (double)r.pull_reads + 8.0 * slots * n + 8.0 * r.atomics + 8.0 * raw_next;
+        else
+            bytes += (S.model == BPT_IC ? 16.0 : 24.0) * work + 8.0 * r.atomics + 24.0 * kept + 8.0 * raw_next;
         const uint64_t row[kLevelCols] = {r.pad >> 32, r.pad & 0xffffffffull, r.raw, kept, work, r.vc, r.coins, r.atomics};
         S.level_rows.insert(S.level_rows.end(), row, row + kLevelCols);
     }
@@ -862,6 +905,15 @@ bpt_status bpt_graph_dims(const bpt_graph* g, uint32_t* n, uint64_t* m, int* mod
     });
 }
 
+// diagnostic (not in the header): the graph's pull records {u, w, e, thr}, m x 16 B into a host buffer
+BPT_API bpt_status bpt_debug_pull_records(const bpt_graph* g, void* host_out) {
+    return guarded([&] {
+        use_device(g->g.device);
+        build_pull_records(g->g, nullptr);
+        BPT_CUDA(cudaMemcpy(host_out, g->g.pull_rec.p, g->g.m * 16, cudaMemcpyDeviceToHost));
+    });
+}
+
 void bpt_graph_free(bpt_graph* g) {
     if (!g) return;
     int cur = -1;
@@ -945,6 +997,15 @@ bpt_status bpt_level_stats(const bpt_samples* s, uint64_t* out, uint64_t cap_row
         const uint64_t rows = s->s.level_rows.size() / kLevelCols;
         if (rows_out) *rows_out = rows;
         if (out) memcpy(out, s->s.level_rows.data(), std::min(rows, cap_rows) * kLevelCols * 8);
+    });
+}
+
+bpt_status bpt_level_times(const bpt_samples* s, float* out, uint64_t cap_rows, uint64_t* rows_out) {
+    return guarded([&] {
+        if (!s) fail(BPT_EINVAL, "samples is NULL");
+        const uint64_t rows = s->s.level_ms.size();
+        if (rows_out) *rows_out = rows;
+        if (out) memcpy(out, s->s.level_ms.data(), std::min(rows, cap_rows) * 4);
     });
 }
 

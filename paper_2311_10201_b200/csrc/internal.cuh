@@ -115,6 +115,10 @@ struct Graph {
     mutable uint32_t walk_epoch = 0;     // last epoch handed out
     mutable std::mutex walk_mu;
     mutable cudaEvent_t walk_ev = nullptr;
+    // IC pull expansion: the forward edges with their canonical reverse ids,
+    // uint4 {u, w, e, thr} per edge u -> w, grouped by u (built on first use, under pull_mu)
+    mutable DevBuf pull_rec;
+    mutable std::mutex pull_mu;
     ~Graph() { if (walk_ev) cudaEventDestroy(walk_ev); }
 };
 
@@ -129,8 +133,8 @@ struct LevelRec {
     unsigned int overflow;       // set if a queue overflowed
     unsigned long long pad;      // stats copy: batch << 32 | level
     unsigned int any;            // touched-bitmap mode: some colour reached this level
-    unsigned int pad2;
-    unsigned long long pad3;
+    unsigned int pull;           // 1: this level was expanded by the pull kernel
+    unsigned long long pull_reads;  // forward-edge records read by the pull expansion of this level
 };
 static_assert(sizeof(LevelRec) == 64, "LevelRec layout");
 constexpr int kPackShift = 36;
@@ -155,6 +159,7 @@ struct Samples {
     uint32_t n_pad = 0;
     bpt_samples_info info{};
     std::vector<uint64_t> level_rows;  // kLevelCols per row (bpt_level_stats)
+    std::vector<float> level_ms;       // expansion ms per level row (BPT_FLAG_PROFILE; bpt_level_times)
     // member lists of all local samples (selection on sparse stores), built on demand
     bool lists_built = false, lists_ok = false;
     bool digests_ready = false;
@@ -202,10 +207,10 @@ struct Ctl {
     uint32_t blocks_done;    // expansion blocks finished (the last one advances the level)
     uint32_t bar_count;      // grid barrier of the cooperative LT level loop: arrivals ...
     uint32_t bar_gen;        // ... and generation
-    uint32_t pad_;
+    uint32_t pull_levels;    // levels expanded by the pull kernel
     unsigned long long kernels_run;  // kernel executions inside the sampling graph, counted by the
                                      // kernels themselves (block 0, thread 0 of every launch)
-    unsigned long long pad2_;
+    unsigned long long pull_reads;   // forward-edge records read by pull levels
 };
 static_assert(sizeof(Ctl) % 16 == 0, "Ctl is read with 16-B vector loads");
 constexpr int kMaxLevels = 8192;
@@ -257,6 +262,14 @@ struct BatchArgs {
     uint64_t umask_words;     // words of umask[]
     uint64_t tstart_cap;      // entries of tstart[]
     int lt_blocks_per_sm;     // ... with this many blocks per SM
+    // pull expansion (touched-bitmap mode only): levels whose push work
+    // (frontier edge reads) is >= pull_min_work are expanded by streaming every forward edge u -> w
+    // once for all slots of the batch; the compaction keeps F exact for every level
+    const uint4* pull;        // forward records {u, w, e, thr} (nullptr: push only)
+    uint64_t pull_edges;      // forward records (= m)
+    uint64_t pull_min_work;
+    unsigned long long* F;    // frontier masks of the current level, vertex-major F[v * slots_max + slot]
+    uint32_t* FB;             // touched words of the previous level (same layout as touched)
 };
 #ifndef BPT_WIDE_BLOCKS
 #define BPT_WIDE_BLOCKS 2
@@ -272,6 +285,8 @@ void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t 
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
                      bool wide, bool umode);
+// k_build.cu: forward records of the pull expansion (Graph::pull_rec), from the reverse CSR
+void build_pull_records(const Graph& g, cudaStream_t st);
 // k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph
 void launch_init(const BatchArgs& a, cudaStream_t st);
 void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cudaStream_t st, cudaEvent_t ev0,

@@ -354,6 +354,30 @@ __global__ void __launch_bounds__(kLtThreads) k_lt_fix_tiles(const uint32_t* __r
     }
 }
 
+// Pull records: per reverse record e (row w): its source, its own index
+// and its row, the sort keys / payloads that regroup the edges by source u
+__global__ void k_pull_keys(const uint2* __restrict__ rec, const uint32_t* __restrict__ roff, uint32_t n, uint64_t m,
+                            uint32_t* __restrict__ src, uint32_t* __restrict__ eid, uint32_t* __restrict__ row) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = warp; w < n; w += nwarps)
+        for (uint64_t e = roff[w] + lane; e < roff[w + 1]; e += 32) {
+            src[e] = rec[e].x;
+            eid[e] = (uint32_t)e;
+            row[e] = (uint32_t)w;
+        }
+}
+
+// pull[i] = {u, w, e, thr(e)} from the records sorted by u ({e, w}) and the sorted keys (u)
+__global__ void k_pull_pack(const uint32_t* __restrict__ u_sorted, const uint2* __restrict__ ew, const uint2* __restrict__ rec,
+                            uint64_t m, uint4* __restrict__ pull) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 x = ew[i];
+        pull[i] = make_uint4(u_sorted[i], x.y, x.x, rec[x.x].y);
+    }
+}
+
 inline unsigned grid_for(uint64_t work, int threads) {
     uint64_t g = (work + threads - 1) / threads;
     uint64_t cap = (uint64_t)num_sms() * 16;
@@ -362,6 +386,49 @@ inline unsigned grid_for(uint64_t work, int threads) {
 }
 
 }  // namespace
+
+// Stable LSD radix sort of m items by key (keys < key_bound), carrying two u32 payloads: the
+// sorted records {a, b} go to rec_out, the sorted keys to keys_out (returned). b comes from wq,
+// or from wf as Q1.31 thresholds (reading C-5) when wf is given.
+static const uint32_t* radix_sort_records(const uint32_t* keys, const uint32_t* pa, const float* wf, const uint32_t* wq,
+                                          uint64_t m, uint64_t key_bound, uint32_t* keys_out, uint2* rec_out,
+                                          cudaStream_t st) {
+    int bits = 0;
+    while (bits < 32 && (1ull << bits) < key_bound) ++bits;
+    const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
+    const uint64_t ntiles = (m + kRsTile - 1) / kRsTile;
+    DevBuf hist(ntiles * kRadix * 4), tmp(scan_temp_bytes(ntiles * kRadix));
+    DevBuf k1(m * 4 + 4), s1(m * 4 + 4), s0(m * 4 + 4), w0(m * 4 + 4), w1(m * 4 + 4);
+    for (auto fn : {k_radix_pass<true, false>, k_radix_pass<false, false>, k_radix_pass<true, true>,
+                    k_radix_pass<false, true>})
+        BPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
+    const uint32_t* kin = keys;
+    const uint32_t* sin = pa;
+    const uint32_t* win = wq;
+    uint32_t* sbuf[2] = {s1.as<uint32_t>(), s0.as<uint32_t>()};
+    uint32_t* wbuf[2] = {w1.as<uint32_t>(), w0.as<uint32_t>()};
+    for (int p = 0; p < passes; ++p) {
+        const int shift = 8 * p;
+        const bool first = p == 0, last = p == passes - 1;
+        k_radix_hist<<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, m, shift, hist.as<uint32_t>(), ntiles);
+        count_launch();
+        exclusive_scan_u32(hist.as<uint32_t>(), hist.as<uint32_t>(), ntiles * kRadix, tmp.p, st);
+        // keys ping-pong between k1 and keys_out so that the last pass writes keys_out
+        uint32_t *ko = ((passes - 1 - p) % 2 == 0) ? keys_out : k1.as<uint32_t>(), *so = sbuf[p & 1], *wo = wbuf[p & 1];
+        const float* wfi = first ? wf : nullptr;
+        auto* fn = first ? (last ? k_radix_pass<true, true> : k_radix_pass<true, false>)
+                         : (last ? k_radix_pass<false, true> : k_radix_pass<false, false>);
+        fn<<<(unsigned)ntiles, kRsThreads, kPassSmem, st>>>(kin, sin, wfi, win, m, shift, hist.as<uint32_t>(), ntiles, ko,
+                                                           so, wo, rec_out);
+        count_launch();
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_radix_pass");
+        kin = ko;
+        sin = so;
+        win = wo;
+    }
+    BPT_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
+    return kin;
+}
 
 void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_col, const float* d_wf,
                        const uint32_t* d_wq, cudaStream_t st) {
@@ -389,44 +456,12 @@ void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_co
     g.rec.alloc((m ? m : 1) * sizeof(uint2));
 
     // stable LSD radix sort of the forward edges by dst, carrying {src, thr}
-    DevBuf k1(m * 4 + 4), s0(m * 4 + 4), s1(m * 4 + 4), w0(m * 4 + 4), w1(m * 4 + 4), k2(m * 4 + 4);
+    DevBuf s0(m * 4 + 4), k2(m * 4 + 4);
     const uint32_t* sorted_keys = d_col;
     if (m) {
         k_expand_rows<<<grid_for((uint64_t)n * 32, 256), 256, 0, st>>>(d_row_ptr, n, s0.as<uint32_t>());
         count_launch();
-        int bits = 0;
-        while (bits < 32 && (1ull << bits) < (uint64_t)n) ++bits;
-        const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
-        const uint64_t ntiles = (m + kRsTile - 1) / kRsTile;
-        DevBuf hist(ntiles * kRadix * 4), tmp(scan_temp_bytes(ntiles * kRadix));
-        for (auto fn : {k_radix_pass<true, false>, k_radix_pass<false, false>, k_radix_pass<true, true>,
-                        k_radix_pass<false, true>})
-            BPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
-        const uint32_t* kin = d_col;
-        const uint32_t* sin = s0.as<uint32_t>();
-        const uint32_t* win = d_wq;
-        uint32_t* kbuf[2] = {k1.as<uint32_t>(), k2.as<uint32_t>()};
-        uint32_t* sbuf[2] = {s1.as<uint32_t>(), s0.as<uint32_t>()};
-        uint32_t* wbuf[2] = {w1.as<uint32_t>(), w0.as<uint32_t>()};
-        for (int p = 0; p < passes; ++p) {
-            const int shift = 8 * p;
-            const bool first = p == 0, last = p == passes - 1;
-            k_radix_hist<<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, m, shift, hist.as<uint32_t>(), ntiles);
-            count_launch();
-            exclusive_scan_u32(hist.as<uint32_t>(), hist.as<uint32_t>(), ntiles * kRadix, tmp.p, st);
-            uint32_t *ko = kbuf[p & 1], *so = sbuf[p & 1], *wo = wbuf[p & 1];
-            const float* wfi = first ? d_wf : nullptr;
-            auto* fn = first ? (last ? k_radix_pass<true, true> : k_radix_pass<true, false>)
-                             : (last ? k_radix_pass<false, true> : k_radix_pass<false, false>);
-            fn<<<(unsigned)ntiles, kRsThreads, kPassSmem, st>>>(kin, sin, wfi, win, m, shift, hist.as<uint32_t>(),
-                                                               ntiles, ko, so, wo, g.rec.as<uint2>());
-            count_launch();
-            ::bpt::check_cuda(cudaGetLastError(), "launch k_radix_pass");
-            kin = ko;
-            sin = so;
-            win = wo;
-        }
-        sorted_keys = kin;
+        sorted_keys = radix_sort_records(d_col, s0.as<uint32_t>(), d_wf, d_wq, m, n, k2.as<uint32_t>(), g.rec.as<uint2>(), st);
     }
     k_row_offsets<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(sorted_keys, m, n, g.roff.as<uint32_t>());
     count_launch();
@@ -446,6 +481,29 @@ void build_reverse_csr(Graph& g, const uint64_t* d_row_ptr, const uint32_t* d_co
             fail(BPT_EINVAL, "LT: sum of in-edge thresholds of vertex " + std::to_string(h.bad_lt) + " exceeds 2^31");
     }
     BPT_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
+}
+
+
+// The forward edges regrouped by source with their canonical reverse ids (reading C-4): a stable
+// radix sort of the reverse records by source u, so inside a group the edges keep reverse-CSR
+// order. Built once per graph, on first use by a pull-enabled bpt_sample (Graph::pull_rec).
+void build_pull_records(const Graph& g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g.pull_mu);
+    if (g.pull_rec.p || !g.m) return;
+    const uint64_t m = g.m;
+    DevBuf src(m * 4), eid(m * 4), row(m * 4), us(m * 4), ew(m * 8);
+    k_pull_keys<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.rec.as<uint2>(), g.roff.as<uint32_t>(), g.n, m,
+                                                                 src.as<uint32_t>(), eid.as<uint32_t>(), row.as<uint32_t>());
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_pull_keys");
+    radix_sort_records(src.as<uint32_t>(), eid.as<uint32_t>(), nullptr, row.as<uint32_t>(), m, g.n, us.as<uint32_t>(),
+                       ew.as<uint2>(), st);
+    DevBuf out(m * 16);
+    k_pull_pack<<<grid_for(m, 256), 256, 0, st>>>(us.as<uint32_t>(), ew.as<uint2>(), g.rec.as<uint2>(), m, out.as<uint4>());
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_pull_pack");
+    BPT_CUDA(cudaStreamSynchronize(st));
+    g.pull_rec = std::move(out);
 }
 
 }  // namespace bpt

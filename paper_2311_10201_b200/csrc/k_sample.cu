@@ -77,6 +77,12 @@ __device__ __forceinline__ uint2 ld_stream(const uint2* p) {
                  : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(policy_evict_first()));
     return r;
 }
+__device__ __forceinline__ uint4 ld_stream4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(policy_evict_first()));
+    return r;
+}
 // coherent (L2) load with evict-last: U is OR-merged by other warps during the same launch (a stale
 // value only skips fewer coins)
 __device__ __forceinline__ uint2 ld_keep_u64(const unsigned long long* p) {
@@ -254,7 +260,8 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
                 for (uint32_t k = k0 + wid; k < k0 + kScreen; k += kWarps) {
                     const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
                     if (t >= ntiles_all) break;
-                    const uint32_t w = LDX(a.touched + t * 32 + lane);
+                    uint32_t w = LDX(a.touched + t * 32 + lane);
+                    if (a.F) w |= LDX(a.FB + t * 32 + lane);  // pull: leavers of the previous frontier
                     if (__any_sync(kFull, w != 0) && lane == 0) nonempty[atomicAdd(&n_nonempty, 1u)] = (uint32_t)t;
                 }
                 __syncthreads();
@@ -275,6 +282,20 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
             uint32_t wv[kCompItems];
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) wv[it] = LDX(wp + 8 * it);
+            if (a.F) {
+                // pull: F[v][slot] holds the frontier masks of the current level; the vertices of the
+                // previous level's frontier that are not in this one are cleared here (FB = the previous
+                // level's touched words), the new ones are written below with their masks
+                uint32_t* fp = a.FB + t * 32 + wid;
+#pragma unroll
+                for (int it = 0; it < kCompItems; ++it) {
+                    const uint32_t pv = LDX(fp + 8 * it);
+                    if (((pv & ~wv[it]) >> lane) & 1u)
+                        a.F[(size_t)(vbase + it * kThreads + threadIdx.x) * a.slots_max + slot] = 0ull;
+                    __syncwarp();
+                    if (lane == it && pv != wv[it]) fp[8 * it] = wv[it];
+                }
+            }
 #pragma unroll
             for (int it = 0; it < kCompItems; ++it) {
                 const bool on = (wv[it] >> lane) & 1u;
@@ -309,6 +330,7 @@ __device__ __forceinline__ void compact_body(const BatchArgs& a, uint32_t* __res
                     const unsigned long long u = LDX(&U[iu]);
                     mask[it] = u & ~LDX(&U[iv]);
                     U[iv] = u;
+                    if (a.F) a.F[(size_t)v * a.slots_max + slot] = mask[it];
                 } else if (a.colors == 64) {
                     const ulonglong2 x = LDX(p);
                     mask[it] = x.y;
@@ -487,6 +509,8 @@ __device__ __forceinline__ void advance_level(const BatchArgs& a, cudaGraphCondi
     c->vc = C.vc + R.vc;
     c->coins = C.coins + R.coins;
     c->atomics = C.atomics + R.atomics;
+    c->pull_reads = C.pull_reads + R.pull_reads;
+    c->pull_levels = C.pull_levels + R.pull;
     if (C.t_start != ~0ull && C.t_end > C.t_start) c->expand_ns = C.expand_ns + (C.t_end - C.t_start);
     if (C.c_start != ~0ull && C.c_end > C.c_start) c->compact_ns = C.compact_ns + (C.c_end - C.c_start);
     c->t_start = ~0ull;
@@ -529,6 +553,11 @@ __device__ __forceinline__ void finish_expand(const BatchArgs& a, cudaGraphCondi
             advance_level(a, h_level, use_cond);
         }
     }
+}
+
+// pull or push for this level (both expansion kernels of a level take the same decision)
+__device__ __forceinline__ bool pull_level(const BatchArgs& a, const LevelRec* L) {
+    return a.pull != nullptr && !L->overflow && (L->packed & kEdgeMask) >= a.pull_min_work;
 }
 
 // IC, Listing 1 lines 9-15: for each frontier entry (v, slot, mask) and each reverse edge e
@@ -905,66 +934,13 @@ __device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, ui
     return 8u * byte + ((sel8[v] >> (3 * (r - before))) & 7u);
 }
 
-template <bool kWhole>
-__device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane, uint32_t le_mask,
-                                               uint32_t unit, uint32_t rem, uint32_t jc0, uint32_t mword,
-                                               uint64_t gblk0, unsigned long long& coins,
-                                               unsigned long long& atoms, bool& any_pass) {
-    const uint32_t t0l = unit * (uint32_t)kUnitBm;  // mod 2^32: edge ids are t + delta (mod 2^32)
-    // entry-start words of the unit (prefetched one unit ahead: lane w holds word w)
-    uint32_t mw[kWinBm];
-#pragma unroll
-    for (int w = 0; w < kWinBm; ++w) mw[w] = __shfl_sync(kFull, mword, w);
-    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;  // cleared for the next level
-    mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
-    uint32_t jl[kWinBm];
-    uint32_t before = jc0;
-#pragma unroll
-    for (int w = 0; w < kWinBm; ++w) {
-        jl[w] = before + __popc(mw[w] & le_mask);
-        before += __popc(mw[w]);
-    }
-    uint4 ent[kWinBm];
-    uint2 rc[kWinBm];
-    BPT_CHECK((uint64_t)unit * kWinBm + kWinBm <= a.umask_words, 1);
-#pragma unroll
-    for (int w = 0; w < kWinBm; ++w) {
-        BPT_CHECK(((kWhole || 32u * w + lane < rem) ? jl[w] : jc0) < a.q_cap, 2);
-        ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
-    }
-#pragma unroll
-    for (int w = 0; w < kWinBm; ++w) {
-        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
-        BPT_CHECK((uint32_t)(t0l + i + ent[w].x) < a.m, 3);
-        BPT_CHECK(ent[w].y < a.slots_max, 4);
-        rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
-    }
-    // ---- gather of U[u] = V[u] | N[u] (union layout), live colours, compacted list of live items
-    const uint32_t lt_mask = le_mask >> 1;  // lanes below this one
-    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
-    uint32_t nlive = 0;
-#pragma unroll
-    for (int w = 0; w < kWinBm; ++w) {
-        const uint32_t vidx = ent[w].y * a.n + rc[w].x;
-        BPT_CHECK(rc[w].x < a.n, 5);
-        const uint2 uu = ld_keep_u64(&U[vidx]);
-        uint32_t lo = ent[w].z & ~uu.x;
-        uint32_t hi = ent[w].w & ~uu.y;
-        if (!kWhole && 32u * w + lane >= rem) lo = hi = 0;
-        const bool lv = (lo | hi) != 0;
-        const uint32_t bal = __ballot_sync(kFull, lv);
-        if (lv) {
-            const uint32_t pos = nlive + __popc(bal & lt_mask);
-            BPT_CHECK(pos < (uint32_t)kUnitBm, 6);
-            W.A[pos] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, lo, hi);
-            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,  // colour-0 sample / slot
-                                  ent[w].y * a.tiles * 32 + (rc[w].x >> 5), rc[w].x & 31u);
-        }
-        nlive += __popc(bal);
-    }
-    if (nlive == 0) return;
-    __syncwarp();
-    // ---- coins and merges, one chunk of <= 32 live items at a time (one live item per lane)
+// Coins and merges of the live items W.A / W.B[0, nlive) of one warp (shared by the push and the
+// pull expansion): item = {edge id, thr, live colours lo, hi} / {colour-0 slot index, U index,
+// touched word, bit}. One chunk of <= 32 live items at a time (one live item per lane).
+__device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
+                                                   uint32_t nlive, unsigned long long& coins,
+                                                   unsigned long long& atoms, bool& any_pass) {
+    const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
     for (uint32_t c0 = 0; c0 < nlive; c0 += 32) {
         const uint32_t j = c0 + lane;
         const bool has = j < nlive;
@@ -1043,6 +1019,68 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
     }
 }
 
+template <bool kWhole>
+__device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane, uint32_t le_mask,
+                                               uint32_t unit, uint32_t rem, uint32_t jc0, uint32_t mword,
+                                               uint64_t gblk0, unsigned long long& coins,
+                                               unsigned long long& atoms, bool& any_pass) {
+    const uint32_t t0l = unit * (uint32_t)kUnitBm;  // mod 2^32: edge ids are t + delta (mod 2^32)
+    // entry-start words of the unit (prefetched one unit ahead: lane w holds word w)
+    uint32_t mw[kWinBm];
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) mw[w] = __shfl_sync(kFull, mword, w);
+    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;  // cleared for the next level
+    mw[0] &= ~1u;  // an entry starting at item 0 is jc0 itself
+    uint32_t jl[kWinBm];
+    uint32_t before = jc0;
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        jl[w] = before + __popc(mw[w] & le_mask);
+        before += __popc(mw[w]);
+    }
+    uint4 ent[kWinBm];
+    uint2 rc[kWinBm];
+    BPT_CHECK((uint64_t)unit * kWinBm + kWinBm <= a.umask_words, 1);
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        BPT_CHECK(((kWhole || 32u * w + lane < rem) ? jl[w] : jc0) < a.q_cap, 2);
+        ent[w] = __ldg(&a.q[(kWhole || 32u * w + lane < rem) ? jl[w] : jc0]);
+    }
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        BPT_CHECK((uint32_t)(t0l + i + ent[w].x) < a.m, 3);
+        BPT_CHECK(ent[w].y < a.slots_max, 4);
+        rc[w] = ld_stream(&a.rec[t0l + i + ent[w].x]);
+    }
+    // ---- gather of U[u] = V[u] | N[u] (union layout), live colours, compacted list of live items
+    const uint32_t lt_mask = le_mask >> 1;  // lanes below this one
+    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
+    uint32_t nlive = 0;
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        const uint32_t vidx = ent[w].y * a.n + rc[w].x;
+        BPT_CHECK(rc[w].x < a.n, 5);
+        const uint2 uu = ld_keep_u64(&U[vidx]);
+        uint32_t lo = ent[w].z & ~uu.x;
+        uint32_t hi = ent[w].w & ~uu.y;
+        if (!kWhole && 32u * w + lane >= rem) lo = hi = 0;
+        const bool lv = (lo | hi) != 0;
+        const uint32_t bal = __ballot_sync(kFull, lv);
+        if (lv) {
+            const uint32_t pos = nlive + __popc(bal & lt_mask);
+            BPT_CHECK(pos < (uint32_t)kUnitBm, 6);
+            W.A[pos] = make_uint4(t0l + 32u * w + lane + ent[w].x, rc[w].y, lo, hi);
+            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + ent[w].y)), vidx,  // colour-0 sample / slot
+                                  ent[w].y * a.tiles * 32 + (rc[w].x >> 5), rc[w].x & 31u);
+        }
+        nlive += __popc(bal);
+    }
+    if (nlive == 0) return;
+    __syncwarp();
+    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+}
+
 #ifndef BPT_BM_MINB
 #define BPT_BM_MINB 4  // 64 registers: no spills; 4 x 8 warps per SM (measured: -4% vs 5 blocks at 48)
 #endif
@@ -1057,6 +1095,7 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     const uint64_t gblk0 = a.slot_sample ? ctl->blk0 : ctl->gblk0;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
+    if (pull_level(a, L)) return;  // k_expand_pull expands this level
     const unsigned long long packed = L->packed;
     const uint64_t nq = packed >> kPackShift;
     const uint64_t total = packed & kEdgeMask;
@@ -1115,6 +1154,116 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     unsigned long long at = block_sum_ull(atoms, red);
     if (threadIdx.x == 0 && at) atomicAdd(&((LevelRec*)L)->atomics, at);
     finish_expand(a, h_level, use_cond, active);
+}
+
+
+// ------------------------------------------------------------------------ pull expansion (IC)
+// SURVEY §8(f) NEXT #1 (direction switching): a level whose push work (the
+// frontier's reverse-edge reads, summed over the batch's slots) is >= pull_min_work is expanded
+// the other way round. Every forward edge u -> w (Graph::pull_rec {u, w, e, thr}, grouped by u)
+// is read ONCE for all slots of the batch: live = F[w][slot] & ~U[slot][u] (F: the frontier masks
+// the compaction keeps exact, vertex-major so one 32-B sector serves 4 slots), and the live
+// (edge, slot) items go through the same coins (keyed by the canonical reverse id e, reading
+// C-4, so the RRR sets are those of the push form) and merges as the push expansion. At the
+// heavy levels the push form reads ~3.5 m reverse edges per batch (C2); the pull form reads m.
+__device__ __forceinline__ void pull_window(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
+                                            const uint4 r, bool valid, uint32_t nslots, uint64_t gblk0,
+                                            unsigned long long& coins, unsigned long long& atoms, bool& any_pass) {
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
+    BPT_CHECK(!valid || (r.x < a.n && r.y < a.n && r.z < a.m), 13);
+    unsigned long long f[4] = {0ull, 0ull, 0ull, 0ull};
+    if (valid) {
+        const unsigned long long* Fw = a.F + (size_t)r.y * a.slots_max;
+        if (a.slots_max == 4) {
+            const ulonglong2 f01 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw));
+            const ulonglong2 f23 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw) + 1);
+            f[0] = f01.x; f[1] = f01.y; f[2] = f23.x; f[3] = f23.y;
+        } else {
+#pragma unroll
+            for (uint32_t sl = 0; sl < 4; ++sl) f[sl] = sl < nslots ? __ldg(Fw + sl) : 0ull;
+        }
+    }
+    uint32_t nlive = 0;
+#pragma unroll
+    for (uint32_t sl = 0; sl < 4; ++sl) {
+        if (sl >= nslots) break;
+        uint32_t lo = (uint32_t)f[sl], hi = (uint32_t)(f[sl] >> 32);
+        const uint32_t vidx = sl * a.n + r.x;
+        if (lo | hi) {
+            const uint2 uu = ld_keep_u64(&U[vidx]);
+            lo &= ~uu.x;
+            hi &= ~uu.y;
+        }
+        const bool lv = (lo | hi) != 0;
+        const uint32_t bal = __ballot_sync(kFull, lv);
+        if (lv) {
+            const uint32_t pos = nlive + __popc(bal & lt_mask);
+            W.A[pos] = make_uint4(r.z, r.w, lo, hi);
+            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), vidx, sl * a.tiles * 32 + (r.x >> 5), r.x & 31u);
+        }
+        nlive += __popc(bal);
+    }
+    if (nlive == 0) return;
+    __syncwarp();
+    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+}
+
+__global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_pull(BatchArgs a, cudaGraphConditionalHandle h_level,
+                                                                int use_cond) {
+    count_self(a.ctl);
+    if (!a.ctl->cont) return;
+    Ctl* ctl = a.ctl;
+    const uint32_t level = ctl->level;
+    LevelRec* L = &a.lv[level];
+    LevelRec* Ln = &a.lv[level + 1];
+    if (!pull_level(a, L)) return;  // k_expand_bm expands this level
+    if (threadIdx.x == 0) atomicMin(&ctl->t_start, global_ns());
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        L->pull = 1;
+        L->pull_reads = a.pull_edges;
+    }
+    const uint64_t gblk0 = a.slot_sample ? ctl->blk0 : ctl->gblk0;
+    const uint32_t nslots = ctl->slots;
+    {   // the compaction marked the entry starts of this level's push units; the push kernel, which
+        // clears them as it reads them, does not run on a pull level
+        const uint64_t words = umin64(((L->packed & kEdgeMask) + 31) / 32 + kWinBm, a.umask_words);
+        for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < words; i += (uint64_t)gridDim.x * kThreads)
+            a.umask[i] = 0;
+    }
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
+    __shared__ unsigned long long red[kWarps];
+    __shared__ uint32_t sel8[256];
+    {
+        uint32_t t = 0;
+        for (uint32_t p = 0, j = 0; p < 8; ++p)
+            if ((threadIdx.x >> p) & 1u) t |= p << (3 * j++);
+        sel8[threadIdx.x] = t;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned long long coins = 0, atoms = 0;
+    bool any_pass = false;
+    const uint64_t nwin = (a.pull_edges + 31) / 32;
+    const uint64_t stride = (uint64_t)gridDim.x * kWarps;
+    uint64_t win = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    // the next window's records are loaded one window ahead
+    uint4 nx = make_uint4(0, 0, 0, 0);
+    if (win < nwin && win * 32 + lane < a.pull_edges) nx = ld_stream4(&a.pull[win * 32 + lane]);
+    for (; win < nwin; win += stride) {
+        const uint4 r = nx;
+        const bool valid = win * 32 + lane < a.pull_edges;
+        const uint64_t nw = win + stride;
+        if (nw < nwin && nw * 32 + lane < a.pull_edges) nx = ld_stream4(&a.pull[nw * 32 + lane]);
+        pull_window(a, W, sel8, lane, r, valid, nslots, gblk0, coins, atoms, any_pass);
+    }
+    if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
+    unsigned long long ct = block_sum_ull(coins, red);
+    if (threadIdx.x == 0 && ct) atomicAdd(&L->coins, ct);
+    unsigned long long at = block_sum_ull(atoms, red);
+    if (threadIdx.x == 0 && at) atomicAdd(&L->atomics, at);
+    finish_expand(a, h_level, use_cond, gridDim.x);
 }
 
 // ------------------------------------------------------------------------ wide fusion (IC)
@@ -2041,6 +2190,7 @@ __global__ void k_next_batch(BatchArgs a, cudaGraphConditionalHandle h_batch, in
 int g_expand_grid = 0;
 int g_expand_grid_w = 0;
 int g_expand_grid_b = 0;
+int g_expand_grid_p = 0;
 int g_expand_grid_lt = 0;
 int g_levels_per_sm_lt = 0;  // co-resident blocks per SM of the cooperative LT loop
 int g_compact_grid = 0;
@@ -2152,6 +2302,12 @@ int expand_grid() {
         BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_expand_bm, kThreads,
                                                                sizeof(BmScratch) * kWarps));
         g_expand_grid_b = num_sms() * (per_sm_b > 0 ? per_sm_b : 1);
+        int per_sm_p = 0;
+        BPT_CUDA(cudaFuncSetAttribute(k_expand_pull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(BmScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, k_expand_pull, kThreads,
+                                                               sizeof(BmScratch) * kWarps));
+        g_expand_grid_p = num_sms() * (per_sm_p > 0 ? per_sm_p : 1);
         int per_sm_w = 0;
         BPT_CUDA(cudaFuncSetAttribute(k_expand_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(WarpScratchW) * kWarps)));
@@ -2209,8 +2365,13 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
     }
     compact_kernel(a)<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap);
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
-    if (a.model == BPT_IC && a.touched)
+    if (a.model == BPT_IC && a.touched) {
         k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        if (a.pull) {
+            k_expand_pull<<<g_expand_grid_p, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, h0, 0);
+            count_launch();
+        }
+    }
     else if (a.model == BPT_IC && a.colors == 64)
         k_expand_ic<true><<<g_expand_grid, kThreads, sizeof(WarpScratch) * kWarps, st>>>(a, tstart, h0, 0);
     else if (a.model == BPT_IC)
@@ -2312,6 +2473,11 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
         : add_kernel(lbody, &n_cmp, (void*)k_expand_lt, dim3(g_expand_grid_lt), dim3(kThreads), sizeof(SmemTile), exp_args);
+    if (a.model == BPT_IC && a.touched && a.pull) {  // pull levels: the push kernel returns at once
+        void* pull_args[] = {&args, &h_level, &one};
+        add_kernel(lbody, &n_exp, (void*)k_expand_pull, dim3(g_expand_grid_p), dim3(kThreads), sizeof(BmScratch) * kWarps,
+                   pull_args);
+    }
     // the expansion's last block advances the level and sets the loop condition
     // finalize + count, then next batch
     cudaGraphNode_t n_store;

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", bpt.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\bT (bpt_[a-z_0-9]+)", out))
     assert set(bpt.header_symbols()) <= exported
-    assert bpt.bpt_abi_version() == 1
+    assert bpt.bpt_abi_version() == 2
 
 
 def test_header_constants_match_binding():
@@ -38,7 +38,7 @@ def test_header_constants_match_binding():
     defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z_]+) (\w+)", hdr)}
     assert defs == {f"BPT_{name}": getattr(bpt, name) for name in
                     ("FLAG_PROFILE", "FLAG_WIDE", "FLAG_SPARSE", "FLAG_LT_FUSED", "FLAG_LT_DENSE", "FLAG_LT_REWALK",
-                     "FLAG_LT_LEVELS", "FLAG_QUEUE", "FLAG_UNSORTED")}
+                     "FLAG_LT_LEVELS", "FLAG_QUEUE", "FLAG_UNSORTED", "FLAG_PULL")}
     flags = list(defs.values())
     assert len(set(flags)) == len(flags) and all(f & (f - 1) == 0 for f in flags)  # distinct single bits
     enums = dict((k, int(v)) for k, v in re.findall(r"(BPT_E[A-Z]+|BPT_OK)\s*=\s*(-?\d+)", hdr))

@@ -709,3 +709,58 @@ def test_sorted_start_slots(bpt, c2_small):
         assert np.array_equal(sh.digests(s0, s1 - s0), ref["digests"][s0:s1])
         order = sorted_slots(row_ptr, col, cfg.n, s1, cfg.seed, s0=s0)
         assert sh.info["e_phys"] == sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64))
+
+
+# ------------------------------------------------------------------ pull expansion
+
+def _level_cols(s):
+    """Per-level structure that does not depend on the expansion direction: batch, level,
+    discovered, kept entries, push work, (vertex, colour) pairs."""
+    return s.level_stats()[:, :6]
+
+
+@pytest.mark.parametrize("permille", [1, 300, 0])
+def test_pull_levels_parity(bpt, c2_small, permille):
+    """BPT_FLAG_PULL (direction switching): levels whose push work reaches
+    permille/1000 x m are expanded by streaming every forward edge once for all slots of the batch
+    (coins keyed by the edge's canonical reverse id). permille = 1 pulls nearly every level,
+    300 mixes both directions inside a batch, 0 is the default threshold. RRR sets, sizes, digests,
+    lists, seeds, gains, sigma, E_phys and the per-level structure equal the oracle / the push form."""
+    cfg, row_ptr, col, thr, ref = c2_small
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    push = g.sample(cfg.theta, seed=cfg.seed)
+    s = g.sample(cfg.theta, seed=cfg.seed, pull=True, pull_permille=permille)
+    check_full(bpt, s, ref, cfg.theta)
+    seeds, gains, sigma = s.select_seeds(cfg.k)
+    assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+    assert sigma == oracle.sigma_hat(cfg.n, int(ref["gains"].sum()), cfg.theta)
+    info, pinfo = s.info, push.info
+    assert info["e_phys"] == pinfo["e_phys"] and info["e_logical"] == int(ref["elog"].sum())
+    assert info["members"] == pinfo["members"]
+    assert np.array_equal(_level_cols(s), _level_cols(push))
+    assert np.array_equal(s.occurrences(), push.occurrences())
+    if permille == 1:  # every level with >= m / 1000 work
+        lim = max(1, int(1 / 1000.0 * cfg.m))
+        assert info["pull_levels"] == sum(int(r[4]) >= lim for r in push.level_stats())
+    if permille in (1, 300):
+        assert 0 < info["pull_levels"] and info["pull_edge_reads"] == info["pull_levels"] * cfg.m
+    assert pinfo["pull_levels"] == 0
+    s.close()
+    push.close()
+
+
+def test_pull_c1_and_ragged(bpt):
+    """Pull on C1 (all 1,024 lists; batches of 4, 3 and 1 slots) and ragged theta, unsorted slots
+    and the host-driven profile loop: same sets and seeds as the oracle."""
+    cfg = graphgen.CONFIGS["C1"]
+    row_ptr, col, thr = graphgen.make_graph(cfg)
+    g = bpt.Graph(row_ptr, col, w_q31=thr)
+    for theta, bg, flags in ((cfg.theta, 0, 0), (3 * 64 + 5, 3, 0), (cfg.theta, 1, bpt.FLAG_UNSORTED),
+                             (200, 0, bpt.FLAG_PROFILE)):
+        ref = oracle_all(row_ptr, col, thr, oracle.IC, theta, cfg.seed, k=cfg.k)
+        s = g.sample(theta, seed=cfg.seed, batch_groups=bg, flags=flags, pull=True, pull_permille=1)
+        check_full(bpt, s, ref, theta)
+        seeds, gains, _ = s.select_seeds(cfg.k)
+        assert np.array_equal(seeds, ref["seeds"]) and np.array_equal(gains, ref["gains"])
+        assert s.info["pull_levels"] > 0
+        s.close()
