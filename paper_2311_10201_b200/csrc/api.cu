@@ -588,6 +588,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.lt_blocks_per_sm = 1;
     a.pull = pull ? g.pull_rec.as<uint4>() : nullptr;
     a.pull_edges = pull ? g.m : 0;
+    a.pull_seg = pull ? g.pull_seg.as<uint4>() : nullptr;
+    a.pull_nseg = pull ? g.pull_nseg : 0;
     // pull when the level's push work reaches kPullAlpha x m (the pull form reads m
     // forward records for all slots of the batch, the push form ~1 record per unit of work)
     a.pull_min_work = (uint64_t)std::max(1.0, (opt.pull_permille ? opt.pull_permille / 1000.0 : kPullAlpha) * (double)g.m);

@@ -118,6 +118,10 @@ struct Graph {
     // IC pull expansion: the forward edges with their canonical reverse ids,
     // uint4 {u, w, e, thr} per edge u -> w, grouped by u (built on first use, under pull_mu)
     mutable DevBuf pull_rec;
+    // ... and its work list: every row u cut into segments of <= kPullSeg edges, uint4 {u, first
+    // record, length, 0}, longest first (a warp's 32 segments have nearly equal lengths)
+    mutable DevBuf pull_seg;
+    mutable uint64_t pull_nseg = 0;
     mutable std::mutex pull_mu;
     ~Graph() { if (walk_ev) cudaEventDestroy(walk_ev); }
 };
@@ -214,6 +218,7 @@ struct Ctl {
 };
 static_assert(sizeof(Ctl) % 16 == 0, "Ctl is read with 16-B vector loads");
 constexpr int kMaxLevels = 8192;
+constexpr uint32_t kPullSeg = 64;  // edges per pull segment (early exit per colour inside a segment)
 
 struct BatchArgs {
     const uint32_t* roff;
@@ -267,6 +272,8 @@ struct BatchArgs {
     // once for all slots of the batch; the compaction keeps F exact for every level
     const uint4* pull;        // forward records {u, w, e, thr} (nullptr: push only)
     uint64_t pull_edges;      // forward records (= m)
+    const uint4* pull_seg;    // row segments {u, first record, length, 0}, longest first
+    uint64_t pull_nseg;
     uint64_t pull_min_work;
     unsigned long long* F;    // frontier masks of the current level, vertex-major F[v * slots_max + slot]
     uint32_t* FB;             // touched words of the previous level (same layout as touched)

@@ -378,6 +378,28 @@ __global__ void k_pull_pack(const uint32_t* __restrict__ u_sorted, const uint2* 
     }
 }
 
+// Pull work list: row u of the grouped records cut into ceil(d / kPullSeg) segments
+__global__ void k_seg_count(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ cnt) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u <= n; u += (uint64_t)gridDim.x * blockDim.x)
+        cnt[u] = u < n ? (off[u + 1] - off[u] + kPullSeg - 1) / kPullSeg : 0u;
+}
+__global__ void k_seg_write(const uint32_t* __restrict__ off, const uint32_t* __restrict__ pos, uint32_t n,
+                            uint32_t* __restrict__ key, uint32_t* __restrict__ su, uint32_t* __restrict__ sst) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = off[u], d = off[u + 1] - a;
+        for (uint32_t k = 0, p = pos[u]; k * kPullSeg < d; ++k, ++p) {
+            key[p] = kPullSeg - min(kPullSeg, d - k * kPullSeg);  // longest first
+            su[p] = (uint32_t)u;
+            sst[p] = a + k * kPullSeg;
+        }
+    }
+}
+__global__ void k_seg_pack(const uint32_t* __restrict__ key, const uint2* __restrict__ us, uint64_t nseg,
+                           uint4* __restrict__ seg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nseg; i += (uint64_t)gridDim.x * blockDim.x)
+        seg[i] = make_uint4(us[i].x, us[i].y, kPullSeg - key[i], 0u);
+}
+
 inline unsigned grid_for(uint64_t work, int threads) {
     uint64_t g = (work + threads - 1) / threads;
     uint64_t cap = (uint64_t)num_sms() * 16;
@@ -502,7 +524,30 @@ void build_pull_records(const Graph& g, cudaStream_t st) {
     k_pull_pack<<<grid_for(m, 256), 256, 0, st>>>(us.as<uint32_t>(), ew.as<uint2>(), g.rec.as<uint2>(), m, out.as<uint4>());
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_pull_pack");
+    // the segment work list: row offsets of the grouped records, segments per row, their positions
+    const uint32_t n = g.n;
+    DevBuf off(((uint64_t)n + 1) * 4), cnt(((uint64_t)n + 1) * 4), pos(((uint64_t)n + 1) * 4),
+        tmp(scan_temp_bytes((uint64_t)n + 1));
+    k_row_offsets<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(us.as<uint32_t>(), m, n, off.as<uint32_t>());
+    k_seg_count<<<grid_for((uint64_t)n + 1, 256), 256, 0, st>>>(off.as<uint32_t>(), n, cnt.as<uint32_t>());
+    count_launch(2);
+    exclusive_scan_u32(cnt.as<uint32_t>(), pos.as<uint32_t>(), (uint64_t)n + 1, tmp.p, st);
+    uint32_t nseg = 0;
+    BPT_CUDA(cudaMemcpyAsync(&nseg, pos.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
     BPT_CUDA(cudaStreamSynchronize(st));
+    DevBuf key(nseg * 4ull + 4), su(nseg * 4ull + 4), sst(nseg * 4ull + 4), skey(nseg * 4ull + 4), sus(nseg * 8ull + 8);
+    k_seg_write<<<grid_for(n, 256), 256, 0, st>>>(off.as<uint32_t>(), pos.as<uint32_t>(), n, key.as<uint32_t>(),
+                                                 su.as<uint32_t>(), sst.as<uint32_t>());
+    count_launch();
+    radix_sort_records(key.as<uint32_t>(), su.as<uint32_t>(), nullptr, sst.as<uint32_t>(), nseg, kPullSeg + 1,
+                       skey.as<uint32_t>(), sus.as<uint2>(), st);
+    DevBuf seg(nseg * 16ull + 16);
+    k_seg_pack<<<grid_for(nseg, 256), 256, 0, st>>>(skey.as<uint32_t>(), sus.as<uint2>(), nseg, seg.as<uint4>());
+    count_launch();
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_seg_pack");
+    BPT_CUDA(cudaStreamSynchronize(st));
+    g.pull_seg = std::move(seg);
+    g.pull_nseg = nseg;
     g.pull_rec = std::move(out);
 }
 

@@ -875,6 +875,10 @@ constexpr int kUnitBm = 32 * kWinBm;
 #define BPT_HEAVY 32
 #endif
 constexpr int kHeavy = BPT_HEAVY;  // live colours from which an item's coins are drawn warp-wide
+#ifndef BPT_PULL_DEFER
+#define BPT_PULL_DEFER 4
+#endif
+constexpr uint32_t kPullDefer = BPT_PULL_DEFER;  // pull: steps whose live items may wait for one coin call
 struct BmScratch {
     uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
     uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
@@ -937,9 +941,12 @@ __device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, ui
 // Coins and merges of the live items W.A / W.B[0, nlive) of one warp (shared by the push and the
 // pull expansion): item = {edge id, thr, live colours lo, hi} / {colour-0 slot index, U index,
 // touched word, bit}. One chunk of <= 32 live items at a time (one live item per lane).
+// fold (pull): the passing colours of every item are also OR-ed into fold[slot * 32 + owner lane]
+// (W.B.w = bit | owner lane << 8 | slot << 16), the owners' per-colour early exit
 __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
                                                    uint32_t nlive, unsigned long long& coins,
-                                                   unsigned long long& atoms, bool& any_pass) {
+                                                   unsigned long long& atoms, bool& any_pass,
+                                                   unsigned long long* fold = nullptr) {
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
     for (uint32_t c0 = 0; c0 < nlive; c0 += 32) {
         const uint32_t j = c0 + lane;
@@ -1009,9 +1016,10 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             if (pass) {
                 const uint4 bb = W.B[j];
                 ++atoms;
-                BPT_CHECK(bb.y < a.slots_max * a.n && bb.z < (uint64_t)a.slots_max * a.tiles * 32 && bb.w < 32, 7);
+                BPT_CHECK(bb.y < a.slots_max * a.n && bb.z < (uint64_t)a.slots_max * a.tiles * 32, 7);
                 atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + bb.y, pass);
-                atomicOr(&a.touched[bb.z], 1u << bb.w);
+                atomicOr(&a.touched[bb.z], 1u << (bb.w & 31u));
+                if (fold) atomicOr(&fold[((bb.w >> 16) & 3u) * 32 + ((bb.w >> 8) & 31u)], pass);  // several pending items per owner
                 any_pass = true;
             }
         }
@@ -1160,55 +1168,17 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
 // ------------------------------------------------------------------------ pull expansion (IC)
 // SURVEY §8(f) NEXT #1 (direction switching): a level whose push work (the
 // frontier's reverse-edge reads, summed over the batch's slots) is >= pull_min_work is expanded
-// the other way round. Every forward edge u -> w (Graph::pull_rec {u, w, e, thr}, grouped by u)
-// is read ONCE for all slots of the batch: live = F[w][slot] & ~U[slot][u] (F: the frontier masks
-// the compaction keeps exact, vertex-major so one 32-B sector serves 4 slots), and the live
-// (edge, slot) items go through the same coins (keyed by the canonical reverse id e, reading
-// C-4, so the RRR sets are those of the push form) and merges as the push expansion. At the
-// heavy levels the push form reads ~3.5 m reverse edges per batch (C2); the pull form reads m.
-__device__ __forceinline__ void pull_window(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
-                                            const uint4 r, bool valid, uint32_t nslots, uint64_t gblk0,
-                                            unsigned long long& coins, unsigned long long& atoms, bool& any_pass) {
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
-    BPT_CHECK(!valid || (r.x < a.n && r.y < a.n && r.z < a.m), 13);
-    unsigned long long f[4] = {0ull, 0ull, 0ull, 0ull};
-    if (valid) {
-        const unsigned long long* Fw = a.F + (size_t)r.y * a.slots_max;
-        if (a.slots_max == 4) {
-            const ulonglong2 f01 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw));
-            const ulonglong2 f23 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw) + 1);
-            f[0] = f01.x; f[1] = f01.y; f[2] = f23.x; f[3] = f23.y;
-        } else {
-#pragma unroll
-            for (uint32_t sl = 0; sl < 4; ++sl) f[sl] = sl < nslots ? __ldg(Fw + sl) : 0ull;
-        }
-    }
-    uint32_t nlive = 0;
-#pragma unroll
-    for (uint32_t sl = 0; sl < 4; ++sl) {
-        if (sl >= nslots) break;
-        uint32_t lo = (uint32_t)f[sl], hi = (uint32_t)(f[sl] >> 32);
-        const uint32_t vidx = sl * a.n + r.x;
-        if (lo | hi) {
-            const uint2 uu = ld_keep_u64(&U[vidx]);
-            lo &= ~uu.x;
-            hi &= ~uu.y;
-        }
-        const bool lv = (lo | hi) != 0;
-        const uint32_t bal = __ballot_sync(kFull, lv);
-        if (lv) {
-            const uint32_t pos = nlive + __popc(bal & lt_mask);
-            W.A[pos] = make_uint4(r.z, r.w, lo, hi);
-            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), vidx, sl * a.tiles * 32 + (r.x >> 5), r.x & 31u);
-        }
-        nlive += __popc(bal);
-    }
-    if (nlive == 0) return;
-    __syncwarp();
-    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
-}
-
+// the other way round, over the forward edges u -> w (Graph::pull_rec {u, w, e, thr}, grouped by
+// u): for every vertex u and slot, the colours u does not hold yet are pulled from its frontier
+// out-neighbours -- live = F[w][slot] & ~known[slot], F the frontier masks the compaction keeps
+// exact (vertex-major: one 32-B sector serves the 4 slots of a batch) -- with the coin of the
+// edge's canonical reverse id e (reading C-4), so the RRR sets are those of the push form.
+// One lane walks one row segment (<= kPullSeg edges, Graph::pull_seg, longest first so a warp's
+// segments have ~equal lengths) edge by edge, and a colour leaves its known mask as soon as one
+// coin passes: per-colour early exit, which the push form only gets from the timing of its
+// merges. Coins and merges go through the push form's machinery (bm_coins_and_merge); the
+// passing colours also come back to the owner lane (fold). Every forward edge is read once per
+// pull level for all slots (m per batch level; the push form reads ~3.5 m at C2's heavy levels).
 __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_pull(BatchArgs a, cudaGraphConditionalHandle h_level,
                                                                 int use_cond) {
     count_self(a.ctl);
@@ -1232,31 +1202,111 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_pull(BatchArgs
             a.umask[i] = 0;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[wid];
     __shared__ unsigned long long red[kWarps];
     __shared__ uint32_t sel8[256];
+    __shared__ unsigned long long fold_all[kWarps][4 * 32];
+    unsigned long long* fold = fold_all[wid];
     {
         uint32_t t = 0;
         for (uint32_t p = 0, j = 0; p < 8; ++p)
             if ((threadIdx.x >> p) & 1u) t |= p << (3 * j++);
         sel8[threadIdx.x] = t;
     }
+    for (int i = lane; i < 4 * 32; i += 32) fold[i] = 0ull;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
     unsigned long long coins = 0, atoms = 0;
     bool any_pass = false;
-    const uint64_t nwin = (a.pull_edges + 31) / 32;
-    const uint64_t stride = (uint64_t)gridDim.x * kWarps;
-    uint64_t win = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-    // the next window's records are loaded one window ahead
-    uint4 nx = make_uint4(0, 0, 0, 0);
-    if (win < nwin && win * 32 + lane < a.pull_edges) nx = ld_stream4(&a.pull[win * 32 + lane]);
-    for (; win < nwin; win += stride) {
-        const uint4 r = nx;
-        const bool valid = win * 32 + lane < a.pull_edges;
-        const uint64_t nw = win + stride;
-        if (nw < nwin && nw * 32 + lane < a.pull_edges) nx = ld_stream4(&a.pull[nw * 32 + lane]);
-        pull_window(a, W, sel8, lane, r, valid, nslots, gblk0, coins, atoms, any_pass);
+    const uint64_t ngroups = (a.pull_nseg + 31) / 32;
+    for (uint64_t grp = (uint64_t)blockIdx.x * kWarps + wid; grp < ngroups; grp += (uint64_t)gridDim.x * kWarps) {
+        const uint64_t i = grp * 32 + lane;
+        const uint4 sg = i < a.pull_nseg ? __ldg(&a.pull_seg[i]) : make_uint4(0, 0, 0, 0);
+        const uint32_t u = sg.x, end = sg.y + sg.z;
+        uint32_t ptr = sg.y;
+        const uint32_t steps = __shfl_sync(kFull, sg.z, 0);  // longest first: lane 0 holds the group's maximum
+        BPT_CHECK(sg.z == 0 || (u < a.n && end <= a.m), 13);
+        unsigned long long known[4];
+#pragma unroll
+        for (uint32_t sl = 0; sl < 4; ++sl) {
+            known[sl] = ~0ull;
+            if (sl < nslots && sg.z) {
+                const uint2 uu = ld_keep_u64(&U[sl * a.n + u]);
+                known[sl] = ((unsigned long long)uu.y << 32) | uu.x;
+            }
+        }
+        // software pipeline: the record of edge k + 2 and the frontier masks of edge k + 1 are in
+        // flight while edge k's coins are drawn (a step is otherwise a chain of two dependent loads)
+        auto load_f = [&](const uint4& rr, bool on, unsigned long long (&ff)[4]) {
+            ff[0] = ff[1] = ff[2] = ff[3] = 0ull;
+            if (!on) return;
+            const unsigned long long* Fw = a.F + (size_t)rr.y * a.slots_max;
+            if (a.slots_max == 4) {
+                const ulonglong2 f01 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw));
+                const ulonglong2 f23 = ld_keep(reinterpret_cast<const ulonglong2*>(Fw) + 1);
+                ff[0] = f01.x; ff[1] = f01.y; ff[2] = f23.x; ff[3] = f23.y;
+            } else {
+#pragma unroll
+                for (uint32_t sl = 0; sl < 4; ++sl) ff[sl] = sl < nslots ? __ldg(Fw + sl) : 0ull;
+            }
+        };
+        uint32_t nlive = 0, deferred = 0;  // pending live items, steps since the last coin call
+        auto flush = [&]() {
+            __syncwarp();
+            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, fold);
+            __syncwarp();
+#pragma unroll
+            for (uint32_t sl = 0; sl < 4; ++sl) {  // early exit: the colours this lane's u just got
+                if (sl >= nslots) break;
+                known[sl] |= fold[sl * 32 + lane];
+                fold[sl * 32 + lane] = 0ull;
+            }
+            __syncwarp();
+            nlive = 0;
+            deferred = 0;
+        };
+        uint4 r1 = ptr < end ? __ldg(&a.pull[ptr]) : make_uint4(0, 0, 0, 0);          // edge k + 1 (k = -1)
+        uint4 r2 = ptr + 1 < end ? __ldg(&a.pull[ptr + 1]) : make_uint4(0, 0, 0, 0);  // edge k + 2
+        unsigned long long fn[4];
+        load_f(r1, ptr < end, fn);
+        for (uint32_t k = 0; k < steps; ++k) {
+            const uint32_t e_k = r1.z, thr_k = r1.w;
+            unsigned long long f[4] = {fn[0], fn[1], fn[2], fn[3]};
+            ++ptr;  // now the index of edge k + 1
+            r1 = r2;
+            if (ptr + 1 < end) r2 = __ldg(&a.pull[ptr + 1]);
+            load_f(r1, ptr < end, fn);
+            // live (edge, slot) items of this step; they join the warp's pending list, whose coins are
+            // drawn once it would overflow (or after kPullDefer steps): the coin machinery has a fixed
+            // cost per call, and a step of 32 edges carries few coins at most pull levels
+#pragma unroll
+            for (uint32_t sl = 0; sl < 4; ++sl) f[sl] &= ~known[sl];
+            uint32_t cnt = 0;
+#pragma unroll
+            for (uint32_t sl = 0; sl < 4; ++sl) cnt += __popc(__ballot_sync(kFull, sl < nslots && f[sl] != 0ull));
+            if (nlive && (nlive + cnt > (uint32_t)kUnitBm || deferred >= kPullDefer)) {
+                flush();
+#pragma unroll
+                for (uint32_t sl = 0; sl < 4; ++sl) f[sl] &= ~known[sl];  // colours the flush just delivered
+            }
+#pragma unroll
+            for (uint32_t sl = 0; sl < 4; ++sl) {
+                if (sl >= nslots) break;
+                const bool lv = f[sl] != 0ull;
+                const uint32_t bal = __ballot_sync(kFull, lv);
+                if (lv) {
+                    const uint32_t pos = nlive + __popc(bal & lt_mask);
+                    W.A[pos] = make_uint4(e_k, thr_k, (uint32_t)f[sl], (uint32_t)(f[sl] >> 32));
+                    W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), sl * a.n + u, sl * a.tiles * 32 + (u >> 5),
+                                          (u & 31u) | ((uint32_t)lane << 8) | (sl << 16));
+                }
+                nlive += __popc(bal);
+            }
+            deferred += nlive != 0;
+        }
+        if (nlive) flush();
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
     unsigned long long ct = block_sum_ull(coins, red);

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--theta", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--print-rows", action="store_true")
     args = ap.parse_args()
     cfg = graphgen.CONFIGS[args.config]
     theta = args.theta or cfg.theta
@@ -60,6 +61,9 @@ def main():
         byb.append([int(b), int(sel.sum()), round(float(ms[sel].sum()), 3), int(work[sel].sum()), int(coins[sel].sum())])
     out["by_batch_sampled_[batch,levels,ms,edges,coins]"] = byb
     print(json.dumps(out))
+    if args.print_rows:
+        for r, t in zip(st.tolist(), ms.tolist()):
+            print(json.dumps({"row": r, "ms": t}))
     if args.out:
         np.savez_compressed(args.out, stats=st, ms=ms)
 
