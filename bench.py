@@ -43,8 +43,9 @@ UNIT = "RRR sets/s"
 CFG = graphgen.CONFIGS["C2"]
 EXTRACT_SAMPLES = 64
 PER_MEMBER_BYTES_LT = "24 B per RRR member (8 B row bounds + 8 B chosen in-edge record + 8 B visited-set insertion)"
-PER_EDGE_BYTES = ("16 B per reverse-edge read (8 B {src,thr} record + 8 B U[u] = V|N gather) + 8 B per atomicOr "
-                  "+ 24 B per frontier entry + 8 B per vertex discovered for the next level")
+PER_EDGE_BYTES = ("per reverse-edge read of a frontier vertex: 8 B {src,thr} record + 8 B x S of U[u] (= V|N of the "
+                  "S = 4 slots of the batch-wide frontier, one 32-B sector); + 8 B per atomicOr + (4 + 8 S) B per "
+                  "frontier entry + 8 B per vertex discovered for the next level")
 
 
 def parse():

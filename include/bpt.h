@@ -173,6 +173,12 @@ typedef struct {
  * differ). Needs 16 B per edge of forward records (built on first use, kept with the graph); falls
  * back to push when they do not fit. */
 #define BPT_FLAG_PULL 512u
+/* IC, 64 colours (touched-bitmap form): by default the <= 4 64-sample blocks of a batch share ONE
+ * frontier of vertices (vertex-major working masks; every reverse edge of a frontier vertex is read
+ * once for up to 256 colours). This flag keeps one frontier per block
+ * (64 colours per entry; implied by BPT_FLAG_PULL). Same RRR sets, sizes, digests and seeds; E_phys
+ * and the level structure are those of the 256-sample (resp. 64-sample) fused groups. */
+#define BPT_FLAG_SLOTWISE 1024u
 
 BPT_API bpt_status bpt_sample(const bpt_graph* g, bpt_model model, uint64_t theta, uint32_t colors, uint64_t seed,
                       void* stream, bpt_samples** out);

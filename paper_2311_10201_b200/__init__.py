@@ -5,7 +5,7 @@ for sm_100a behind the C-ABI of include/bpt.h); this package is its thin ctypes 
 """
 from .bpt import (  # noqa: F401
     BPT_EINVAL, BPT_ENOMEM, BPT_ECUDA, BPT_ENCCL, BPT_ESTATE, BPT_OK, FLAG_PROFILE, FLAG_SPARSE, FLAG_WIDE, IC, LT, LIB_PATH,
-    FLAG_LT_DENSE, FLAG_LT_FUSED, FLAG_LT_LEVELS, FLAG_LT_REWALK, FLAG_QUEUE, FLAG_UNSORTED, FLAG_PULL,
+    FLAG_LT_DENSE, FLAG_LT_FUSED, FLAG_LT_LEVELS, FLAG_LT_REWALK, FLAG_QUEUE, FLAG_UNSORTED, FLAG_PULL, FLAG_SLOTWISE,
     BptError, Comm, Graph, Samples, bpt_abi_version, bpt_comm_free, bpt_comm_init, bpt_comm_unique_id,
     bpt_graph_free, bpt_graph_load, bpt_kernel_launch_count, bpt_last_error, bpt_level_stats, bpt_occurrences,
     bpt_rrr_digests, bpt_rrr_extract, bpt_rrr_sizes, bpt_sample, bpt_samples_free, bpt_samples_get_info,

@@ -35,6 +35,7 @@ FLAG_LT_LEVELS = 64  # LT fused: per-level launches instead of one cooperative l
 FLAG_QUEUE = 128  # IC 64 colours: first-setter queue instead of the touched bitmap
 FLAG_UNSORTED = 256  # IC 64 colours: sample s in slot s (no start-vertex sort)
 FLAG_PULL = 512  # IC 64 colours: pull expansion of the heavy levels (direction switching)
+FLAG_SLOTWISE = 1024  # IC 64 colours: one frontier per 64-sample block instead of one per batch
 _STATUS = {0: "BPT_OK", -1: "BPT_EINVAL", -2: "BPT_ENOMEM", -3: "BPT_ECUDA", -4: "BPT_ENCCL", -5: "BPT_ESTATE"}
 
 _p, _u32, _u64, _i = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int

@@ -473,14 +473,19 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     uint64_t slots = wide ? kWide : umin64(umax64(want, 1), S.blocks);
     const uint32_t tile = wide ? kUnitWide : expand_unit(S.model, bitmap);
     const uint64_t tiles = (n + 1023) / 1024;  // bitmap: 1,024-vertex tiles per slot
+    // batch-wide frontier (IC, 64 colours, bitmap form, <= 4 blocks per batch; k_sample.cu "Batch-wide
+    // frontier"): the default; BPT_FLAG_SLOTWISE (and the pull form) keep one frontier per block
+    bool vmajor = bitmap && !(opt.flags & BPT_FLAG_SLOTWISE) && !(opt.flags & BPT_FLAG_PULL);
     auto plan_bytes = [&](uint64_t sl, uint64_t& raw_cap, uint64_t& q_cap, uint64_t& ts_cap) {
-        raw_cap = umin64(wide ? n : sl * slices * n, (1ull << 28) - 1);  // wide: one entry per vertex
+        const bool vm = vmajor && sl <= 4;
+        raw_cap = umin64(wide || vm ? n : sl * slices * n, (1ull << 28) - 1);  // wide / vmajor: one entry per vertex
         q_cap = raw_cap;
         if (bitmap) raw_cap = 1;  // no queue
-        const uint64_t work = S.model == BPT_IC ? umin64((wide ? 1 : sl * slices) * g.m, kEdgeMask)
+        const uint64_t work = S.model == BPT_IC ? umin64((wide || vm ? 1 : sl * slices) * g.m, kEdgeMask)
                                                 : umin64(sl * 64 * n, kEdgeMask);
         ts_cap = work / tile + 2;
-        return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (16 + 8) + ts_cap * 20 + (bitmap ? sl * tiles * 128 : 0);
+        return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (vm ? 4 + 8 * sl : 16 + 8) + ts_cap * 20 +
+               (bitmap ? (vm ? 1 : sl) * tiles * 128 : 0);
     };
     size_t free_b = 0, total_b = 0;
     BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -498,18 +503,24 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     while (!wide && slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
     while (!wide && slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
     if (wide && (uint64_t)kWide * n >= (1ull << 32)) fail(BPT_EINVAL, "wide fusion needs kWide * n < 2^32");
+    if (slots > 4) vmajor = false;
     plan_bytes(slots, raw_cap, q_cap, ts_cap);
 
     const uint64_t nbatches = (S.blocks + slots - 1) / slots;
     const uint32_t stats_cap = (uint32_t)umin64(nbatches * 64 + 8192, 1ull << 22);
-    DevBuf VN((size_t)slots * n * 16), raw(raw_cap * 8), q(q_cap * 16), qoff(q_cap * 8), tstart(ts_cap * 4),
+    DevBuf VN((size_t)slots * n * 16), raw(raw_cap * 8), q(vmajor ? 16 : q_cap * 16), qoff(vmajor ? 16 : q_cap * 8),
+        tstart(ts_cap * 4),
         umask(S.model == BPT_IC ? (ts_cap * tile / 32 + 4) * 4 : 16),
         lv((size_t)kMaxLevels * sizeof(LevelRec)), stats((size_t)stats_cap * sizeof(LevelRec)), ctl(sizeof(Ctl)),
         elog(8);
     BPT_CUDA(cudaMemsetAsync(VN.p, 0, VN.bytes, st));  // the finaliser re-zeroes it after every batch
     DevBuf vflag, qd, qmask, touched, Fbuf, FBbuf;
+    if (vmajor) {
+        qd.alloc(q_cap * 4 + 4);
+        qmask.alloc(q_cap * slots * 8 + 16);
+    }
     if (bitmap) {
-        touched.alloc(slots * tiles * 128);
+        touched.alloc((vmajor ? 1 : slots) * tiles * 128);
         BPT_CUDA(cudaMemsetAsync(touched.p, 0, touched.bytes, st));  // the compaction clears what it reads
     }
     if (pull) {
@@ -577,8 +588,9 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.k_start = stream_key(S.seed, kTagStart);
     a.wide = wide ? 1 : 0;
     a.vflag = wide ? vflag.as<uint32_t>() : nullptr;
-    a.qd = wide ? qd.as<uint32_t>() : nullptr;
-    a.qmask = wide ? qmask.as<unsigned long long>() : nullptr;
+    a.qd = wide || vmajor ? qd.as<uint32_t>() : nullptr;
+    a.qmask = wide || vmajor ? qmask.as<unsigned long long>() : nullptr;
+    a.vmajor = vmajor ? 1 : 0;
     a.touched = bitmap ? touched.as<uint32_t>() : nullptr;
     a.tiles = (uint32_t)tiles;
     a.lt_persist = (opt.flags & BPT_FLAG_LT_LEVELS) ? 0 : 1;
@@ -654,7 +666,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
                 cur ^= 1;
             }
             launch_finalize(S, a.VN, a.ctl, a.slots_max, g.roff.as<uint32_t>(), st, elog.as<unsigned long long>(),
-                            a.wide != 0, a.touched != nullptr);
+                            a.wide != 0, a.touched ? (a.vmajor ? 2 : 1) : 0);
             launch_next_batch(a, st);
         }
         BPT_CUDA(cudaStreamSynchronize(st));
@@ -709,6 +721,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         const uint64_t raw_next = (i + 1 < rows && (R[i + 1].pad >> 32) == (r.pad >> 32)) ? R[i + 1].raw : 0;
         if (r.pull)  // 16 B forward record + the slots' F[w] words per edge, U[u] per vertex and slot, merges
             bytes += (16.0 + 8.0 * slots) * (double)r.pull_reads + 8.0 * slots * n + 8.0 * r.atomics + 8.0 * raw_next;
+        else if (vmajor)  // record + the S slots' U[u] per edge read, entries {delta, S masks}
+            bytes += (8.0 + 8.0 * slots) * work + 8.0 * r.atomics + (4.0 + 8.0 * slots) * kept + 8.0 * raw_next;
         else
             bytes += (S.model == BPT_IC ? 16.0 : 24.0) * work + 8.0 * r.atomics + 24.0 * kept + 8.0 * raw_next;
         const uint64_t row[kLevelCols] = {r.pad >> 32, r.pad & 0xffffffffull, r.raw, kept, work, r.vc, r.coins, r.atomics};

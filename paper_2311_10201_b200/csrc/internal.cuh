@@ -277,6 +277,11 @@ struct BatchArgs {
     uint64_t pull_min_work;
     unsigned long long* F;    // frontier masks of the current level, vertex-major F[v * slots_max + slot]
     uint32_t* FB;             // touched words of the previous level (same layout as touched)
+    // batch-wide frontier (IC, 64 colours, touched-bitmap mode): the slots_max
+    // blocks of a batch share ONE frontier. Vertex-major union layout U[v * S + slot] (then V at
+    // S * n), one touched bit per vertex, one entry per frontier vertex with S masks (qd, qmask):
+    // every reverse edge of a frontier vertex is read once for all 64 S colours
+    int vmajor;
 };
 #ifndef BPT_WIDE_BLOCKS
 #define BPT_WIDE_BLOCKS 2
@@ -287,11 +292,12 @@ constexpr uint32_t kWide = BPT_WIDE_BLOCKS;  // blocks (x 64 colours) per wide f
 #endif
 constexpr uint32_t kUnitWide = BPT_UNIT_WIDE;  // work items per wide expansion unit (windows of 32)
 // k_store.cu
+// umode: 0 {V, N} pairs, 1 slot-major union layout, 2 vertex-major union layout (a.vmajor)
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog, bool wide, bool umode);
+                     cudaStream_t st, unsigned long long* d_elog, bool wide, int umode);
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
-                     bool wide, bool umode);
+                     bool wide, int umode);
 // k_build.cu: forward records of the pull expansion (Graph::pull_rec), from the reverse CSR
 void build_pull_records(const Graph& g, cudaStream_t st);
 // k_sample.cu: host-driven level loop (profiling with CUDA events) and the device-resident graph

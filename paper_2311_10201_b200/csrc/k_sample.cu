@@ -154,6 +154,20 @@ __device__ __forceinline__ unsigned long long block_sum_ull(unsigned long long x
 // Sample s = 64*(gblk0 + slot) + bit, colour bit of block slot. start(s) per reading C-3.
 // Listing 1 lines 1-3: frontier[start].c = 1 -> here VN[slot][start].N |= bit,
 // first setter of the (slot, slice) enqueues the raw entry of level 0.
+// bitmap mode: colour `bit` of slot `slot` starts at v (U |= bit, v touched); vertex-major layout
+// (a.vmajor): U[v * slots + slot] and one touched bit per vertex for all slots of the batch
+__device__ __forceinline__ void mark_start(const BatchArgs& a, uint32_t slot, uint32_t v, uint32_t bit) {
+    unsigned long long* U = reinterpret_cast<unsigned long long*>(a.VN);
+    if (a.vmajor) {
+        atomicOr(U + (size_t)v * a.slots_max + slot, 1ull << bit);
+        atomicOr(&a.touched[v >> 5], 1u << (v & 31));
+    } else {
+        atomicOr(U + (size_t)slot * a.n + v, 1ull << bit);
+        atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (v >> 5)], 1u << (v & 31));
+    }
+    a.lv[0].any = 1;
+}
+
 __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_cond) {
     count_self(a.ctl);
     const uint64_t total = (uint64_t)a.ctl->slots * 64;
@@ -178,15 +192,11 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
             const uint2 w2 = philox2x32_10(ss, 0u, a.k_start);
             const uint32_t st2 = (uint32_t)__umul64hi(((uint64_t)w2.y << 32) | w2.x, (uint64_t)a.n);
             BPT_CHECK(st2 < a.n, 12);
-            atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + st2, 1ull << bit);
-            atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (st2 >> 5)], 1u << (st2 & 31));
-            a.lv[0].any = 1;
+            mark_start(a, slot, st2, bit);
             continue;
         }
         if (a.touched) {  // bitmap mode: mark the start, the compaction of level 0 finds it
-            atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)slot * a.n + start, 1ull << bit);
-            atomicOr(&a.touched[(size_t)slot * a.tiles * 32 + (start >> 5)], 1u << (start & 31));
-            a.lv[0].any = 1;
+            mark_start(a, slot, start, bit);
             continue;
         }
         const uint32_t slice = bit / a.colors;
@@ -585,6 +595,158 @@ __global__ void __launch_bounds__(kThreads) k_compact_bm(BatchArgs a, uint32_t* 
                     for (uint64_t x = u0; x < u1c; ++x) tstart[x] = (uint32_t)myq;
             }
             for (uint32_t lb = __ballot_sync(kFull, longr); lb; lb &= lb - 1u) {  // hub ranges: the whole warp
+                const int src = __ffs(lb) - 1;
+                const uint64_t a0 = __shfl_sync(kFull, u0, src), a1 = __shfl_sync(kFull, u1c, src);
+                const uint32_t qv = (uint32_t)__shfl_sync(kFull, myq, src);
+                for (uint64_t x = a0 + lane; x < a1; x += 32) tstart[x] = qv;
+            }
+            qi += __popc(kb);
+            off += chunk_work;
+        }
+        __syncwarp();
+    }
+    unsigned long long vc_tot = block_sum_ull(vc_local, red);
+    if (threadIdx.x == 0 && vc_tot) atomicAdd(&L->vc, vc_tot);
+    const unsigned long long tt = block_sum_ull(touched_local, red);
+    if (threadIdx.x == 0 && tt) atomicAdd(&L->raw, (unsigned)tt);
+    if (blockIdx.x * kWarps < ntiles && threadIdx.x == 0) atomicMax(&ctl->c_end, global_ns());
+}
+
+
+// Batch-wide frontier (a.vmajor; SURVEY §8(f) NEXT #2 with the product's machinery): the S <= 4
+// blocks of a batch share one frontier of VERTICES. Tiles are 1,024-vertex tiles of the single
+// per-vertex touched bitmap; a touched vertex's new colours of every slot come from one 32-B
+// sector of U and of V (vertex-major union layout), and it becomes ONE entry {delta} + S masks.
+// Measured with the oracle on C2's sorted groups: one 256-sample fused traversal reads 3.1-3.3x
+// fewer reverse edges than its four 64-sample groups (scripts/dbg/overlap.py).
+template <uint32_t kUnit>
+__global__ void __launch_bounds__(kThreads) k_compact_bmv(BatchArgs a, uint32_t* __restrict__ tstart,
+                                                          uint64_t tstart_cap) {
+    count_self(a.ctl);
+    if (!a.ctl->cont) return;
+    Ctl* ctl = a.ctl;
+    LevelRec* L = &a.lv[ctl->level];
+    const uint32_t ntiles = a.tiles, S = a.slots_max;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    __shared__ uint16_t vlist[kWarps][kTileV];
+    __shared__ unsigned long long red[kWarps];
+    if (blockIdx.x * kWarps < ntiles && threadIdx.x == 0) atomicMin(&ctl->c_start, global_ns());
+    unsigned long long vc_local = 0;
+    uint32_t touched_local = 0;
+    unsigned long long* U = reinterpret_cast<unsigned long long*>(a.VN);
+    unsigned long long* V = U + (size_t)S * a.n;
+    for (uint32_t t = blockIdx.x * kWarps + wid; t < ntiles; t += gridDim.x * kWarps) {
+        const uint32_t w = a.touched[(size_t)t * 32 + lane];
+        if (!__any_sync(kFull, w != 0u)) continue;
+        const uint32_t vbase = t * kTileV;
+        if (w) a.touched[(size_t)t * 32 + lane] = 0u;  // cleared for the next level
+        const uint32_t c = __popc(w);
+        uint32_t incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        touched_local += c;
+        {
+            uint32_t pos = incl - c;
+            for (uint32_t x = w; x; x &= x - 1u) vlist[wid][pos++] = (uint16_t)(32u * lane + __ffs(x) - 1u);
+        }
+        __syncwarp();
+        uint32_t cnt = 0;
+        unsigned long long work = 0;
+        for (uint32_t j = lane; j < total; j += 32) {
+            const uint32_t v = vbase + vlist[wid][j];
+            const uint32_t d = __ldg(&a.roff[v + 1]) - __ldg(&a.roff[v]);
+            cnt += d != 0u;
+            work += d;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            cnt += __shfl_xor_sync(kFull, cnt, d);
+            work += __shfl_xor_sync(kFull, work, d);
+        }
+        unsigned long long base = ~0ull;
+        if (lane == 0 && cnt) {
+            const unsigned long long old = atomicAdd(&L->packed, ((unsigned long long)cnt << kPackShift) + work);
+            if ((old >> kPackShift) + cnt > a.q_cap || (old & kEdgeMask) + work > kEdgeMask) L->overflow = 1;
+            else base = old;
+        }
+        base = __shfl_sync(kFull, base, 0);
+        uint64_t qi = base >> kPackShift, off = base & kEdgeMask;
+        for (uint32_t j0 = 0; j0 < total; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const bool has = j < total;
+            uint32_t v = 0, rs = 0, d = 0;
+            unsigned long long nm[4] = {0ull, 0ull, 0ull, 0ull};
+            if (has) {
+                v = vbase + vlist[wid][j];
+                BPT_CHECK(v < a.n, 9);
+                const size_t b = (size_t)v * S;
+                if (S == 4) {
+                    const ulonglong2 u01 = *reinterpret_cast<const ulonglong2*>(U + b);
+                    const ulonglong2 u23 = *reinterpret_cast<const ulonglong2*>(U + b + 2);
+                    const ulonglong2 v01 = *reinterpret_cast<const ulonglong2*>(V + b);
+                    const ulonglong2 v23 = *reinterpret_cast<const ulonglong2*>(V + b + 2);
+                    nm[0] = u01.x & ~v01.x; nm[1] = u01.y & ~v01.y; nm[2] = u23.x & ~v23.x; nm[3] = u23.y & ~v23.y;
+                    *reinterpret_cast<ulonglong2*>(V + b) = u01;
+                    *reinterpret_cast<ulonglong2*>(V + b + 2) = u23;
+                } else {
+#pragma unroll
+                    for (uint32_t sl = 0; sl < 4; ++sl)
+                        if (sl < S) {
+                            const unsigned long long uu = U[b + sl];
+                            nm[sl] = uu & ~V[b + sl];
+                            V[b + sl] = uu;
+                        }
+                }
+#pragma unroll
+                for (uint32_t sl = 0; sl < 4; ++sl) vc_local += __popcll(nm[sl]);
+                rs = __ldg(&a.roff[v]);
+                d = __ldg(&a.roff[v + 1]) - rs;
+            }
+            const bool kept = d != 0u;
+            const uint32_t kb = __ballot_sync(kFull, kept);
+            uint32_t wx = kept ? d : 0u;
+            uint32_t wi = wx;
+#pragma unroll
+            for (int s2 = 1; s2 < 32; s2 <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, wi, s2);
+                if (lane >= s2) wi += y;
+            }
+            const uint32_t chunk_work = __shfl_sync(kFull, wi, 31);
+            if (base == ~0ull) continue;
+            bool longr = false;
+            uint64_t u0 = 0, u1c = 0, myq = 0;
+            if (kept) {
+                myq = qi + __popc(kb & lt_mask);
+                const uint64_t myoff = off + (wi - wx);
+                BPT_CHECK(myq < a.q_cap, 9);
+                a.qd[myq] = rs - (uint32_t)myoff;  // edge id e = work item + delta (mod 2^32)
+                unsigned long long* qm = a.qmask + (size_t)myq * S;
+                if (S == 4) {
+                    *reinterpret_cast<ulonglong2*>(qm) = make_ulonglong2(nm[0], nm[1]);
+                    *reinterpret_cast<ulonglong2*>(qm + 2) = make_ulonglong2(nm[2], nm[3]);
+                } else {
+#pragma unroll
+                    for (uint32_t sl = 0; sl < 4; ++sl)
+                        if (sl < S) qm[sl] = nm[sl];
+                }
+                if (myoff / kUnit < tstart_cap) {
+                    BPT_CHECK((myoff >> 5) < a.umask_words, 10);
+                    atomicOr(&a.umask[myoff >> 5], 1u << (myoff & 31u));
+                }
+                u0 = (myoff + kUnit - 1) / kUnit;
+                const uint64_t u1 = (myoff + d + kUnit - 1) / kUnit;
+                if (u1 > tstart_cap) L->overflow = 1;
+                u1c = umin64(u1, tstart_cap);
+                longr = u1c > u0 + 4;
+                if (!longr)
+                    for (uint64_t x = u0; x < u1c; ++x) tstart[x] = (uint32_t)myq;
+            }
+            for (uint32_t lb = __ballot_sync(kFull, longr); lb; lb &= lb - 1u) {
                 const int src = __ffs(lb) - 1;
                 const uint64_t a0 = __shfl_sync(kFull, u0, src), a1 = __shfl_sync(kFull, u1c, src);
                 const uint32_t qv = (uint32_t)__shfl_sync(kFull, myq, src);
@@ -1236,9 +1398,117 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
     bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
 }
 
+
+// Batch-wide frontier (a.vmajor): the same units of kUnitBm work items, but an item is a reverse
+// edge of a frontier VERTEX read once for the S slots of the batch: its source's S masks come
+// from one 32-B sector (U[u * S .. u * S + S)), each slot with live colours becomes a live item of
+// the coin machinery. The items of a unit are flushed to the coins whenever the next slot's ballot
+// would overflow the warp's list.
+template <bool kWhole>
+__device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
+                                                uint32_t le_mask, uint32_t unit, uint32_t rem, uint32_t jc0,
+                                                uint32_t mword, uint64_t gblk0, uint32_t nslots,
+                                                unsigned long long& coins, unsigned long long& atoms,
+                                                bool& any_pass) {
+    const uint32_t t0l = unit * (uint32_t)kUnitBm;
+    uint32_t mw[kWinBm];
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) mw[w] = __shfl_sync(kFull, mword, w);
+    if (lane < kWinBm) a.umask[(size_t)unit * kWinBm + lane] = 0;  // cleared for the next level
+    mw[0] &= ~1u;
+    uint32_t jl[kWinBm];
+    uint32_t before = jc0;
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        jl[w] = before + __popc(mw[w] & le_mask);
+        before += __popc(mw[w]);
+        if (!(kWhole || 32u * w + lane < rem)) jl[w] = jc0;
+    }
+    BPT_CHECK((uint64_t)unit * kWinBm + kWinBm <= a.umask_words, 1);
+    uint32_t dl[kWinBm];
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        BPT_CHECK(jl[w] < a.q_cap, 2);
+        dl[w] = __ldg(&a.qd[jl[w]]);
+    }
+    uint2 rc[kWinBm];
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        const uint32_t i = (kWhole || 32u * w + lane < rem) ? 32u * w + lane : 0u;
+        BPT_CHECK((uint32_t)(t0l + i + dl[w]) < a.m, 3);
+        rc[w] = ld_stream(&a.rec[t0l + i + dl[w]]);
+    }
+    const uint32_t lt_mask = le_mask >> 1;
+    const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
+    const uint32_t S = a.slots_max;
+    uint32_t nlive = 0;
+#pragma unroll
+    for (int w = 0; w < kWinBm; ++w) {
+        const bool valid = kWhole || 32u * w + lane < rem;
+        const uint32_t u = rc[w].x;
+        BPT_CHECK(u < a.n, 5);
+        const unsigned long long* qm = a.qmask + (size_t)jl[w] * S;
+        const unsigned long long* Uu = U + (size_t)u * S;
+        unsigned long long live[4] = {0ull, 0ull, 0ull, 0ull};
+        if (valid) {
+            if (S == 4) {
+                const ulonglong2 m01 = __ldg(reinterpret_cast<const ulonglong2*>(qm));
+                const ulonglong2 m23 = __ldg(reinterpret_cast<const ulonglong2*>(qm) + 1);
+                const ulonglong2 u01 = ld_keep_cg(reinterpret_cast<const ulonglong2*>(Uu));
+                const ulonglong2 u23 = ld_keep_cg(reinterpret_cast<const ulonglong2*>(Uu) + 1);
+                live[0] = m01.x & ~u01.x; live[1] = m01.y & ~u01.y; live[2] = m23.x & ~u23.x; live[3] = m23.y & ~u23.y;
+            } else {
+#pragma unroll
+                for (uint32_t sl = 0; sl < 4; ++sl)
+                    if (sl < S) {
+                        const unsigned long long m = __ldg(qm + sl);
+                        if (m) {
+                            const uint2 uu = ld_keep_u64(Uu + sl);
+                            live[sl] = m & ~(((unsigned long long)uu.y << 32) | uu.x);
+                        }
+                    }
+            }
+        }
+        const uint32_t e = t0l + 32u * w + lane + dl[w];
+        // live slots of this lane's edge (slots past the batch's own have no colours, so no mask),
+        // one warp scan places the window's items
+        uint32_t smask = 0;
+#pragma unroll
+        for (uint32_t sl = 0; sl < 4; ++sl) smask |= live[sl] != 0ull ? 1u << sl : 0u;
+        const uint32_t c = __popc(smask);
+        uint32_t incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const uint32_t wtot = __shfl_sync(kFull, incl, 31);
+        if (wtot == 0) continue;
+        if (nlive + wtot > (uint32_t)kUnitBm) {  // the list is full: draw its coins first
+            __syncwarp();
+            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+            __syncwarp();
+            nlive = 0;
+        }
+        uint32_t pos = nlive + incl - c;
+        for (uint32_t x = smask; x; x &= x - 1u) {
+            const uint32_t sl = __ffs(x) - 1u;
+            const unsigned long long lv = sl == 0 ? live[0] : sl == 1 ? live[1] : sl == 2 ? live[2] : live[3];  // registers
+            W.A[pos] = make_uint4(e, rc[w].y, (uint32_t)lv, (uint32_t)(lv >> 32));
+            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), u * S + sl, u >> 5, u & 31u);
+            ++pos;
+        }
+        nlive += wtot;
+    }
+    if (nlive == 0) return;
+    __syncwarp();
+    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+}
+
 #ifndef BPT_BM_MINB
 #define BPT_BM_MINB 4  // 64 registers: no spills; 4 x 8 warps per SM (measured: -4% vs 5 blocks at 48)
 #endif
+template <bool kVmajor>
 __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a, const uint32_t* __restrict__ tstart,
                                                               cudaGraphConditionalHandle h_level, int use_cond) {
     count_self(a.ctl);
@@ -1248,6 +1518,7 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     // colour 0 of slot k is sample 64 * (gblk0 + k) -- or, with sorted start vertices, local slot
     // 64 * (blk0 + k), mapped through slot_sample
     const uint64_t gblk0 = a.slot_sample ? ctl->blk0 : ctl->gblk0;
+    const uint32_t nslots = ctl->slots;
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
     if (pull_level(a, L)) return;  // k_expand_pull expands this level
@@ -1297,11 +1568,19 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
             nx_t = __ldg(&tstart[nxt]);
             nx_m = lane < kWinBm ? a.umask[(size_t)nxt * kWinBm + lane] : 0u;
         }
-        if (unit < nfull)
+        if (kVmajor) {
+            if (unit < nfull)
+                expand_unit_bmv<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, nslots, coins, atoms,
+                                      any_pass);
+            else
+                expand_unit_bmv<false>(a, W, sel8, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0,
+                                       mword, gblk0, nslots, coins, atoms, any_pass);
+        } else if (unit < nfull) {
             expand_unit_bm<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass);
-        else
+        } else {
             expand_unit_bm<false>(a, W, sel8, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, mword,
                                   gblk0, coins, atoms, any_pass);
+        }
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
     unsigned long long ct = block_sum_ull(coins, red);
@@ -2476,7 +2755,8 @@ void launch_walk_lt_lists(uint32_t n, const uint32_t* roff, const uint2* rec, ui
 using CompactFn = void (*)(BatchArgs, uint32_t*, uint64_t);
 static CompactFn compact_kernel(const BatchArgs& a) {
     if (a.model != BPT_IC) return k_compact<kTile>;
-    return a.touched ? k_compact_bm<kUnitBm> : k_compact<kUnitIC>;
+    if (a.touched) return a.vmajor ? k_compact_bmv<kUnitBm> : k_compact_bm<kUnitBm>;
+    return k_compact<kUnitIC>;
 }
 
 uint32_t expand_unit(int model, bool bitmap) {
@@ -2494,9 +2774,10 @@ int expand_grid() {
                                                                sizeof(WarpScratch) * kWarps));
         g_expand_grid = num_sms() * (per_sm > 0 ? per_sm : 1);
         int per_sm_b = 0;
-        BPT_CUDA(cudaFuncSetAttribute(k_expand_bm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(BmScratch) * kWarps)));
-        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_expand_bm, kThreads,
+        for (void* f : {(void*)k_expand_bm<false>, (void*)k_expand_bm<true>})
+            BPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(BmScratch) * kWarps)));
+        BPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_expand_bm<false>, kThreads,
                                                                sizeof(BmScratch) * kWarps));
         g_expand_grid_b = num_sms() * (per_sm_b > 0 ? per_sm_b : 1);
         int per_sm_p = 0;
@@ -2563,7 +2844,8 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
     compact_kernel(a)<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap);
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
     if (a.model == BPT_IC && a.touched) {
-        k_expand_bm<<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        if (a.vmajor) k_expand_bm<true><<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        else k_expand_bm<false><<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
         if (a.pull) {
             k_expand_pull<<<g_expand_grid_p, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, h0, 0);
             count_launch();
@@ -2637,7 +2919,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         coop.cooperative = 1;
         BPT_CUDA(cudaGraphKernelNodeSetAttribute(n_lv, cudaLaunchAttributeCooperative, &coop));
         cudaGraphNode_t n_store;
-        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched != nullptr);
+        add_store_nodes(body, n_lv, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched ? (a.vmajor ? 2 : 1) : 0);
         void* nb_args[] = {&args, &h_batch, &one};
         add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
         cudaGraphExec_t exec;
@@ -2664,8 +2946,8 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
         ? add_kernel(lbody, &n_cmp, (void*)k_expand_w, dim3(g_expand_grid_w), dim3(kThreads),
                      sizeof(WarpScratchW) * kWarps, exp_args)
         : a.model == BPT_IC && a.touched
-        ? add_kernel(lbody, &n_cmp, (void*)k_expand_bm, dim3(g_expand_grid_b), dim3(kThreads),
-                     sizeof(BmScratch) * kWarps, exp_args)
+        ? add_kernel(lbody, &n_cmp, a.vmajor ? (void*)k_expand_bm<true> : (void*)k_expand_bm<false>,
+                     dim3(g_expand_grid_b), dim3(kThreads), sizeof(BmScratch) * kWarps, exp_args)
         : a.model == BPT_IC
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
@@ -2678,7 +2960,7 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
     // the expansion's last block advances the level and sets the loop condition
     // finalize + count, then next batch
     cudaGraphNode_t n_store;
-    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched != nullptr);
+    add_store_nodes(body, n_level, *h.S, h.VN, a.ctl, a.slots_max, h.roff, h.d_elog, &n_store, a.wide != 0, a.touched ? (a.vmajor ? 2 : 1) : 0);
     void* nb_args[] = {&args, &h_batch, &one};
     add_kernel(body, &n_store, (void*)k_next_batch, dim3(1), dim3(256), 0, nb_args);
 

@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     // union layout: U[slot][n] then V[slot][n]; sstride = n, gridDim.y = slots_max
     unsigned long long* UV = reinterpret_cast<unsigned long long*>(VN) + (size_t)blockIdx.y * n;
     const size_t slots_max_n = (size_t)gridDim.y * n;
+    // vertex-major union layout (umode 2): U[v * slots_max + slot], V after slots_max * n words
+    unsigned long long* UVm = reinterpret_cast<unsigned long long*>(VN);
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -66,7 +68,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
         for (int u = 0; u < kU; ++u) {
             const uint64_t v = base + 32ull * u + lane;
             // N is 0 after the last level (union layout: U == V, V after the U block)
-            m[u] = v < v_end ? (umode ? UV[slots_max_n + v] : W[v * vstride].x) : 0ull;
+            m[u] = v < v_end ? (umode == 2 ? UVm[slots_max_n + v * gridDim.y + blockIdx.y]
+                                : umode ? UV[slots_max_n + v] : W[v * vstride].x) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -74,7 +77,10 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
             if (v < v_end) {
                 V[v] = m[u];
                 if (m[u]) {
-                    if (umode) {
+                    if (umode == 2) {
+                        UVm[v * gridDim.y + blockIdx.y] = 0ull;
+                        UVm[slots_max_n + v * gridDim.y + blockIdx.y] = 0ull;
+                    } else if (umode) {
                         UV[v] = 0ull;
                         UV[slots_max_n + v] = 0ull;
                     } else {
@@ -282,13 +288,13 @@ void compute_digests(const Samples& S, cudaStream_t st) {
 }
 
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
-                     cudaStream_t st, unsigned long long* d_elog, bool wide, bool umode) {
+                     cudaStream_t st, unsigned long long* d_elog, bool wide, int umode) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
                                              S.sizes.as<uint32_t>(), d_elog,
                                              S.count0.as<uint32_t>(), slots_max == 1 ? 1 : 0,
-                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n, umode ? 1 : 0,
+                                             wide ? kWide : 1u, wide ? (uint64_t)1 : (uint64_t)S.n, umode,
                                              S.sorted ? S.slot_sample.as<uint32_t>() : nullptr, S.s0);
     count_launch();
     ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize");
@@ -297,7 +303,7 @@ void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t 
 // graph node for the finaliser (device-resident batch loop)
 void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulonglong2* VN, const Ctl* ctl,
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
-                     bool wide, bool umode) {
+                     bool wide, int umode) {
     uint64_t chunk = 0;
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     uint64_t* store = S.store.as<uint64_t>();
@@ -308,7 +314,7 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
     int single = slots_max == 1 ? 1 : 0;
     uint32_t vstride = wide ? kWide : 1u;
     uint64_t sstride = wide ? 1 : (uint64_t)n;
-    int um = umode ? 1 : 0;
+    int um = umode;
     const uint32_t* slot_sample = S.sorted ? S.slot_sample.as<uint32_t>() : nullptr;
     uint64_t s0 = S.s0;
     void* fin_args[] = {&VN, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog,

@@ -38,7 +38,7 @@ def test_header_constants_match_binding():
     defs = {k: int(v.rstrip("u"), 0) for k, v in re.findall(r"#define (BPT_FLAG_[A-Z_]+) (\w+)", hdr)}
     assert defs == {f"BPT_{name}": getattr(bpt, name) for name in
                     ("FLAG_PROFILE", "FLAG_WIDE", "FLAG_SPARSE", "FLAG_LT_FUSED", "FLAG_LT_DENSE", "FLAG_LT_REWALK",
-                     "FLAG_LT_LEVELS", "FLAG_QUEUE", "FLAG_UNSORTED", "FLAG_PULL")}
+                     "FLAG_LT_LEVELS", "FLAG_QUEUE", "FLAG_UNSORTED", "FLAG_PULL", "FLAG_SLOTWISE")}
     flags = list(defs.values())
     assert len(set(flags)) == len(flags) and all(f & (f - 1) == 0 for f in flags)  # distinct single bits
     enums = dict((k, int(v)) for k, v in re.findall(r"(BPT_E[A-Z]+|BPT_OK)\s*=\s*(-?\d+)", hdr))

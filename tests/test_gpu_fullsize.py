@@ -4,6 +4,7 @@ only) where the oracle needs tens of minutes (C2 all 65,536 samples, C4), else r
 Bar (SURVEY §8(c) parity protocol): bit-exact RRR sets (all sizes + digests; member lists where
 stored or sampled), seeds, gains; sigma_hat identical (same integers, same f64 formula); exact
 E_phys / E_logical / per-level frontier sizes."""
+import json
 import os
 
 import numpy as np
@@ -48,7 +49,7 @@ def test_c2_full_theta(bpt, c2):
     cfg, row_ptr, col, thr, gold, g = c2
     # consecutive-sample groups here (the golden group work is of those groups); the default
     # sorted start vertices are checked in test_c2_full_sorted_start_vertices
-    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED)
+    s = g.sample(cfg.theta, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED | bpt.FLAG_SLOTWISE)
     assert np.array_equal(s.sizes(0, cfg.theta), gold["sizes"])
     assert np.array_equal(s.digests(0, cfg.theta), gold["digests"])
     info = s.info
@@ -120,10 +121,34 @@ def test_c2_full_sorted_start_vertices(bpt, c2):
     s.close()
 
 
+def test_c2_full_batch_wide_frontier(bpt, c2):
+    """The bench's launch configuration: sorted start vertices and one frontier per batch of 4
+    blocks (the default). The edge reads, level count and per-level frontier sizes of batches 0 and
+    90 equal the oracle's fused traversal of their 256 samples, and with one frontier per block
+    (BPT_FLAG_SLOTWISE) the edge reads equal the sum of the four 64-sample groups (golden
+    c2_sorted_batch_groups_oracle.json, scripts/batch_groups_oracle.py, oracle/ only)."""
+    cfg, row_ptr, col, thr, gold, g = c2
+    bg = json.load(open(os.path.join(GOLD, "c2_sorted_batch_groups_oracle.json")))
+    assert bg["seed"] == cfg.seed
+    for flags, key in ((0, "e_phys_256"), (bpt.FLAG_SLOTWISE, "e_phys_4x64")):
+        s = g.sample(cfg.theta, colors=64, seed=cfg.seed, flags=flags)
+        assert s.info["batch_groups"] == 4
+        rows = s.level_stats()
+        for b, want in bg["batches"].items():
+            r = rows[rows[:, 0] == int(b)]
+            exp = want[key] if key == "e_phys_256" else sum(want[key])
+            assert int(r[:, 4].sum()) == exp, f"edge reads of batch {b}"
+            if not flags:
+                assert len(r) == want["levels_256"]
+                assert r[:, 2].tolist() == want["frontier_256"], f"frontier sizes of batch {b}"
+        assert np.array_equal(s.digests(0, cfg.theta), gold["digests"])
+        s.close()
+
+
 def test_c2_full_graph_theta_2048(bpt, c2):
     """The C2 graph with theta = 2,048 (32 groups): sizes, digests, seeds, gains, sigma_hat."""
     cfg, row_ptr, col, thr, gold, g = c2
-    s = g.sample(2048, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED)
+    s = g.sample(2048, colors=64, seed=cfg.seed, flags=bpt.FLAG_UNSORTED | bpt.FLAG_SLOTWISE)
     assert np.array_equal(s.sizes(0, 2048), gold["sizes"][:2048])
     assert np.array_equal(s.digests(0, 2048), gold["digests"][:2048])
     assert s.info["e_phys"] == int(gold["e_phys"][:32].sum())

@@ -284,10 +284,12 @@ def test_c1_full_parity(bpt, colors):
         info = s.info
         # exact work counters: E_phys = sum over traversal groups of the
         # distinct (v, level) pairs weighted by in-degree; E_logical = unfused reads. With 64
-        # colours the groups are 64 samples in sorted start order (BPT_FLAG_UNSORTED off)
+        # colours the samples are in sorted start order (BPT_FLAG_UNSORTED off) and a batch of
+        # <= 4 blocks shares one frontier (BPT_FLAG_SLOTWISE off): one group per batch
         order = (sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed) if colors == 64
                  else np.arange(cfg.theta))
-        e_phys = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, colors))
+        group = 64 * info["batch_groups"] if colors == 64 and info["batch_groups"] <= 4 else colors
+        e_phys = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, group))
         assert info["e_phys"] == e_phys
         assert info["e_logical"] == int(ref["elog"].sum())
         assert info["members"] == int(ref["sizes"].sum())
@@ -392,8 +394,9 @@ def test_level_loop_variants(bpt, model):
         row_ptr, col, thr = graphgen.make_graph(cfg)
         ref = oracle_all(row_ptr, col, thr, oracle.IC, cfg.theta, cfg.seed, k=cfg.k)
         g = bpt.Graph(row_ptr, col, w_q31=thr)
-        # consecutive-sample groups in both forms (equal work counters), then the default sorted slots
-        variants = [bpt.FLAG_UNSORTED, bpt.FLAG_QUEUE, 0]
+        # consecutive-sample 64-colour groups in both forms (equal work counters), then the default
+        # (sorted slots, one frontier per batch)
+        variants = [bpt.FLAG_UNSORTED | bpt.FLAG_SLOTWISE, bpt.FLAG_QUEUE, 0]
     else:
         cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 12, theta=2048)
         row_ptr, col, thr = graphgen.make_graph(cfg)
@@ -695,20 +698,31 @@ def test_sorted_start_slots(bpt, c2_small):
     assert np.array_equal(srt.occurrences(), uns.occurrences())
     order = sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed)
     B = srt.info["batch_groups"]
-    want = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64))
-    assert srt.info["e_phys"] == want
+    # the default form: one frontier per batch of B blocks = one fused group of 64 B samples
+    ws = group_e_phys(ref["g"], cfg.seed, order, 64 * B)
+    assert srt.info["e_phys"] == sum(w["e_phys"] for w in ws)
     assert srt.info["e_phys"] < uns.info["e_phys"]
     assert srt.info["e_logical"] == uns.info["e_logical"] == int(ref["elog"].sum())
     rows = srt.level_stats()
-    ws = group_e_phys(ref["g"], cfg.seed, order, 64)
-    for b in range(len(ws) // B):  # per batch of B slots: the sum of its groups' edge reads
-        assert int(rows[rows[:, 0] == b][:, 4].sum()) == sum(w["e_phys"] for w in ws[B * b:B * b + B])
+    for b, w in enumerate(ws):  # per batch: edge reads, levels and per-level frontier sizes of its group
+        r = rows[rows[:, 0] == b]
+        assert int(r[:, 4].sum()) == w["e_phys"]
+        assert r[:, 2].tolist() == w["frontier"].tolist()
+    # one frontier per block (BPT_FLAG_SLOTWISE): 64-sample groups, summed per batch
+    sw = g.sample(cfg.theta, seed=cfg.seed, flags=bpt.FLAG_SLOTWISE)
+    check_full(bpt, sw, ref, cfg.theta)
+    ws64 = group_e_phys(ref["g"], cfg.seed, order, 64)
+    assert sw.info["e_phys"] == sum(w["e_phys"] for w in ws64) > srt.info["e_phys"]
+    rows = sw.level_stats()
+    for b in range(len(ws64) // B):
+        assert int(rows[rows[:, 0] == b][:, 4].sum()) == sum(w["e_phys"] for w in ws64[B * b:B * b + B])
     for W, r in ((3, 1), (3, 2)):
         s0, s1 = graphgen.shard_range(cfg.theta, W, r)
         sh = g.sample(cfg.theta, seed=cfg.seed, shard=(W, r))
         assert np.array_equal(sh.digests(s0, s1 - s0), ref["digests"][s0:s1])
         order = sorted_slots(row_ptr, col, cfg.n, s1, cfg.seed, s0=s0)
-        assert sh.info["e_phys"] == sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64))
+        Bs = sh.info["batch_groups"]
+        assert sh.info["e_phys"] == sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, 64 * Bs))
 
 
 # ------------------------------------------------------------------ pull expansion
@@ -728,7 +742,7 @@ def test_pull_levels_parity(bpt, c2_small, permille):
     lists, seeds, gains, sigma, E_phys and the per-level structure equal the oracle / the push form."""
     cfg, row_ptr, col, thr, ref = c2_small
     g = bpt.Graph(row_ptr, col, w_q31=thr)
-    push = g.sample(cfg.theta, seed=cfg.seed)
+    push = g.sample(cfg.theta, seed=cfg.seed, flags=bpt.FLAG_SLOTWISE)  # the pull form keeps one frontier per block
     s = g.sample(cfg.theta, seed=cfg.seed, pull=True, pull_permille=permille)
     check_full(bpt, s, ref, cfg.theta)
     seeds, gains, sigma = s.select_seeds(cfg.k)
