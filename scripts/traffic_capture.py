@@ -18,14 +18,15 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "gpurun_out")
 
 
-def alg_bytes(rows):
-    """DESIGN.md §6 per-level byte model (same as bpt_samples_info.expand_bytes): 16 B per reverse-edge
-    read, 8 B per atomicOr, 24 B per frontier entry, 8 B per vertex discovered for the next level."""
+def alg_bytes(rows, slots=4):
+    """DESIGN.md §6 per-level byte model of the batch-wide frontier (same as
+    bpt_samples_info.expand_bytes): 8 B record + 8 B x S of U[u] per reverse-edge read, 8 B per
+    atomicOr, (4 + 8 S) B per frontier entry, 8 B per vertex discovered for the next level."""
     out = []
     for i, r in enumerate(rows):
         batch, level, raw, kept, work, vc, coins, atomics = r
         raw_next = rows[i + 1][2] if i + 1 < len(rows) and rows[i + 1][0] == batch else 0
-        out.append(16.0 * work + 8.0 * atomics + 24.0 * kept + 8.0 * raw_next)
+        out.append((8.0 + 8.0 * slots) * work + 8.0 * atomics + (4.0 + 8.0 * slots) * kept + 8.0 * raw_next)
     return out
 
 
