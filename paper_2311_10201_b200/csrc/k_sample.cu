@@ -1207,6 +1207,40 @@ __device__ __forceinline__ uint32_t philox_ks0(uint32_t x0, uint32_t x1, const u
     return x0;
 }
 
+// Philox2x32-10 from round 1 on, round 0 done by the caller: h0 = hi(M * x0) ^ ks[0], l0 = lo(M * x0)
+// (x0 = the edge id is shared by all colours of an item, x1 = the sample id is not)
+__device__ __forceinline__ uint32_t philox_from1(uint32_t h0, uint32_t l0, uint32_t x1, const uint32_t (&ks)[10]) {
+    uint32_t x0 = h0 ^ x1;
+    x1 = l0;
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        const uint64_t p = (uint64_t)kPhiloxM * (uint64_t)x0;
+        const uint32_t hi = (uint32_t)(p >> 32), lo = (uint32_t)p;
+        x0 = hi ^ ks[r] ^ x1;
+        x1 = lo;
+    }
+    return x0;
+}
+
+// Sample ids of the colours of the batch's slots in shared memory (the coins' counter word):
+// sidt[64 slot + bit] = slot_sample[64 (blk0 + slot) + bit] with sorted start vertices, else the
+// global id 64 (gblk0 + slot) + bit; nullptr when the batch has more than kSidSlots slots
+constexpr uint32_t kSidSlots = 4;  // the product's batch (1 KB of shared memory: more would cut the L1)
+__device__ __forceinline__ const uint32_t* fill_sid_table(const BatchArgs& a, uint32_t* sidt, uint64_t gblk0) {
+#ifdef BPT_NO_SIDT
+    return nullptr;
+#endif
+    if (a.slots_max > kSidSlots) return nullptr;
+    for (uint32_t i = threadIdx.x; i < a.slots_max * 64; i += blockDim.x) {
+        const uint64_t li = 64ull * gblk0 + i;
+        sidt[i] = a.slot_sample ? (li < a.nlocal ? __ldg(&a.slot_sample[li]) : 0u) : (uint32_t)li;
+    }
+    return sidt;
+}
+__device__ __forceinline__ uint32_t coin_sample(const BatchArgs& a, const uint32_t* sidt, uint32_t sbase, uint32_t sid) {
+    return sidt ? sidt[sid - sbase] : (a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid);
+}
+
 // position of the r-th (0-based) set bit of the 64-bit mask hi:lo: the 32-bit half by one popcount,
 // the byte by SWAR byte popcounts and their prefix sums (compared with r in all bytes at once), the
 // bit inside the byte from a 256-entry table of packed 3-bit positions (shared memory)
@@ -1255,6 +1289,7 @@ __device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, ui
 __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
                                                    uint32_t nlive, unsigned long long& coins,
                                                    unsigned long long& atoms, bool& any_pass,
+                                                   const uint32_t* sidt, uint32_t sbase,
                                                    unsigned long long* fold = nullptr) {
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
     for (uint32_t c0 = 0; c0 < nlive; c0 += 32) {
@@ -1275,15 +1310,13 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             const uint32_t hj = __ffs(hb) - 1;
             const uint4 it = W.A[c0 + hj];  // broadcast
             const uint32_t sb = W.B[c0 + hj].x;
+            const uint64_t pe = (uint64_t)kPhiloxM * it.x;  // round 0's product: once for the item's 64 coins
+            const uint32_t h0 = (uint32_t)(pe >> 32) ^ a.ic_keys[0], l0 = (uint32_t)pe;
             bool p0 = false, p1 = false;
-            if ((it.z >> lane) & 1u) {
-                const uint32_t sid = sb + lane;
-                p0 = (philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys) >> 1) < it.y;
-            }
-            if ((it.w >> lane) & 1u) {
-                const uint32_t sid = sb + 32 + lane;
-                p1 = (philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys) >> 1) < it.y;
-            }
+            if ((it.z >> lane) & 1u)
+                p0 = (philox_from1(h0, l0, coin_sample(a, sidt, sbase, sb + lane), a.ic_keys) >> 1) < it.y;
+            if ((it.w >> lane) & 1u)
+                p1 = (philox_from1(h0, l0, coin_sample(a, sidt, sbase, sb + 32 + lane), a.ic_keys) >> 1) < it.y;
             const uint32_t lo = __ballot_sync(kFull, p0), hi = __ballot_sync(kFull, p1);
             if (lane == (int)hj) hpass = ((unsigned long long)hi << 32) | lo;
         }
@@ -1312,8 +1345,7 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
-                const uint32_t sid = W.B[c0 + o].x + bit;  // slot index (sorted) or sample id
-                const uint32_t x = philox_ks0(it.x, a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid, a.ic_keys);
+                const uint32_t x = philox_ks0(it.x, coin_sample(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
                 if ((x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
@@ -1340,7 +1372,8 @@ template <bool kWhole>
 __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane, uint32_t le_mask,
                                                uint32_t unit, uint32_t rem, uint32_t jc0, uint32_t mword,
                                                uint64_t gblk0, unsigned long long& coins,
-                                               unsigned long long& atoms, bool& any_pass) {
+                                               unsigned long long& atoms, bool& any_pass,
+                                               const uint32_t* sidt, uint32_t sbase) {
     const uint32_t t0l = unit * (uint32_t)kUnitBm;  // mod 2^32: edge ids are t + delta (mod 2^32)
     // entry-start words of the unit (prefetched one unit ahead: lane w holds word w)
     uint32_t mw[kWinBm];
@@ -1395,7 +1428,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
     }
     if (nlive == 0) return;
     __syncwarp();
-    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
 }
 
 
@@ -1409,7 +1442,7 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
                                                 uint32_t le_mask, uint32_t unit, uint32_t rem, uint32_t jc0,
                                                 uint32_t mword, uint64_t gblk0, uint32_t nslots,
                                                 unsigned long long& coins, unsigned long long& atoms,
-                                                bool& any_pass) {
+                                                bool& any_pass, const uint32_t* sidt, uint32_t sbase) {
     const uint32_t t0l = unit * (uint32_t)kUnitBm;
     uint32_t mw[kWinBm];
 #pragma unroll
@@ -1486,7 +1519,7 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
         if (wtot == 0) continue;
         if (nlive + wtot > (uint32_t)kUnitBm) {  // the list is full: draw its coins first
             __syncwarp();
-            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
             __syncwarp();
             nlive = 0;
         }
@@ -1502,7 +1535,7 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
     }
     if (nlive == 0) return;
     __syncwarp();
-    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass);
+    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
 }
 
 #ifndef BPT_BM_MINB
@@ -1538,12 +1571,15 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
     BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
     __shared__ unsigned long long red[kWarps];
     __shared__ uint32_t sel8[256];  // bit positions of every byte value, 3 bits each (rank_select64)
+    __shared__ uint32_t sid_sh[kSidSlots * 64];
     {
         uint32_t t = 0;
         for (uint32_t p = 0, j = 0; p < 8; ++p)
             if ((threadIdx.x >> p) & 1u) t |= p << (3 * j++);
         sel8[threadIdx.x] = t;
     }
+    const uint32_t* sidt = fill_sid_table(a, sid_sh, gblk0);
+    const uint32_t sbase = (uint32_t)(64ull * gblk0);
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t le_mask = lane == 31 ? kFull : ((2u << lane) - 1u);
@@ -1571,15 +1607,16 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
         if (kVmajor) {
             if (unit < nfull)
                 expand_unit_bmv<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, nslots, coins, atoms,
-                                      any_pass);
+                                      any_pass, sidt, sbase);
             else
                 expand_unit_bmv<false>(a, W, sel8, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0,
-                                       mword, gblk0, nslots, coins, atoms, any_pass);
+                                       mword, gblk0, nslots, coins, atoms, any_pass, sidt, sbase);
         } else if (unit < nfull) {
-            expand_unit_bm<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass);
+            expand_unit_bm<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, coins, atoms, any_pass, sidt,
+                                 sbase);
         } else {
             expand_unit_bm<false>(a, W, sel8, lane, le_mask, unit, (uint32_t)(total - (uint64_t)unit * kUnitBm), jc0, mword,
-                                  gblk0, coins, atoms, any_pass);
+                                  gblk0, coins, atoms, any_pass, sidt, sbase);
         }
     }
     if (__any_sync(kFull, any_pass) && lane == 0) Ln->any = 1;
@@ -1641,6 +1678,9 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_pull(BatchArgs
         sel8[threadIdx.x] = t;
     }
     for (int i = lane; i < 4 * 32; i += 32) fold[i] = 0ull;
+    __shared__ uint32_t sid_sh[kSidSlots * 64];
+    const uint32_t* sidt = fill_sid_table(a, sid_sh, gblk0);
+    const uint32_t sbase = (uint32_t)(64ull * gblk0);
     __syncthreads();
     const uint32_t lt_mask = (1u << lane) - 1u;
     const unsigned long long* U = reinterpret_cast<const unsigned long long*>(a.VN);
@@ -1681,7 +1721,7 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_pull(BatchArgs
         uint32_t nlive = 0, deferred = 0;  // pending live items, steps since the last coin call
         auto flush = [&]() {
             __syncwarp();
-            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, fold);
+            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase, fold);
             __syncwarp();
 #pragma unroll
             for (uint32_t sl = 0; sl < 4; ++sl) {  // early exit: the colours this lane's u just got
