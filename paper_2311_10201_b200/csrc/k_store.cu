@@ -130,6 +130,103 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(ulonglong2* __restrict
     }
 }
 
+
+// Vertex-major finaliser (batch-wide frontier, umode 2): one thread per vertex handles the S <= 4
+// slots of the batch -- one 32-B read of V[v][0..S), S coalesced store writes, U / V re-zeroed with
+// 16-B stores, occurrences without atomics (one writer per vertex), per-colour sizes of every slot
+// (lane l counts colours l and l + 32 of the warp's non-zero masks, broadcast from shared memory).
+__global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* __restrict__ UV, uint64_t* __restrict__ store,
+                                                            uint32_t n, const Ctl* __restrict__ ctl, uint64_t chunk,
+                                                            const uint32_t* __restrict__ roff, uint64_t nlocal,
+                                                            uint32_t* __restrict__ sizes,
+                                                            unsigned long long* __restrict__ elog_total,
+                                                            uint32_t* __restrict__ count0, uint32_t S,
+                                                            const uint32_t* __restrict__ slot_sample, uint64_t s0) {
+    constexpr int kW = kFinThreads / 32;
+    __shared__ unsigned long long s_mask[kW][32];
+    __shared__ uint32_t s_size[kW][4][64];
+    __shared__ unsigned long long s_el[kW];
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // launch evidence (Ctl::kernels_run)
+        atomicAdd(&const_cast<Ctl*>(ctl)->kernels_run, 1ull);
+    const uint32_t nsl = ctl->slots;
+    const uint64_t blk0 = ctl->blk0;
+    unsigned long long* V = UV + (size_t)S * n;
+    const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
+    const uint64_t v_end = umin64(v_begin + chunk, n);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t sz[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    unsigned long long el = 0;
+    for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
+        const uint64_t v = base + lane;
+        unsigned long long m[4] = {0ull, 0ull, 0ull, 0ull};
+        if (v < v_end) {
+            if (S == 4) {
+                const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(V + v * 4);
+                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(V + v * 4 + 2);
+                m[0] = a.x; m[1] = a.y; m[2] = b.x; m[3] = b.y;
+            } else {
+#pragma unroll
+                for (uint32_t s = 0; s < 4; ++s) m[s] = s < S ? V[v * S + s] : 0ull;
+            }
+#pragma unroll
+            for (uint32_t s = 0; s < 4; ++s)
+                if (s < nsl) store[(size_t)(blk0 + s) * n + v] = m[s];
+            const bool any = (m[0] | m[1] | m[2] | m[3]) != 0ull;
+            if (any) {
+                if (S == 4) {
+                    const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+                    *reinterpret_cast<ulonglong2*>(V + v * 4) = z;
+                    *reinterpret_cast<ulonglong2*>(V + v * 4 + 2) = z;
+                    *reinterpret_cast<ulonglong2*>(UV + v * 4) = z;
+                    *reinterpret_cast<ulonglong2*>(UV + v * 4 + 2) = z;
+                } else {
+                    for (uint32_t s = 0; s < S; ++s) { V[v * S + s] = 0ull; UV[v * S + s] = 0ull; }
+                }
+                const uint32_t pc = __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
+                count0[v] += pc;  // occurrences (A7 round 0); one writer per vertex
+                el += (unsigned long long)pc * (roff[v + 1] - roff[v]);  // E_logical: unfused reads
+            }
+        }
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) {
+            uint32_t b = __ballot_sync(0xffffffffu, m[s] != 0ull);
+            if (!b) continue;
+            s_mask[wid][lane] = m[s];
+            __syncwarp();
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                const unsigned long long mj = s_mask[wid][j];
+                sz[s][0] += (uint32_t)(mj >> lane) & 1u;
+                sz[s][1] += (uint32_t)(mj >> (lane + 32)) & 1u;
+            }
+            __syncwarp();
+        }
+    }
+#pragma unroll
+    for (uint32_t s = 0; s < 4; ++s) {
+        s_size[wid][s][lane] = sz[s][0];
+        s_size[wid][s][lane + 32] = sz[s][1];
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) el += __shfl_xor_sync(0xffffffffu, el, d);
+    if (lane == 0) s_el[wid] = el;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 4 * 64; i += kFinThreads) {
+        const uint32_t s = i / 64, c = i % 64;
+        if (s >= nsl) continue;
+        uint32_t T = 0;
+        for (int q = 0; q < kW; ++q) T += s_size[q][s][c];
+        const uint64_t li = 64ull * (blk0 + s) + c;  // local slot = local sample index unless start-sorted
+        if (li < nlocal && T) atomicAdd(&sizes[slot_sample ? slot_sample[li] - s0 : li], T);
+    }
+    if (threadIdx.x == 0) {
+        unsigned long long E = 0;
+        for (int q = 0; q < kW; ++q) E += s_el[q];
+        if (E) atomicAdd(elog_total, E);
+    }
+}
+
 // Per-sample digests, computed on demand from the store (verification
 // checksums, not part of the method): block (r, g) accumulates colour sums of splitmix64(v)
 // over vertices [r*chunk, (r+1)*chunk) of local block g.
@@ -290,6 +387,16 @@ void compute_digests(const Samples& S, cudaStream_t st) {
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog, bool wide, int umode) {
     uint64_t chunk = 0;
+    if (umode == 2) {
+        const dim3 grid = finalize_grid(S.n, 1, &chunk);
+        k_finalize_v<<<grid.x, kFinThreads, 0, st>>>(reinterpret_cast<unsigned long long*>(VN), S.store.as<uint64_t>(),
+                                                     S.n, ctl, chunk, roff, S.s1 - S.s0, S.sizes.as<uint32_t>(), d_elog,
+                                                     S.count0.as<uint32_t>(), slots_max,
+                                                     S.sorted ? S.slot_sample.as<uint32_t>() : nullptr, S.s0);
+        count_launch();
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_finalize_v");
+        return;
+    }
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     k_finalize<<<grid, kFinThreads, 0, st>>>(VN, S.store.as<uint64_t>(), S.n, ctl, chunk, roff, S.s1 - S.s0,
                                              S.sizes.as<uint32_t>(), d_elog,
@@ -305,6 +412,25 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
                      uint32_t slots_max, const uint32_t* roff, unsigned long long* d_elog, cudaGraphNode_t* last,
                      bool wide, int umode) {
     uint64_t chunk = 0;
+    if (umode == 2) {
+        const dim3 grid = finalize_grid(S.n, 1, &chunk);
+        unsigned long long* UV = reinterpret_cast<unsigned long long*>(VN);
+        uint64_t* store = S.store.as<uint64_t>();
+        uint32_t n = S.n, Sl = slots_max;
+        uint64_t nlocal = S.s1 - S.s0, s0 = S.s0;
+        uint32_t* sizes = S.sizes.as<uint32_t>();
+        uint32_t* count0 = S.count0.as<uint32_t>();
+        const uint32_t* slot_sample = S.sorted ? S.slot_sample.as<uint32_t>() : nullptr;
+        void* args[] = {&UV, &store, &n, (void*)&ctl, &chunk, (void*)&roff, &nlocal, &sizes, &d_elog, &count0, &Sl,
+                        (void*)&slot_sample, &s0};
+        cudaKernelNodeParams p{};
+        p.func = (void*)k_finalize_v;
+        p.gridDim = dim3(grid.x);
+        p.blockDim = dim3(kFinThreads);
+        p.kernelParams = args;
+        BPT_CUDA(cudaGraphAddKernelNode(last, g, &dep, 1, &p));
+        return;
+    }
     const dim3 grid = finalize_grid(S.n, slots_max, &chunk);
     uint64_t* store = S.store.as<uint64_t>();
     uint32_t n = S.n;
