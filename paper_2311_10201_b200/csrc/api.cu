@@ -57,6 +57,11 @@ struct Pool {
     std::mutex mu;
     std::multimap<size_t, Cached> free_blocks[64];  // per device: size -> block
     size_t cached[64] = {};
+    size_t held[64] = {};   // bytes this library holds from cudaMalloc (in use + cached)
+    // free-memory estimate (free_estimate): one cudaMemGetInfo snapshot per device and the bytes
+    // held at that moment; the snapshot is refreshed every kMemInfoTtl seconds
+    double snap_t[64] = {};
+    size_t snap_free[64] = {}, snap_held[64] = {};
 };
 Pool& pool() {
     static Pool* p = new Pool();  // never destroyed: the CUDA context may be gone at exit
@@ -73,6 +78,26 @@ int current_device() {
     return d < 0 || d >= 64 ? 0 : d;
 }
 }  // namespace
+
+// Free device memory, estimated without a cudaMemGetInfo per call (it stalled bpt_sample and the
+// selection for 10-40 ms at times, on every rank of a multi-GPU step): the last snapshot's free
+// bytes minus what this library allocated since (other allocators are seen at the next refresh)
+size_t free_estimate() {
+    constexpr double kMemInfoTtl = 30.0;
+    Pool& P = pool();
+    const int dev = current_device();
+    const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.snap_t[dev] == 0.0 || now - P.snap_t[dev] > kMemInfoTtl) {
+        size_t f = 0, t = 0;
+        if (cudaMemGetInfo(&f, &t) != cudaSuccess) { cudaGetLastError(); f = 0; }
+        P.snap_t[dev] = now;
+        P.snap_free[dev] = f;
+        P.snap_held[dev] = P.held[dev];
+    }
+    const long long est = (long long)P.snap_free[dev] - ((long long)P.held[dev] - (long long)P.snap_held[dev]);
+    return est > 0 ? (size_t)est : 0;
+}
 
 size_t cached_bytes() {
     Pool& P = pool();
@@ -93,6 +118,7 @@ void release_cached_blocks() {
                 cudaEventDestroy(kv.second.ev);
             }
             cudaFree(kv.second.p);
+            P.held[d] -= kv.first;
         }
         P.free_blocks[d].clear();
         P.cached[d] = 0;
@@ -138,6 +164,9 @@ void DevBuf::alloc(size_t b) {
     bytes = b;
     device = dev;
     stream = g_cur_stream;
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.held[dev] += b;
 }
 void DevBuf::reset() {
     if (p) {
@@ -487,8 +516,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
         return sl * (uint64_t)n * 16 + raw_cap * 8 + q_cap * (vm ? 4 + 8 * sl : 16 + 8) + ts_cap * 20 +
                (bitmap ? (vm ? 1 : sl) * tiles * 128 : 0);
     };
-    size_t free_b = 0, total_b = 0;
-    BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t free_b = free_estimate();
     free_b += cached_bytes();  // the pool's cached blocks are released if an allocation needs them
     // pull expansion of the heavy levels (BPT_FLAG_PULL; touched-bitmap form): forward records
     // (16 B per edge, cached on the graph) + vertex-major frontier masks + the previous level's

@@ -343,5 +343,6 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
 int num_sms();
 void release_cached_blocks();
 size_t cached_bytes();  // bytes held by the device-memory pool of the current device
+size_t free_estimate(); // free device memory (cudaMemGetInfo snapshot minus this library's allocations since)
 
 }  // namespace bpt

@@ -186,8 +186,7 @@ static bool build_lists(const Samples& S, cudaStream_t st) {
     M.lists_built = true;
     const uint64_t nlocal = S.s1 - S.s0;
     const uint64_t bytes = S.info.members * 4 + (nlocal + 1) * 8;
-    size_t free_b = 0, total_b = 0;
-    BPT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = free_estimate() + cached_bytes();
     // lists pay off when they are much smaller than one pass over the store
     if (nlocal == 0 || bytes > free_b / 4 || bytes * 8 > S.store.bytes) return M.lists_ok = false;
     std::vector<uint32_t> sz(nlocal);
