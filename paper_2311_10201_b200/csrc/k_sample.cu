@@ -1237,7 +1237,10 @@ __device__ __forceinline__ const uint32_t* fill_sid_table(const BatchArgs& a, ui
     }
     return sidt;
 }
+// kTable: the table is known to exist (batch-wide frontier: <= 4 slots), no run-time test
+template <bool kTable = false>
 __device__ __forceinline__ uint32_t coin_sample(const BatchArgs& a, const uint32_t* sidt, uint32_t sbase, uint32_t sid) {
+    if (kTable) return sidt[sid - sbase];
     return sidt ? sidt[sid - sbase] : (a.slot_sample ? __ldg(&a.slot_sample[sid]) : sid);
 }
 
@@ -1286,6 +1289,7 @@ __device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, ui
 // touched word, bit}. One chunk of <= 32 live items at a time (one live item per lane).
 // fold (pull): the passing colours of every item are also OR-ed into fold[slot * 32 + owner lane]
 // (W.B.w = bit | owner lane << 8 | slot << 16), the owners' per-colour early exit
+template <bool kTable = false>
 __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
                                                    uint32_t nlive, unsigned long long& coins,
                                                    unsigned long long& atoms, bool& any_pass,
@@ -1314,9 +1318,9 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             const uint32_t h0 = (uint32_t)(pe >> 32) ^ a.ic_keys[0], l0 = (uint32_t)pe;
             bool p0 = false, p1 = false;
             if ((it.z >> lane) & 1u)
-                p0 = (philox_from1(h0, l0, coin_sample(a, sidt, sbase, sb + lane), a.ic_keys) >> 1) < it.y;
+                p0 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + lane), a.ic_keys) >> 1) < it.y;
             if ((it.w >> lane) & 1u)
-                p1 = (philox_from1(h0, l0, coin_sample(a, sidt, sbase, sb + 32 + lane), a.ic_keys) >> 1) < it.y;
+                p1 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + 32 + lane), a.ic_keys) >> 1) < it.y;
             const uint32_t lo = __ballot_sync(kFull, p0), hi = __ballot_sync(kFull, p1);
             if (lane == (int)hj) hpass = ((unsigned long long)hi << 32) | lo;
         }
@@ -1345,7 +1349,7 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
-                const uint32_t x = philox_ks0(it.x, coin_sample(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
+                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
                 if ((x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
@@ -1505,10 +1509,9 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
         const uint32_t e = t0l + 32u * w + lane + dl[w];
         // live slots of this lane's edge (slots past the batch's own have no colours, so no mask),
         // one warp scan places the window's items
-        uint32_t smask = 0;
+        uint32_t c = 0;
 #pragma unroll
-        for (uint32_t sl = 0; sl < 4; ++sl) smask |= live[sl] != 0ull ? 1u << sl : 0u;
-        const uint32_t c = __popc(smask);
+        for (uint32_t sl = 0; sl < 4; ++sl) c += live[sl] != 0ull;
         uint32_t incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -1519,23 +1522,24 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
         if (wtot == 0) continue;
         if (nlive + wtot > (uint32_t)kUnitBm) {  // the list is full: draw its coins first
             __syncwarp();
-            bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
+            bm_coins_and_merge<true>(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
             __syncwarp();
             nlive = 0;
         }
         uint32_t pos = nlive + incl - c;
-        for (uint32_t x = smask; x; x &= x - 1u) {
-            const uint32_t sl = __ffs(x) - 1u;
-            const unsigned long long lv = sl == 0 ? live[0] : sl == 1 ? live[1] : sl == 2 ? live[2] : live[3];  // registers
-            W.A[pos] = make_uint4(e, rc[w].y, (uint32_t)lv, (uint32_t)(lv >> 32));
-            W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), u * S + sl, u >> 5, u & 31u);
-            ++pos;
+#pragma unroll
+        for (uint32_t sl = 0; sl < 4; ++sl) {  // unrolled: live[sl] stays in registers
+            if (live[sl] != 0ull) {
+                W.A[pos] = make_uint4(e, rc[w].y, (uint32_t)live[sl], (uint32_t)(live[sl] >> 32));
+                W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), u * S + sl, u >> 5, u & 31u);
+                ++pos;
+            }
         }
         nlive += wtot;
     }
     if (nlive == 0) return;
     __syncwarp();
-    bm_coins_and_merge(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
+    bm_coins_and_merge<true>(a, W, sel8, lane, nlive, coins, atoms, any_pass, sidt, sbase);
 }
 
 #ifndef BPT_BM_MINB
