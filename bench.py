@@ -425,6 +425,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, row_ptr, col, thr, args.cpu_samples or None)
+    entry_colours = 64.0 * (infos[0]["batch_groups"] if cfg.model == "IC" and cfg.colors == 64 and infos
+                            and infos[0]["batch_groups"] <= 4 else 1)
     line = {
         "metric": METRICS.get(cfg.name, METRIC), "value": cfg.theta / (ms_max / 1000.0), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -437,9 +439,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "edges_visited_per_s": e_phys_all / (ms_max / 1000.0),
         "unfused_equiv_edges_per_s": e_log_all / (ms_max / 1000.0),
         "fusion_factor": e_log_all / e_phys_all if e_phys_all else None,
+        # live colours per frontier entry / the colours an entry carries (64 per block; the default
+        # IC 64-colour form shares one frontier entry between the <= 4 blocks of a batch)
         "frontier_occupancy": (float(np.mean([i["members"] for i in infos])) /
-                               (64.0 * float(np.mean([i["frontier_entries"] for i in infos])))
+                               (entry_colours * float(np.mean([i["frontier_entries"] for i in infos])))
                                if infos and infos[0]["frontier_entries"] else None),
+        "frontier_entry_colours": entry_colours,
         "ms_sample_per_step": ms_sample,
         "roofline": roofline,
         "cpu_baseline": cpu,
