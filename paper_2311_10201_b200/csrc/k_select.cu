@@ -1,10 +1,14 @@
 // k_select.cu -- A7 greedy max-k-cover seed selection over the fused RRR store.
 //
-// State (device): count[v] = uncovered samples of THIS rank containing v; cov[g] = covered
-// samples of local 64-sample block g; selected[v].
-// Round r:  (1) key[v] = selected ? 0 : count[v] << 32 | ~v   (max gain, smallest id,
-//               reading C-11); multi-rank: count is ReduceScatter'ed first and the
-//               per-rank maxima are AllReduce(max)'ed -- the only collectives.
+// State (device): count[v] = uncovered samples containing v (this rank's; with W > 1 ranks and a
+// dense store the GLOBAL count, see below); cov[g] = covered samples of local 64-sample block g;
+// selected[v].
+// Round r:  (1) key[v] = selected ? 0 : count[v] << 32 | ~v   (max gain, smallest id, reading C-11)
+//           multi-rank dense stores: the counts are AllReduce'd once, every
+//           rank takes the same argmax, round 0's decrements are AllReduce'd densely and later
+//           rounds' (few covered samples) are exchanged as AllGathered (vertex, decrement) pairs;
+//           if a rank's pairs overflow, the selection is redone with the per-round ReduceScatter of
+//           the counts and AllReduce(max) of the per-rank maxima.
 //           (2) new_g = V_g[v*] & ~cov_g ; cov_g |= new_g ; list the blocks with new_g != 0
 //           (3) count[v] -= sum over listed g of popcount(V_g[v] & new_g)
 // Each sample leaves `count` exactly once, so the decrements over all rounds cost at most one
@@ -95,6 +99,52 @@ __global__ void k_decrement(const uint64_t* __restrict__ store, uint32_t n, cons
         for (uint32_t i = 0; i < L; ++i) d += __popcll(store[(size_t)list[i] * n + v] & newm[i]);
         if (d) count[v] -= d;
     }
+}
+
+// Multi-rank dense stores, rounds >= 1: every rank keeps the GLOBAL counts,
+// so the argmax needs no collective; a round's decrements are sparse after round 0 (the later
+// seeds cover few samples), so each rank lists its nonzero decrements as (v | d << 32) pairs
+// (warp-aggregated appends, at most cap; more sets *overflow and the selection is redone with the
+// per-round ReduceScatter) and the pairs of all ranks are AllGathered and applied.
+__global__ void k_decrement_pairs(const uint64_t* __restrict__ store, uint32_t n, const uint32_t* __restrict__ nlist,
+                                  const uint32_t* __restrict__ list, const uint64_t* __restrict__ newm,
+                                  unsigned long long* __restrict__ pairs, uint32_t cap, uint32_t* __restrict__ npairs,
+                                  uint32_t* __restrict__ overflow) {
+    const uint32_t L = *nlist;
+    if (L == 0) return;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v0 = blockIdx.x * (uint64_t)blockDim.x; v0 < n; v0 += stride) {  // whole warps per pass
+        const uint64_t v = v0 + threadIdx.x;
+        uint32_t d = 0;
+        if (v < n)
+            for (uint32_t i = 0; i < L; ++i) d += __popcll(store[(size_t)list[i] * n + v] & newm[i]);
+        const uint32_t bal = __ballot_sync(0xffffffffu, d != 0);
+        if (!bal) continue;
+        uint32_t base = 0;
+        if (lane == __ffs(bal) - 1) base = atomicAdd(npairs, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+        if (d) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (pos < cap) pairs[pos] = (unsigned long long)v | ((unsigned long long)d << 32);
+            else *overflow = 1;
+        }
+    }
+}
+
+__global__ void k_apply_pairs(const unsigned long long* __restrict__ pairs, uint64_t total, uint32_t* __restrict__ count) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long p = pairs[i];
+        if (p != ~0ull) atomicSub(&count[(uint32_t)p], (uint32_t)(p >> 32));
+    }
+}
+
+__global__ void k_widen_flag(const uint32_t* __restrict__ flag, unsigned long long* __restrict__ out) {
+    if (threadIdx.x == 0) *out = *flag ? 1ull : 0ull;
+}
+
+__global__ void k_add_u32(uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t len) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) a[i] += b[i];
 }
 
 // sparse stores (e.g. LT): decrement through the members of the newly covered samples,
@@ -304,7 +354,21 @@ static void gather_lists(Samples& M, cudaStream_t st) {
     BPT_CUDA(cudaStreamSynchronize(st));
 }
 
+static void select_rounds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st,
+                          bool pair_exchange, bool* overflowed);
+
 void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st) {
+    const int world = S.comm ? S.comm->world : 1;
+    bool ovf = false;
+    // multi-rank dense stores: global counts + sparse decrement exchange; if any rank's decrements of
+    // some round outgrew the pair buffer, every rank redoes the selection with the per-round ReduceScatter
+    select_rounds(S, k, h_seeds, h_gains, st, world > 1 && !S.sparse, &ovf);
+    if (ovf) select_rounds(S, k, h_seeds, h_gains, st, false, &ovf);
+}
+
+static void select_rounds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_gains, cudaStream_t st,
+                          bool pair_exchange, bool* overflowed) {
+    *overflowed = false;
     const uint32_t n = S.n;
     Comm* comm = S.comm;
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
@@ -337,8 +401,46 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     DevBuf covered(S.sparse ? L.nlists * 4 + 4 : 4);
     if (S.sparse) BPT_CUDA(cudaMemsetAsync(covered.p, 0, covered.bytes, st));
     const auto t1 = clk::now();
+    // pair exchange (multi-rank dense stores): the counts become global once
+#ifndef BPT_PAIR_CAP
+#define BPT_PAIR_CAP (1u << 16)
+#endif
+    constexpr uint32_t kPairCap = BPT_PAIR_CAP;  // decrement pairs per rank and round (-D for the overflow test build)
+    DevBuf pairs(pair_exchange ? kPairCap * 8ull : 8), pairs_all(pair_exchange ? (uint64_t)world * kPairCap * 8 : 8),
+        npairs(8), tmp(pair_exchange ? (uint64_t)S.n_pad * 4 : 4);
+    if (pair_exchange) {
+        comm_allreduce_sum_u32(comm, count.as<uint32_t>(), S.n_pad, st);
+        BPT_CUDA(cudaMemsetAsync(npairs.p, 0, 8, st));  // [0] pairs of the round, [1] overflow
+    }
     for (uint32_t r = 0; r < k; ++r) {
         unsigned long long* key = keys.as<unsigned long long>() + r;
+        if (pair_exchange) {
+            // identical global counts on every rank: the same argmax everywhere, no collective
+            k_argmax<<<vgrid, kSelThreads, 0, st>>>(count.as<uint32_t>(), n, 0, n, sel.as<uint8_t>(), key,
+                                                    nlist.as<uint32_t>());
+            k_cover<<<ggrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, blocks, key, cov.as<uint64_t>(), sel.as<uint8_t>(),
+                                           nlist.as<uint32_t>(), list.as<uint32_t>(), newm.as<uint64_t>());
+            count_launch(2);
+            if (r == 0) {  // the first seed covers a large share of the samples: one dense exchange
+                BPT_CUDA(cudaMemsetAsync(tmp.p, 0, tmp.bytes, st));
+                k_decrement<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
+                                                   newm.as<uint64_t>(), tmp.as<uint32_t>());  // tmp = -d (mod 2^32)
+                comm_allreduce_sum_u32(comm, tmp.as<uint32_t>(), S.n_pad, st);
+                k_add_u32<<<dgrid, 256, 0, st>>>(count.as<uint32_t>(), tmp.as<uint32_t>(), S.n_pad);
+            } else {
+                BPT_CUDA(cudaMemsetAsync(pairs.p, 0xff, pairs.bytes, st));
+                BPT_CUDA(cudaMemsetAsync(npairs.p, 0, 4, st));
+                k_decrement_pairs<<<dgrid, 256, 0, st>>>(S.store.as<uint64_t>(), n, nlist.as<uint32_t>(), list.as<uint32_t>(),
+                                                         newm.as<uint64_t>(), pairs.as<unsigned long long>(), kPairCap,
+                                                         npairs.as<uint32_t>(), npairs.as<uint32_t>() + 1);
+                comm_allgather_u64(comm, pairs.as<uint64_t>(), pairs_all.as<uint64_t>(), kPairCap, st);
+                k_apply_pairs<<<num_sms() * 4, 256, 0, st>>>(pairs_all.as<unsigned long long>(),
+                                                             (uint64_t)world * kPairCap, count.as<uint32_t>());
+            }
+            count_launch(2);
+            ::bpt::check_cuda(cudaGetLastError(), "launch selection pair exchange");
+            continue;
+        }
         if (world > 1 && !S.sparse) {
             comm_reduce_scatter_u32(comm, count.as<uint32_t>(), shard.as<uint32_t>(), shard_len, st);
             k_argmax<<<vgrid, kSelThreads, 0, st>>>(shard.as<uint32_t>(), shard_len, (uint64_t)rank * shard_len, n,
@@ -373,6 +475,16 @@ void select_seeds(const Samples& S, uint32_t k, uint32_t* h_seeds, uint64_t* h_g
     }
     std::vector<unsigned long long> hk(k);
     BPT_CUDA(cudaMemcpyAsync(hk.data(), keys.p, (uint64_t)k * 8, cudaMemcpyDeviceToHost, st));
+    if (pair_exchange) {  // did any rank's pairs of any round overflow? (the same answer on every rank)
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(npairs.p);
+        // [1] (the overflow word) -> a u64 for the max-reduction
+        k_widen_flag<<<1, 32, 0, st>>>(npairs.as<uint32_t>() + 1, f);
+        comm_allreduce_max_u64(comm, f, 1, st);
+        unsigned long long hf = 0;
+        BPT_CUDA(cudaMemcpyAsync(&hf, f, 8, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
+        if (hf) { *overflowed = true; return; }
+    }
     BPT_CUDA(cudaStreamSynchronize(st));
     if (getenv("BPT_TRACE")) {
         auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
