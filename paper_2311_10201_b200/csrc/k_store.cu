@@ -278,9 +278,15 @@ __global__ void __launch_bounds__(kFinThreads) k_digests(const uint64_t* __restr
 constexpr int kExRounds = 32;
 constexpr uint32_t kExTile = 32 * kExRounds;
 
+// All requested store blocks in one launch: grid.y = j-th requested block (blk[j], colour set
+// cms[j]); its counts / positions are the j-th [64][ntiles] slab of tcnt / tpos, its colours'
+// output offsets cbase[64 j + c].
 // pass 1: per-(colour, tile) member counts, colour-major; colours outside the requested set cm = 0
-__global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint64_t cm,
-                                uint32_t ntiles, uint32_t* __restrict__ tcnt) {
+__global__ void k_extract_count(const uint64_t* __restrict__ store, uint32_t n, const uint64_t* __restrict__ blk,
+                                const uint64_t* __restrict__ cms, uint32_t ntiles, uint32_t* __restrict__ tcnt_all) {
+    const uint64_t* V = store + (size_t)blk[blockIdx.y] * n;
+    const uint64_t cm = cms[blockIdx.y];
+    uint32_t* tcnt = tcnt_all + (uint64_t)blockIdx.y * 64 * ntiles;
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     if (tile >= ntiles) return;
@@ -302,9 +308,13 @@ __global__ void k_extract_count(const uint64_t* __restrict__ V, uint32_t n, uint
 
 // pass 2: ordered scatter; tpos = exclusive colour-major scan of tcnt; colour c's members go to
 // cbase[c] + (its members in earlier tiles) + rank, vertices ascending (reading C-10)
-__global__ void k_extract_write(const uint64_t* __restrict__ V, uint32_t n, uint64_t cm,
-                                uint32_t ntiles, const uint32_t* __restrict__ tpos, const uint64_t* __restrict__ cbase,
-                                uint32_t* __restrict__ members) {
+__global__ void k_extract_write(const uint64_t* __restrict__ store, uint32_t n, const uint64_t* __restrict__ blk,
+                                const uint64_t* __restrict__ cms, uint32_t ntiles, const uint32_t* __restrict__ tpos_all,
+                                const uint64_t* __restrict__ cbase_all, uint32_t* __restrict__ members) {
+    const uint64_t* V = store + (size_t)blk[blockIdx.y] * n;
+    const uint64_t cm = cms[blockIdx.y];
+    const uint32_t* tpos = tpos_all + (uint64_t)blockIdx.y * 64 * ntiles;
+    const uint64_t* cbase = cbase_all + 64ull * blockIdx.y;
     const int lane = threadIdx.x & 31;
     const uint64_t tile = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     if (tile >= ntiles) return;
@@ -469,23 +479,36 @@ void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint6
         b.mask |= 1ull << (slot % 64);
         b.base[slot % 64] = h_offsets[i];
     }
-    std::vector<uint64_t> hbase(blocks.size() * 64, 0);
-    size_t bi = 0;
-    for (auto& kv : blocks) memcpy(&hbase[64 * bi++], kv.second.base, sizeof(kv.second.base));
-    DevBuf tcnt((uint64_t)64 * ntiles * 4), tmp(scan_temp_bytes((uint64_t)64 * ntiles)), dbase(hbase.size() * 8);
-    BPT_CUDA(cudaMemcpyAsync(dbase.p, hbase.data(), hbase.size() * 8, cudaMemcpyHostToDevice, st));
-    const unsigned grid = (unsigned)(((uint64_t)ntiles * 32 + 255) / 256);
-    bi = 0;
-    for (auto& kv : blocks) {
-        const uint64_t* V = S.store.as<uint64_t>() + (size_t)kv.first * n;
-        k_extract_count<<<grid, 256, 0, st>>>(V, n, kv.second.mask, ntiles, tcnt.as<uint32_t>());
+    // one slab per requested block: [blk ids | colour sets | colour offsets (64 per block)]; up to
+    // kExGroup blocks share the same three launches (with sorted start vertices 64 consecutive samples
+    // sit in up to 64 blocks; the group bounds the count slabs to kExGroup x 1.2 MB on C2)
+    constexpr uint64_t kExGroup = 64;
+    const uint64_t slab = (uint64_t)64 * ntiles;
+    std::vector<std::pair<uint64_t, const Blk*>> all;
+    for (auto& kv : blocks) all.emplace_back(kv.first, &kv.second);
+    const uint64_t gmax = umin64(kExGroup, all.size());
+    DevBuf tcnt(gmax * slab * 4), tmp(scan_temp_bytes(gmax * slab)), dhdr(gmax * (2 + 64) * 8);
+    for (uint64_t g0 = 0; g0 < all.size(); g0 += kExGroup) {
+        const uint64_t nb = umin64(kExGroup, all.size() - g0);
+        std::vector<uint64_t> hdr(nb * (2 + 64), 0);
+        for (uint64_t bi = 0; bi < nb; ++bi) {
+            hdr[bi] = all[g0 + bi].first;
+            hdr[nb + bi] = all[g0 + bi].second->mask;
+            memcpy(&hdr[2 * nb + 64 * bi], all[g0 + bi].second->base, sizeof(all[g0 + bi].second->base));
+        }
+        BPT_CUDA(cudaMemcpyAsync(dhdr.p, hdr.data(), hdr.size() * 8, cudaMemcpyHostToDevice, st));
+        const uint64_t* dblk = dhdr.as<uint64_t>();
+        const uint64_t* dcm = dblk + nb;
+        const uint64_t* dbase = dblk + 2 * nb;
+        const dim3 grid((unsigned)(((uint64_t)ntiles * 32 + 255) / 256), (unsigned)nb);
+        k_extract_count<<<grid, 256, 0, st>>>(S.store.as<uint64_t>(), n, dblk, dcm, ntiles, tcnt.as<uint32_t>());
         count_launch();
-        exclusive_scan_u32(tcnt.as<uint32_t>(), tcnt.as<uint32_t>(), (uint64_t)64 * ntiles, tmp.p, st);
-        k_extract_write<<<grid, 256, 0, st>>>(V, n, kv.second.mask, ntiles, tcnt.as<uint32_t>(),
-                                              dbase.as<uint64_t>() + 64 * bi++, d_members);
-        count_launch();
-        ::bpt::check_cuda(cudaGetLastError(), "launch k_extract_write");
+        exclusive_scan_u32(tcnt.as<uint32_t>(), tcnt.as<uint32_t>(), nb * slab, tmp.p, st);
+        k_extract_write<<<grid, 256, 0, st>>>(S.store.as<uint64_t>(), n, dblk, dcm, ntiles, tcnt.as<uint32_t>(), dbase,
+                                              d_members);
+        count_launch();  // the next group's header copy is stream-ordered after these kernels
     }
+    ::bpt::check_cuda(cudaGetLastError(), "launch k_extract_write");
 }
 
 }  // namespace bpt
