@@ -1317,10 +1317,18 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             const uint64_t pe = (uint64_t)kPhiloxM * it.x;  // round 0's product: once for the item's 64 coins
             const uint32_t h0 = (uint32_t)(pe >> 32) ^ a.ic_keys[0], l0 = (uint32_t)pe;
             bool p0 = false, p1 = false;
-            if ((it.z >> lane) & 1u)
-                p0 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + lane), a.ic_keys) >> 1) < it.y;
-            if ((it.w >> lane) & 1u)
-                p1 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + 32 + lane), a.ic_keys) >> 1) < it.y;
+            if (kTable) {  // both coins of every lane, branch-free (the table covers all 64 colours): two
+                           // independent Philox chains interleave, and >= half the bits are live anyway
+                const uint32_t x0 = philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + lane), a.ic_keys);
+                const uint32_t x1 = philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + 32 + lane), a.ic_keys);
+                p0 = ((it.z >> lane) & 1u) && (x0 >> 1) < it.y;
+                p1 = ((it.w >> lane) & 1u) && (x1 >> 1) < it.y;
+            } else {
+                if ((it.z >> lane) & 1u)
+                    p0 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + lane), a.ic_keys) >> 1) < it.y;
+                if ((it.w >> lane) & 1u)
+                    p1 = (philox_from1(h0, l0, coin_sample<kTable>(a, sidt, sbase, sb + 32 + lane), a.ic_keys) >> 1) < it.y;
+            }
             const uint32_t lo = __ballot_sync(kFull, p0), hi = __ballot_sync(kFull, p1);
             if (lane == (int)hj) hpass = ((unsigned long long)hi << 32) | lo;
         }
@@ -1335,14 +1343,15 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
         const uint32_t ntask = __shfl_sync(kFull, incl, 31);
         const uint32_t excl = incl - lcnt;
         __syncwarp();
+        uint32_t below = 0;  // live lanes whose tasks start before the window (carried from window to window)
         for (uint32_t b = 0; b < ntask; b += 32) {
             // owner of task b + i = (lanes with excl <= b + i) - 1 (every live item has >= 1 task, so the
-            // excl of the live lanes strictly increase): the lanes below the window by one ballot, the
-            // ranges starting inside it by one OR-reduction -- no search
-            const uint32_t below = __popc(__ballot_sync(kFull, has && excl < b));
+            // excl of the live lanes strictly increase): the lanes below the window plus the ranges
+            // starting inside it (one OR-reduction) -- no search
             const uint32_t d = excl - b;
             const uint32_t starts = __reduce_or_sync(kFull, (has && d < 32u) ? (1u << d) : 0u);
             const uint32_t o = (below + __popc(starts & le_mask) - 1u) & 31u;
+            below += __popc(starts);
             const uint32_t eo = __shfl_sync(kFull, excl, o);
             const bool oheavy = __shfl_sync(kFull, heavy, o);
             const uint32_t k = b + lane;
@@ -1511,7 +1520,7 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
         // one warp scan places the window's items
         uint32_t c = 0;
 #pragma unroll
-        for (uint32_t sl = 0; sl < 4; ++sl) c += live[sl] != 0ull;
+        for (uint32_t sl = 0; sl < 4; ++sl) c += ((uint32_t)live[sl] | (uint32_t)(live[sl] >> 32)) != 0u;
         uint32_t incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
