@@ -1355,7 +1355,14 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
             const uint32_t eo = __shfl_sync(kFull, excl, o);
             const bool oheavy = __shfl_sync(kFull, heavy, o);
             const uint32_t k = b + lane;
-            if (k < ntask && !oheavy) {
+            if (kTable) {  // branch-free: lanes past the last task compute a coin and drop it (bit < 64 always)
+                const bool act = k < ntask && !oheavy;
+                const uint4 it = W.A[c0 + o];
+                const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
+                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
+                if (act && (x >> 1) < it.y)
+                    atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
+            } else if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
                 const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
