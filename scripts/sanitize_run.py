@@ -1,8 +1,8 @@
 """Small end-to-end run of every execution form of the hot path, for compute-sanitizer
 (memcheck / racecheck / synccheck, one tool per run):
   compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/sanitize_run.py
-C1 (R-MAT scale 10) and a C2-shaped scale-14 graph (IC: touched-bitmap default, first-setter queue,
-C = 8, wide fusion, profile mode), a C3-shaped scale-12 graph (LT: sparse walks, dense walks, fused
+C1 (R-MAT scale 10) and a C2-shaped scale-14 graph (IC: batch-wide frontier default, one frontier per
+block, pull, first-setter queue, C = 8, wide fusion, profile mode), a C3-shaped scale-12 graph (LT: sparse walks, dense walks, fused
 level loop), selection, extraction; every result is checked against the CPU oracle, so a run that
 the tool passes is also a correct one."""
 import os
@@ -21,8 +21,11 @@ def main():
     torch.cuda.set_device(0)
     import paper_2311_10201_b200 as bpt
     cases = [("C1", None, 512, bpt.IC, [dict(), dict(flags=bpt.FLAG_QUEUE), dict(colors=8), dict(wide=True),
-                                         dict(profile=True), dict(batch_groups=3)]),
-             ("C2", 1 << 14, 320, bpt.IC, [dict(), dict(flags=bpt.FLAG_QUEUE), dict(wide=True), dict(profile=True)]),
+                                         dict(profile=True), dict(batch_groups=3), dict(flags=bpt.FLAG_SLOTWISE),
+                                         dict(pull=True, pull_permille=1), dict(batch_groups=8)]),
+             ("C2", 1 << 14, 320, bpt.IC, [dict(), dict(flags=bpt.FLAG_QUEUE), dict(wide=True), dict(profile=True),
+                                          dict(flags=bpt.FLAG_SLOTWISE | bpt.FLAG_UNSORTED),
+                                          dict(pull=True, pull_permille=1)]),
              ("C3", 1 << 12, 400, bpt.LT, [dict(), dict(flags=bpt.FLAG_LT_DENSE), dict(flags=bpt.FLAG_LT_FUSED),
                                           dict(flags=bpt.FLAG_LT_FUSED | bpt.FLAG_LT_LEVELS)])]
     for name, n, theta, model, variants in cases:
