@@ -2277,15 +2277,15 @@ __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, c
 #pragma unroll
     for (int j = 0; j < 8; ++j) k += (w0 + j >= a && w0 + j < b && ys[j] <= r) ? 1u : 0u;
     const uint32_t j = a + k;  // first index of [a, b) with cum > r, b if none
-    // register selects (no dynamic indexing: that would put the window in local memory)
-    uint32_t xj = 0, xa = 0, ya = 0, yb = 0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        xj = (w0 + t == j) ? xs[t] : xj;
-        xa = (w0 + t == a) ? xs[t] : xa;
-        ya = (w0 + t == a) ? ys[t] : ya;
-        yb = (w0 + t + 1 == b) ? ys[t] : yb;
-    }
+    // register selects (no dynamic indexing: that would put the window in local memory) as binary
+    // trees over the window offset (3 levels of SEL instead of 8 compares and 8 SELs per value)
+    auto pick = [&](const uint32_t (&vals)[8], uint32_t t) -> uint32_t {
+        const uint32_t l0 = (t & 1u) ? vals[1] : vals[0], l1 = (t & 1u) ? vals[3] : vals[2];
+        const uint32_t l2 = (t & 1u) ? vals[5] : vals[4], l3 = (t & 1u) ? vals[7] : vals[6];
+        const uint32_t m0 = (t & 2u) ? l1 : l0, m1 = (t & 2u) ? l3 : l2;
+        return (t & 4u) ? m1 : m0;
+    };
+    const uint32_t xj = pick(xs, (j - w0) & 7u), xa = pick(xs, a - w0), ya = pick(ys, a - w0), yb = pick(ys, b - 1 - w0);
     uint32_t clo, chi;
     uint2 hit;
     if (j < b) {
