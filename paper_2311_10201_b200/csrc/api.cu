@@ -531,7 +531,7 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     while (!wide && slots > 1 && plan_bytes(slots, raw_cap, q_cap, ts_cap) > free_b * 0.85) slots /= 2;
     while (!wide && slots > 1 && slots * (uint64_t)n >= (1ull << 32)) slots /= 2;  // 32-bit working-mask indices
     if (wide && (uint64_t)kWide * n >= (1ull << 32)) fail(BPT_EINVAL, "wide fusion needs kWide * n < 2^32");
-    if (slots > 4) vmajor = false;
+    if (slots > 4 || n >= (1u << 30)) vmajor = false;  // items pack u | slot << 30
     plan_bytes(slots, raw_cap, q_cap, ts_cap);
 
     const uint64_t nbatches = (S.blocks + slots - 1) / slots;

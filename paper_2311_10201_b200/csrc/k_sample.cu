@@ -1188,6 +1188,14 @@ constexpr int kHeavy = BPT_HEAVY;  // live colours from which an item's coins ar
 #define BPT_PULL_DEFER 4
 #endif
 constexpr uint32_t kPullDefer = BPT_PULL_DEFER;  // pull: steps whose live items may wait for one coin call
+// Batch-wide frontier (a.vmajor): an item's merge target and colour base follow from (u, slot), so B is
+// one word u | slot << 30 (n < 2^30) -- 12 KB less shared memory per block, more L1 for the gathers
+struct BmScratchV {
+    uint4 A[kUnitBm];
+    uint32_t B[kUnitBm];
+    unsigned long long pass[32];
+    uint2 cum[32];
+};
 struct BmScratch {
     uint4 A[kUnitBm];                       // live items: {edge id, thr, live lo, live hi}
     uint4 B[kUnitBm];                       // live items: {colour-0 sample id, VN index, touched word | ~0, bit}
@@ -1236,6 +1244,11 @@ __device__ __forceinline__ const uint32_t* fill_sid_table(const BatchArgs& a, ui
         sidt[i] = a.slot_sample ? (li < a.nlocal ? __ldg(&a.slot_sample[li]) : 0u) : (uint32_t)li;
     }
     return sidt;
+}
+// colour 0 of item j in the coins' sample numbering: the global id 64 (gblk0 + slot) (sbase = 64 gblk0)
+__device__ __forceinline__ uint32_t item_sample0(const BmScratch& W, uint32_t j, uint32_t) { return W.B[j].x; }
+__device__ __forceinline__ uint32_t item_sample0(const BmScratchV& W, uint32_t j, uint32_t sbase) {
+    return sbase + 64u * (W.B[j] >> 30);
 }
 // kTable: the table is known to exist (batch-wide frontier: <= 4 slots), no run-time test
 template <bool kTable = false>
@@ -1289,8 +1302,8 @@ __device__ __forceinline__ uint32_t rank_select_cum(uint32_t lo, uint32_t hi, ui
 // touched word, bit}. One chunk of <= 32 live items at a time (one live item per lane).
 // fold (pull): the passing colours of every item are also OR-ed into fold[slot * 32 + owner lane]
 // (W.B.w = bit | owner lane << 8 | slot << 16), the owners' per-colour early exit
-template <bool kTable = false>
-__device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
+template <bool kTable = false, class Scr = BmScratch>
+__device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, Scr& W, const uint32_t* sel8, int lane,
                                                    uint32_t nlive, unsigned long long& coins,
                                                    unsigned long long& atoms, bool& any_pass,
                                                    const uint32_t* sidt, uint32_t sbase,
@@ -1313,7 +1326,7 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
         for (uint32_t hb = __ballot_sync(kFull, heavy); hb; hb &= hb - 1) {
             const uint32_t hj = __ffs(hb) - 1;
             const uint4 it = W.A[c0 + hj];  // broadcast
-            const uint32_t sb = W.B[c0 + hj].x;
+            const uint32_t sb = item_sample0(W, c0 + hj, sbase);
             const uint64_t pe = (uint64_t)kPhiloxM * it.x;  // round 0's product: once for the item's 64 coins
             const uint32_t h0 = (uint32_t)(pe >> 32) ^ a.ic_keys[0], l0 = (uint32_t)pe;
             bool p0 = false, p1 = false;
@@ -1359,13 +1372,13 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
                 const bool act = k < ntask && !oheavy;
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
-                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
+                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, item_sample0(W, c0 + o, sbase) + bit), a.ic_keys);
                 if (act && (x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             } else if (k < ntask && !oheavy) {
                 const uint4 it = W.A[c0 + o];
                 const uint32_t bit = rank_select_cum(it.z, it.w, W.cum[o], k - eo, sel8);
-                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, W.B[c0 + o].x + bit), a.ic_keys);
+                const uint32_t x = philox_ks0(it.x, coin_sample<kTable>(a, sidt, sbase, item_sample0(W, c0 + o, sbase) + bit), a.ic_keys);
                 if ((x >> 1) < it.y)
                     atomicOr(reinterpret_cast<uint32_t*>(&W.pass[o]) + (bit >> 5), 1u << (bit & 31));
             }
@@ -1375,12 +1388,19 @@ __device__ __forceinline__ void bm_coins_and_merge(const BatchArgs& a, BmScratch
         if (has) {
             const unsigned long long pass = W.pass[lane];
             if (pass) {
-                const uint4 bb = W.B[j];
                 ++atoms;
-                BPT_CHECK(bb.y < a.slots_max * a.n && bb.z < (uint64_t)a.slots_max * a.tiles * 32, 7);
-                atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + bb.y, pass);
-                atomicOr(&a.touched[bb.z], 1u << (bb.w & 31u));
-                if (fold) atomicOr(&fold[((bb.w >> 16) & 3u) * 32 + ((bb.w >> 8) & 31u)], pass);  // several pending items per owner
+                if constexpr (std::is_same<Scr, BmScratchV>::value) {
+                    const uint32_t bw = W.B[j], u = bw & ((1u << 30) - 1u), sl = bw >> 30;
+                    BPT_CHECK(u < a.n && sl < a.slots_max, 7);
+                    atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + (size_t)u * a.slots_max + sl, pass);
+                    atomicOr(&a.touched[u >> 5], 1u << (u & 31u));
+                } else {
+                    const uint4 bb = W.B[j];
+                    BPT_CHECK(bb.y < a.slots_max * a.n && bb.z < (uint64_t)a.slots_max * a.tiles * 32, 7);
+                    atomicOr(reinterpret_cast<unsigned long long*>(a.VN) + bb.y, pass);
+                    atomicOr(&a.touched[bb.z], 1u << (bb.w & 31u));
+                    if (fold) atomicOr(&fold[((bb.w >> 16) & 3u) * 32 + ((bb.w >> 8) & 31u)], pass);  // several pending items per owner
+                }
                 any_pass = true;
             }
         }
@@ -1458,7 +1478,7 @@ __device__ __forceinline__ void expand_unit_bm(const BatchArgs& a, BmScratch& W,
 // the coin machinery. The items of a unit are flushed to the coins whenever the next slot's ballot
 // would overflow the warp's list.
 template <bool kWhole>
-__device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W, const uint32_t* sel8, int lane,
+__device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratchV& W, const uint32_t* sel8, int lane,
                                                 uint32_t le_mask, uint32_t unit, uint32_t rem, uint32_t jc0,
                                                 uint32_t mword, uint64_t gblk0, uint32_t nslots,
                                                 unsigned long long& coins, unsigned long long& atoms,
@@ -1547,7 +1567,7 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratch& W
         for (uint32_t sl = 0; sl < 4; ++sl) {  // unrolled: live[sl] stays in registers
             if (live[sl] != 0ull) {
                 W.A[pos] = make_uint4(e, rc[w].y, (uint32_t)live[sl], (uint32_t)(live[sl] >> 32));
-                W.B[pos] = make_uint4((uint32_t)(64ull * (gblk0 + sl)), u * S + sl, u >> 5, u & 31u);
+                W.B[pos] = u | (sl << 30);
                 ++pos;
             }
         }
@@ -1588,7 +1608,8 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
         return;
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BmScratch& W = reinterpret_cast<BmScratch*>(smem_raw)[threadIdx.x >> 5];
+    using Scr = std::conditional_t<kVmajor, BmScratchV, BmScratch>;
+    Scr& W = reinterpret_cast<Scr*>(smem_raw)[threadIdx.x >> 5];
     __shared__ unsigned long long red[kWarps];
     __shared__ uint32_t sel8[256];  // bit positions of every byte value, 3 bits each (rank_select64)
     __shared__ uint32_t sid_sh[kSidSlots * 64];
@@ -1624,7 +1645,7 @@ __global__ void __launch_bounds__(kThreads, BPT_BM_MINB) k_expand_bm(BatchArgs a
             nx_t = __ldg(&tstart[nxt]);
             nx_m = lane < kWinBm ? a.umask[(size_t)nxt * kWinBm + lane] : 0u;
         }
-        if (kVmajor) {
+        if constexpr (kVmajor) {
             if (unit < nfull)
                 expand_unit_bmv<true>(a, W, sel8, lane, le_mask, unit, kUnitBm, jc0, mword, gblk0, nslots, coins, atoms,
                                       any_pass, sidt, sbase);
@@ -2904,7 +2925,7 @@ void launch_level(const BatchArgs& a, uint32_t* tstart, uint64_t tstart_cap, cud
     compact_kernel(a)<<<g_compact_grid, kThreads, 0, st>>>(a, tstart, tstart_cap);
     if (ev0) BPT_CUDA(cudaEventRecord(ev0, st));
     if (a.model == BPT_IC && a.touched) {
-        if (a.vmajor) k_expand_bm<true><<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
+        if (a.vmajor) k_expand_bm<true><<<g_expand_grid_b, kThreads, sizeof(BmScratchV) * kWarps, st>>>(a, tstart, h0, 0);
         else k_expand_bm<false><<<g_expand_grid_b, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, tstart, h0, 0);
         if (a.pull) {
             k_expand_pull<<<g_expand_grid_p, kThreads, sizeof(BmScratch) * kWarps, st>>>(a, h0, 0);
@@ -3007,7 +3028,8 @@ cudaGraphExec_t build_sampling_graph(const BatchArgs& a, uint32_t* tstart, uint6
                      sizeof(WarpScratchW) * kWarps, exp_args)
         : a.model == BPT_IC && a.touched
         ? add_kernel(lbody, &n_cmp, a.vmajor ? (void*)k_expand_bm<true> : (void*)k_expand_bm<false>,
-                     dim3(g_expand_grid_b), dim3(kThreads), sizeof(BmScratch) * kWarps, exp_args)
+                     dim3(g_expand_grid_b), dim3(kThreads),
+                     a.vmajor ? sizeof(BmScratchV) * kWarps : sizeof(BmScratch) * kWarps, exp_args)
         : a.model == BPT_IC
         ? add_kernel(lbody, &n_cmp, a.colors == 64 ? (void*)k_expand_ic<true> : (void*)k_expand_ic<false>,
                      dim3(g_expand_grid), dim3(kThreads), sizeof(WarpScratch) * kWarps, exp_args)
