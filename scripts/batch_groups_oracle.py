@@ -16,7 +16,12 @@ import oracle  # noqa: E402
 
 
 def main():
-    batches = [int(x) for x in sys.argv[1:]] or [0, 40, 90]
+    args = sys.argv[1:]
+    group = 256
+    if args and args[0].startswith("--group="):
+        group = int(args[0].split("=")[1])
+        args = args[1:]
+    batches = [int(x) for x in args] or [0, 40, 90]
     cfg = graphgen.CONFIGS["C2"]
     row_ptr, col, thr = graphgen.make_graph(cfg)
     og = oracle.Graph(row_ptr, col, w_q31=thr)
@@ -32,14 +37,20 @@ def main():
            "seed": seed, "batches": {}}
     for b in batches:
         t = time.time()
-        grp = order[256 * b:256 * b + 256].astype(np.uint64)
+        grp = order[group * b:group * b + group].astype(np.uint64)
         w256 = og.group_work_ids(seed, grp)
+        if group != 256:  # exploration of wider batches: the fused group's work and its 256-sample halves
+            w4 = [og.group_work_ids(seed, grp[256 * i:256 * i + 256]) for i in range(group // 256)]
+            print(b, group, int(w256["e_phys"]), [int(w["e_phys"]) for w in w4], flush=True)
+            continue
         w64 = [og.group_work_ids(seed, grp[64 * i:64 * i + 64]) for i in range(4)]
         out["batches"][str(b)] = {"e_phys_256": int(w256["e_phys"]), "levels_256": int(w256["levels"]),
                                   "frontier_256": [int(x) for x in w256["frontier"]],
                                   "e_phys_4x64": [int(w["e_phys"]) for w in w64]}
         print(b, out["batches"][str(b)]["e_phys_256"], sum(out["batches"][str(b)]["e_phys_4x64"]),
               round(time.time() - t, 1), "s", flush=True)
+    if group != 256:
+        return
     path = os.path.join(ROOT, "tests", "golden", "c2_sorted_batch_groups_oracle.json")
     json.dump(out, open(path, "w"), indent=1)
     print(path)
