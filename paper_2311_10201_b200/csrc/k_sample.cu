@@ -2287,10 +2287,15 @@ __device__ __forceinline__ bool lt_pick_win(const uint32_t* __restrict__ roff, c
     if (lo >= hi) return false;
     uint32_t g = lo + (uint32_t)(((uint64_t)r * (hi - lo)) >> 31);
     g = min(g, hi - 1);
-    const uint32_t w0 = (g >= 3 ? g - 3 : 0u) & ~1u;  // 16-B aligned
+    const uint32_t w0 = (g >= 3 ? g - 3 : 0u) & ~3u;  // 32-B aligned: the window is two 256-bit loads
     if (w0 + 8 > m) return lt_pick(roff, rec, v, r, u_out);
-    const uint4* wp = reinterpret_cast<const uint4*>(rec + w0);
-    const uint4 q0 = __ldg(wp), q1 = __ldg(wp + 1), q2 = __ldg(wp + 2), q3 = __ldg(wp + 3);
+    uint4 q0, q1, q2, q3;
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w), "=r"(q1.x), "=r"(q1.y), "=r"(q1.z), "=r"(q1.w)
+        : "l"(rec + w0));
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(q2.x), "=r"(q2.y), "=r"(q2.z), "=r"(q2.w), "=r"(q3.x), "=r"(q3.y), "=r"(q3.z), "=r"(q3.w)
+        : "l"(rec + w0 + 4));
     const uint32_t xs[8] = {q0.x, q0.z, q1.x, q1.z, q2.x, q2.z, q3.x, q3.z};
     const uint32_t ys[8] = {q0.y, q0.w, q1.y, q1.w, q2.y, q2.w, q3.y, q3.w};
     const uint32_t a = max(lo, w0), b = min(hi, w0 + 8);  // window part inside the row (a < b)
