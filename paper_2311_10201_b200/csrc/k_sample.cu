@@ -98,6 +98,29 @@ __device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p) {
     return r;
 }
 
+// 256-bit loads / stores of a vertex's 4 slot masks (one 32-B sector, LDG/STG.E.ENL2.256)
+struct U4 { unsigned long long x, y, z, w; };
+__device__ __forceinline__ U4 ld_nc4(const unsigned long long* p) {
+    U4 r;
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ U4 ld_cg4(const unsigned long long* p) {
+    U4 r;
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w) : "l"(p), "l"(policy_evict_last()));
+    return r;
+}
+__device__ __forceinline__ U4 ld_plain4(const unsigned long long* p) {
+    U4 r;
+    asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st4(unsigned long long* p, unsigned long long x, unsigned long long y,
+                                    unsigned long long z, unsigned long long w) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" :: "l"(p), "l"(x), "l"(y), "l"(z), "l"(w) : "memory");
+}
+
 // coherent (L2) variant for loops that run several levels in one launch
 __device__ __forceinline__ ulonglong2 ld_keep_cg(const ulonglong2* p) {
     ulonglong2 r;
@@ -686,13 +709,9 @@ __global__ void __launch_bounds__(kThreads) k_compact_bmv(BatchArgs a, uint32_t*
                 BPT_CHECK(v < a.n, 9);
                 const size_t b = (size_t)v * S;
                 if (S == 4) {
-                    const ulonglong2 u01 = *reinterpret_cast<const ulonglong2*>(U + b);
-                    const ulonglong2 u23 = *reinterpret_cast<const ulonglong2*>(U + b + 2);
-                    const ulonglong2 v01 = *reinterpret_cast<const ulonglong2*>(V + b);
-                    const ulonglong2 v23 = *reinterpret_cast<const ulonglong2*>(V + b + 2);
-                    nm[0] = u01.x & ~v01.x; nm[1] = u01.y & ~v01.y; nm[2] = u23.x & ~v23.x; nm[3] = u23.y & ~v23.y;
-                    *reinterpret_cast<ulonglong2*>(V + b) = u01;
-                    *reinterpret_cast<ulonglong2*>(V + b + 2) = u23;
+                    const U4 uu = ld_plain4(U + b), vv = ld_plain4(V + b);
+                    nm[0] = uu.x & ~vv.x; nm[1] = uu.y & ~vv.y; nm[2] = uu.z & ~vv.z; nm[3] = uu.w & ~vv.w;
+                    st4(V + b, uu.x, uu.y, uu.z, uu.w);
                 } else {
 #pragma unroll
                     for (uint32_t sl = 0; sl < 4; ++sl)
@@ -727,8 +746,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_bmv(BatchArgs a, uint32_t*
                 a.qd[myq] = rs - (uint32_t)myoff;  // edge id e = work item + delta (mod 2^32)
                 unsigned long long* qm = a.qmask + (size_t)myq * S;
                 if (S == 4) {
-                    *reinterpret_cast<ulonglong2*>(qm) = make_ulonglong2(nm[0], nm[1]);
-                    *reinterpret_cast<ulonglong2*>(qm + 2) = make_ulonglong2(nm[2], nm[3]);
+                    st4(qm, nm[0], nm[1], nm[2], nm[3]);
                 } else {
 #pragma unroll
                     for (uint32_t sl = 0; sl < 4; ++sl)
@@ -1525,11 +1543,8 @@ __device__ __forceinline__ void expand_unit_bmv(const BatchArgs& a, BmScratchV& 
         unsigned long long live[4] = {0ull, 0ull, 0ull, 0ull};
         if (valid) {
             if (S == 4) {
-                const ulonglong2 m01 = __ldg(reinterpret_cast<const ulonglong2*>(qm));
-                const ulonglong2 m23 = __ldg(reinterpret_cast<const ulonglong2*>(qm) + 1);
-                const ulonglong2 u01 = ld_keep_cg(reinterpret_cast<const ulonglong2*>(Uu));
-                const ulonglong2 u23 = ld_keep_cg(reinterpret_cast<const ulonglong2*>(Uu) + 1);
-                live[0] = m01.x & ~u01.x; live[1] = m01.y & ~u01.y; live[2] = m23.x & ~u23.x; live[3] = m23.y & ~u23.y;
+                const U4 mm = ld_nc4(qm), uu = ld_cg4(Uu);
+                live[0] = mm.x & ~uu.x; live[1] = mm.y & ~uu.y; live[2] = mm.z & ~uu.z; live[3] = mm.w & ~uu.w;
             } else {
 #pragma unroll
                 for (uint32_t sl = 0; sl < 4; ++sl)
