@@ -26,6 +26,14 @@ __device__ __forceinline__ uint64_t digest_mix(uint64_t v) {
 
 constexpr int kFinThreads = 256;
 
+// 256-bit load / store of a vertex's 4 slot masks (one 32-B sector)
+__device__ __forceinline__ void ld4(const unsigned long long* p, unsigned long long (&m)[4]) {
+    asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(m[0]), "=l"(m[1]), "=l"(m[2]), "=l"(m[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st4z(unsigned long long* p) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %1, %1, %1};" :: "l"(p), "l"(0ull) : "memory");
+}
+
 // grid (ranges, slots). Block (r, slot) scans vertices [r*chunk, (r+1)*chunk) of the working
 // masks of in-flight block `slot` (= local block blk0+slot): writes V to the RRR store, clears
 // the working pair for the next batch and adds the occurrences. Each warp walks its own
@@ -161,9 +169,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* 
         unsigned long long m[4] = {0ull, 0ull, 0ull, 0ull};
         if (v < v_end) {
             if (S == 4) {
-                const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(V + v * 4);
-                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(V + v * 4 + 2);
-                m[0] = a.x; m[1] = a.y; m[2] = b.x; m[3] = b.y;
+                ld4(V + v * 4, m);
             } else {
 #pragma unroll
                 for (uint32_t s = 0; s < 4; ++s) m[s] = s < S ? V[v * S + s] : 0ull;
@@ -174,11 +180,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* 
             const bool any = (m[0] | m[1] | m[2] | m[3]) != 0ull;
             if (any) {
                 if (S == 4) {
-                    const ulonglong2 z = make_ulonglong2(0ull, 0ull);
-                    *reinterpret_cast<ulonglong2*>(V + v * 4) = z;
-                    *reinterpret_cast<ulonglong2*>(V + v * 4 + 2) = z;
-                    *reinterpret_cast<ulonglong2*>(UV + v * 4) = z;
-                    *reinterpret_cast<ulonglong2*>(UV + v * 4 + 2) = z;
+                    st4z(V + v * 4);
+                    st4z(UV + v * 4);
                 } else {
                     for (uint32_t s = 0; s < S; ++s) { V[v * S + s] = 0ull; UV[v * S + s] = 0ull; }
                 }
