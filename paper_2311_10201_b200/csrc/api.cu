@@ -600,6 +600,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.blocks = S.blocks;
     // sorted start vertices (IC touched-bitmap form; k_order.cu)
     S.sorted = bitmap && !(opt.flags & BPT_FLAG_UNSORTED);
+    S.lazy_sizes = vmajor;  // k_finalize_v leaves the sizes to ensure_sizes
+    if (vmajor) S.blk_sized.assign(S.blocks, 0);
     if (S.sorted) {
         S.slot_sample.alloc(nlocal * 4);
         S.sample_slot.alloc(nlocal * 4);
@@ -1067,6 +1069,7 @@ bpt_status bpt_rrr_sizes(const bpt_samples* s, uint64_t first, uint64_t count, u
         check_range(s->s, first, count);
         use_device(s->s.device);
         StreamScope scope(s->s.stream);
+        ensure_sizes(const_cast<Samples&>(s->s), first, count, s->s.stream);
         copy_out(sizes, s->s.sizes.as<uint32_t>() + (first - s->s.s0), count * 4, s->s.stream);
         BPT_CUDA(cudaStreamSynchronize(s->s.stream));
     });
@@ -1098,6 +1101,7 @@ bpt_status bpt_rrr_extract(const bpt_samples* s, uint64_t first, uint64_t count,
         const cudaStream_t st = S.stream;
         StreamScope scope(st);
         std::vector<uint32_t> sz(count);
+        ensure_sizes(const_cast<Samples&>(S), first, count, st);
         BPT_CUDA(cudaMemcpyAsync(sz.data(), S.sizes.as<uint32_t>() + (first - S.s0), count * 4, cudaMemcpyDeviceToHost, st));
         BPT_CUDA(cudaStreamSynchronize(st));
         std::vector<uint64_t> off(count + 1, 0);

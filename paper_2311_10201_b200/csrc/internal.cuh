@@ -179,6 +179,10 @@ struct Samples {
     DevBuf slot_sample;   // u32[nlocal]: global sample id of local slot j
     DevBuf sample_slot;   // u32[nlocal]: local slot of local sample i
     std::vector<uint32_t> h_sample_slot;  // host copy, on demand (extraction)
+    // batch-wide frontier: the finaliser leaves the per-sample sizes to a pass over the store blocks a
+    // sizes / extraction / list request touches (ensure_sizes); blk_sized marks the blocks done
+    bool lazy_sizes = false;
+    std::vector<uint8_t> blk_sized;
     // multi-rank sparse selection: every rank's lists gathered once (offsets over all ranks'
     // samples, padded members, global occurrence counts)
     DevBuf g_off, g_mem, g_count0;
@@ -292,6 +296,8 @@ constexpr uint32_t kWide = BPT_WIDE_BLOCKS;  // blocks (x 64 colours) per wide f
 #endif
 constexpr uint32_t kUnitWide = BPT_UNIT_WIDE;  // work items per wide expansion unit (windows of 32)
 // k_store.cu
+// per-sample sizes of local samples [first, first + count) present in S.sizes (a no-op unless S.lazy_sizes)
+void ensure_sizes(Samples& S, uint64_t first, uint64_t count, cudaStream_t st);
 // umode: 0 {V, N} pairs, 1 slot-major union layout, 2 vertex-major union layout (a.vmajor)
 void launch_finalize(const Samples& S, ulonglong2* VN, const Ctl* ctl, uint32_t slots_max, const uint32_t* roff,
                      cudaStream_t st, unsigned long long* d_elog, bool wide, int umode);

@@ -240,6 +240,8 @@ static bool build_lists(const Samples& S, cudaStream_t st) {
     // lists pay off when they are much smaller than one pass over the store
     if (nlocal == 0 || bytes > free_b / 4 || bytes * 8 > S.store.bytes) return M.lists_ok = false;
     std::vector<uint32_t> sz(nlocal);
+    ensure_sizes(M, S.s0, nlocal, st);
+    BPT_CUDA(cudaStreamSynchronize(st));
     BPT_CUDA(cudaMemcpy(sz.data(), S.sizes.p, nlocal * 4, cudaMemcpyDeviceToHost));
     if (S.sorted) {  // the lists follow the store: one per slot (the slot's sample's size)
         std::vector<uint32_t> slot_sample(nlocal), by_slot(nlocal);

@@ -151,8 +151,6 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* 
                                                             uint32_t* __restrict__ count0, uint32_t S,
                                                             const uint32_t* __restrict__ slot_sample, uint64_t s0) {
     constexpr int kW = kFinThreads / 32;
-    __shared__ unsigned long long s_mask[kW][32];
-    __shared__ uint32_t s_size[kW][4][64];
     __shared__ unsigned long long s_el[kW];
     if (blockIdx.x == 0 && threadIdx.x == 0)  // launch evidence (Ctl::kernels_run)
         atomicAdd(&const_cast<Ctl*>(ctl)->kernels_run, 1ull);
@@ -162,7 +160,6 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* 
     const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
     const uint64_t v_end = umin64(v_begin + chunk, n);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t sz[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
     unsigned long long el = 0;
     for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
         const uint64_t v = base + lane;
@@ -190,43 +187,61 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_v(unsigned long long* 
                 el += (unsigned long long)pc * (roff[v + 1] - roff[v]);  // E_logical: unfused reads
             }
         }
-#pragma unroll
-        for (uint32_t s = 0; s < 4; ++s) {
-            uint32_t b = __ballot_sync(0xffffffffu, m[s] != 0ull);
-            if (!b) continue;
-            s_mask[wid][lane] = m[s];
-            __syncwarp();
-            while (b) {
-                const int j = __ffs(b) - 1;
-                b &= b - 1;
-                const unsigned long long mj = s_mask[wid][j];
-                sz[s][0] += (uint32_t)(mj >> lane) & 1u;
-                sz[s][1] += (uint32_t)(mj >> (lane + 32)) & 1u;
-            }
-            __syncwarp();
-        }
-    }
-#pragma unroll
-    for (uint32_t s = 0; s < 4; ++s) {
-        s_size[wid][s][lane] = sz[s][0];
-        s_size[wid][s][lane + 32] = sz[s][1];
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) el += __shfl_xor_sync(0xffffffffu, el, d);
     if (lane == 0) s_el[wid] = el;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < 4 * 64; i += kFinThreads) {
-        const uint32_t s = i / 64, c = i % 64;
-        if (s >= nsl) continue;
-        uint32_t T = 0;
-        for (int q = 0; q < kW; ++q) T += s_size[q][s][c];
-        const uint64_t li = 64ull * (blk0 + s) + c;  // local slot = local sample index unless start-sorted
-        if (li < nlocal && T) atomicAdd(&sizes[slot_sample ? slot_sample[li] - s0 : li], T);
-    }
     if (threadIdx.x == 0) {
         unsigned long long E = 0;
         for (int q = 0; q < kW; ++q) E += s_el[q];
         if (E) atomicAdd(elog_total, E);
+    }
+}
+
+
+// Per-sample sizes of listed store blocks (the batch-wide frontier's finaliser leaves them to the
+// requests that need them, see ensure_sizes): block (r, j) counts, per colour, the set bits of
+// vertices [r chunk, (r + 1) chunk) of store block blk[j] (lane l counts colours l and l + 32 of the
+// warp's non-zero masks, broadcast from shared memory).
+__global__ void __launch_bounds__(kFinThreads) k_block_sizes(const uint64_t* __restrict__ store, uint32_t n,
+                                                             uint64_t chunk, const uint64_t* __restrict__ blk,
+                                                             uint64_t nlocal, const uint32_t* __restrict__ slot_sample,
+                                                             uint64_t s0, uint32_t* __restrict__ sizes) {
+    constexpr int kW = kFinThreads / 32;
+    __shared__ unsigned long long s_mask[kW][32];
+    __shared__ uint32_t s_size[kW][64];
+    const uint64_t b = blk[blockIdx.y];
+    const uint64_t* V = store + (size_t)b * n;
+    const uint64_t v_begin = (uint64_t)blockIdx.x * chunk;
+    const uint64_t v_end = umin64(v_begin + chunk, n);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t sz_lo = 0, sz_hi = 0;
+    for (uint64_t base = v_begin + 32ull * wid; base < v_end; base += 32ull * kW) {
+        const uint64_t v = base + lane;
+        const uint64_t m = v < v_end ? V[v] : 0ull;
+        uint32_t bl = __ballot_sync(kFull, m != 0);
+        if (!bl) continue;
+        s_mask[wid][lane] = m;
+        __syncwarp();
+        while (bl) {
+            const int j = __ffs(bl) - 1;
+            bl &= bl - 1;
+            const unsigned long long mj = s_mask[wid][j];
+            sz_lo += (uint32_t)(mj >> lane) & 1u;
+            sz_hi += (uint32_t)(mj >> (lane + 32)) & 1u;
+        }
+        __syncwarp();
+    }
+    s_size[wid][lane] = sz_lo;
+    s_size[wid][lane + 32] = sz_hi;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int c = threadIdx.x;
+        uint32_t T = 0;
+        for (int q = 0; q < kW; ++q) T += s_size[q][c];
+        const uint64_t li = 64ull * b + c;  // local slot
+        if (li < nlocal && T) atomicAdd(&sizes[slot_sample ? slot_sample[li] - s0 : li], T);
     }
 }
 
@@ -467,6 +482,36 @@ void add_store_nodes(cudaGraph_t g, cudaGraphNode_t dep, const Samples& S, ulong
 }
 
 // d_offsets[count+1] must already hold the exclusive scan of sizes (offsets[count] = total)
+void ensure_sizes(Samples& S, uint64_t first, uint64_t count, cudaStream_t st) {
+    if (!S.lazy_sizes || count == 0) return;
+    const uint64_t lfirst = first - S.s0;
+    if (S.sorted && S.h_sample_slot.empty()) {
+        S.h_sample_slot.resize(S.s1 - S.s0);
+        BPT_CUDA(cudaMemcpyAsync(S.h_sample_slot.data(), S.sample_slot.p, (S.s1 - S.s0) * 4, cudaMemcpyDeviceToHost, st));
+        BPT_CUDA(cudaStreamSynchronize(st));
+    }
+    std::vector<uint64_t> need;
+    for (uint64_t i = 0; i < count; ++i) {
+        const uint64_t slot = S.sorted ? S.h_sample_slot[lfirst + i] : lfirst + i;
+        const uint64_t b = slot / 64;
+        if (!S.blk_sized[b]) { S.blk_sized[b] = 1; need.push_back(b); }
+    }
+    if (need.empty()) return;
+    uint64_t chunk = 0;
+    const dim3 grid = finalize_grid(S.n, 1, &chunk);
+    constexpr uint64_t kGroup = 1024;
+    DevBuf dblk(umin64(need.size(), kGroup) * 8);
+    for (uint64_t g0 = 0; g0 < need.size(); g0 += kGroup) {
+        const uint64_t nb = umin64(kGroup, need.size() - g0);
+        BPT_CUDA(cudaMemcpyAsync(dblk.p, need.data() + g0, nb * 8, cudaMemcpyHostToDevice, st));
+        k_block_sizes<<<dim3(grid.x, (unsigned)nb), kFinThreads, 0, st>>>(
+            S.store.as<uint64_t>(), S.n, chunk, dblk.as<uint64_t>(), S.s1 - S.s0,
+            S.sorted ? S.slot_sample.as<uint32_t>() : nullptr, S.s0, S.sizes.as<uint32_t>());
+        count_launch();
+        ::bpt::check_cuda(cudaGetLastError(), "launch k_block_sizes");
+    }
+}
+
 void extract_range(const Samples& S, uint64_t first, uint64_t count, const uint64_t* h_offsets, uint32_t* d_members,
                    cudaStream_t st) {
     const uint32_t n = S.n;
