@@ -13,6 +13,8 @@
  *   - Pointer arguments are plain pointers to HOST or DEVICE memory; the library
  *     detects which (cudaPointerGetAttributes). Input arrays are caller-owned and
  *     copied: the library never retains a caller pointer after the call returns.
+ *     Host buffers may be pageable; page-locked (pinned) ones are copied at full PCIe /
+ *     C2C rate with no staging (large member extractions: pass a reused pinned buffer).
  *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
  *     Calls are synchronous with respect to the host on return (results are ready).
  *   - Handles own their device memory until the matching *_free (NULL-safe).
