@@ -333,9 +333,17 @@ def test_ragged_theta_and_ranges(bpt):
             a, b = int(ref["offsets"][first]), int(ref["offsets"][first + count])
             assert np.array_equal(mem, ref["members"][a:b])
             assert np.array_equal(off, ref["offsets"][first:first + count + 1] - ref["offsets"][first])
+            # pinned host buffers with spare capacity (bench.py's end-to-end path)
+            import torch
+            pm = torch.full((b - a + 7,), 0xABCD, dtype=torch.int32).pin_memory()
+            po = torch.empty(count + 1, dtype=torch.int64).pin_memory()
+            s.extract(first, count, offsets=po, members=pm, capacity=pm.numel())
+            assert np.array_equal(pm.numpy()[: b - a].view(np.uint32), ref["members"][a:b])
+            assert (pm.numpy()[b - a:] == 0xABCD).all()
+            assert np.array_equal(po.numpy().view(np.uint64), ref["offsets"][first:first + count + 1] - ref["offsets"][first])
 
 
-@pytest.mark.parametrize("mode", ["ic", "ic_queue", "ic_wide", "lt", "lt_dense", "lt_fused"])
+@pytest.mark.parametrize("mode",["ic", "ic_queue", "ic_wide", "lt", "lt_dense", "lt_fused"])
 def test_graph_without_edges(bpt, mode):
     n = 10
     flags = {"lt_dense": bpt.FLAG_LT_DENSE, "lt_fused": bpt.FLAG_LT_FUSED, "ic_queue": bpt.FLAG_QUEUE}.get(mode, 0)
