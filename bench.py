@@ -439,7 +439,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "config": {"workload": workload_desc(cfg), "theta": cfg.theta, "colors": cfg.colors, "k": cfg.k,
                    "step": f"graph_load + sample + extract({EXTRACT_SAMPLES}/rank) + select_seeds(k={cfg.k})",
                    "seeds": f"sampling seed rotates over {cfg.seed:#x} + (0, 1, 2) across steps",
-                   "l2": "inputs and 39.7 GB store >> 126 MB L2 (no flush needed)",
+                   "l2": (f"graph input {(row_ptr.nbytes + col.nbytes + thr.nbytes) / 1e6:.0f} MB and "
+                          f"{float(np.mean([i['store_bytes'] for i in infos])) / 1e9:.1f} GB store per rank, "
+                          "each step rewrites its store: >> 126 MB L2 (no flush needed)"),
                    "parallelism": f"sample-sharded x{world} (NCCL in selection only)"},
         "edges_visited_per_s": e_phys_all / (ms_max / 1000.0),
         "unfused_equiv_edges_per_s": e_log_all / (ms_max / 1000.0),
