@@ -161,9 +161,10 @@ typedef struct {
                                    launch per batch */
 #define BPT_FLAG_QUEUE 128u     /* IC, 64 colours: discovered vertices through a first-setter
                                    queue (atomicOr with return) instead of the touched bitmap */
-/* IC, 64 colours (touched-bitmap form): samples are assigned to the traversal slots in the order
+/* IC, 64 colours (touched-bitmap form) and 1 < C < 64: samples are assigned to the traversal slots in the order
  * of their start vertices (in-degree descending, then start id, then sample id; "sorting the
- * starting vertices"), so samples with large reverse BPTs share groups.
+ * starting vertices"), so samples with large reverse BPTs share groups
+ * (a C-colour group = C samples adjacent in that order).
  * On by default; this flag keeps sample s in slot s (groups of consecutive samples, reading C-9).
  * RRR sets, sizes, digests and seeds are identical either way; E_phys / levels differ. */
 #define BPT_FLAG_UNSORTED 256u

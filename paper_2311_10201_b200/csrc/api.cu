@@ -599,7 +599,8 @@ static void run_sampling(Samples& S, const bpt_sample_opts& opt, cudaStream_t st
     a.slots_max = (uint32_t)slots;
     a.blocks = S.blocks;
     // sorted start vertices (IC touched-bitmap form; k_order.cu)
-    S.sorted = bitmap && !(opt.flags & BPT_FLAG_UNSORTED);
+    // (and the C < 64 queue form: its C-colour groups become C samples adjacent in start order)
+    S.sorted = (bitmap || (S.model == BPT_IC && C > 1 && C < 64 && !wide)) && !(opt.flags & BPT_FLAG_UNSORTED);
     S.lazy_sizes = vmajor;  // k_finalize_v leaves the sizes to ensure_sizes
     if (vmajor) S.blk_sized.assign(S.blocks, 0);
     if (S.sorted) {

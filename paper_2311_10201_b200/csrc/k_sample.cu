@@ -222,12 +222,20 @@ __global__ void k_init(BatchArgs a, cudaGraphConditionalHandle h_level, int use_
             mark_start(a, slot, start, bit);
             continue;
         }
+        uint32_t st = start;
+        if (a.slot_sample) {  // sorted start vertices (C < 64 queue form): the slot holds another sample
+            const uint64_t li = 64ull * (a.ctl->blk0 + slot) + bit;
+            if (li >= a.nlocal) continue;
+            const uint2 w2 = philox2x32_10(a.slot_sample[li], 0u, a.k_start);
+            st = (uint32_t)__umul64hi(((uint64_t)w2.y << 32) | w2.x, (uint64_t)a.n);
+            BPT_CHECK(st < a.n, 12);
+        }
         const uint32_t slice = bit / a.colors;
         const uint64_t smask = slice_mask_of(a.colors, slice);
-        const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + start].y, 1ull << bit);
+        const unsigned long long old = atomicOr(&a.VN[(size_t)slot * a.n + st].y, 1ull << bit);
         if ((old & smask) == 0) {
             const unsigned pos = atomicAdd(&a.lv[0].raw, 1u);
-            if (pos < a.raw_cap) a.raw[pos] = raw_pack(start, slot, slice);
+            if (pos < a.raw_cap) a.raw[pos] = raw_pack(st, slot, slice);
             else a.lv[0].overflow = 1;
         }
     }
@@ -949,7 +957,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x, int lane) {
 }
 
 __device__ __forceinline__ void coin_task(const BatchArgs& a, WarpScratch& W, uint32_t o, uint32_t w, uint32_t bit) {
-    const uint32_t x = philox2x32_10(W.e[w][o], W.sbase[w][o] + bit, a.k_ic).x;
+    // sorted start vertices (C < 64): sbase is the slot's local index, mapped to its sample
+    const uint32_t sid = a.slot_sample ? __ldg(&a.slot_sample[W.sbase[w][o] + bit]) : W.sbase[w][o] + bit;
+    const uint32_t x = philox2x32_10(W.e[w][o], sid, a.k_ic).x;
     if ((x >> 1) < W.thr[w][o])
         atomicOr(reinterpret_cast<uint32_t*>(&W.pass[w][o]) + (bit >> 5), 1u << (bit & 31));
 }
@@ -1120,7 +1130,7 @@ __device__ __forceinline__ void expand_ic_body(const BatchArgs& a, const uint32_
                                                cudaGraphConditionalHandle h_level, int use_cond) {
     Ctl* ctl = a.ctl;
     const uint32_t level = LDX(&ctl->level);
-    const uint64_t gblk0 = LDX(&ctl->gblk0);
+    const uint64_t gblk0 = a.slot_sample ? LDX(&ctl->blk0) : LDX(&ctl->gblk0);  // sorted: local slot base
     const LevelRec* L = &a.lv[level];
     LevelRec* Ln = &a.lv[level + 1];
     const unsigned long long packed = LDX(&L->packed);

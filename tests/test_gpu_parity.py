@@ -284,9 +284,9 @@ def test_c1_full_parity(bpt, colors):
         info = s.info
         # exact work counters: E_phys = sum over traversal groups of the
         # distinct (v, level) pairs weighted by in-degree; E_logical = unfused reads. With 64
-        # colours the samples are in sorted start order (BPT_FLAG_UNSORTED off) and a batch of
+        # colours (and 1 < C < 64) the samples are in sorted start order (BPT_FLAG_UNSORTED off); at 64: a batch of
         # <= 4 blocks shares one frontier (BPT_FLAG_SLOTWISE off): one group per batch
-        order = (sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed) if colors == 64
+        order = (sorted_slots(row_ptr, col, cfg.n, cfg.theta, cfg.seed) if colors > 1  # C = 1: no sort
                  else np.arange(cfg.theta))
         group = 64 * info["batch_groups"] if colors == 64 and info["batch_groups"] <= 4 else colors
         e_phys = sum(w["e_phys"] for w in group_e_phys(ref["g"], cfg.seed, order, group))
@@ -404,7 +404,7 @@ def test_level_loop_variants(bpt, model):
         g = bpt.Graph(row_ptr, col, w_q31=thr)
         # consecutive-sample 64-colour groups in both forms (equal work counters), then the default
         # (sorted slots, one frontier per batch)
-        variants = [bpt.FLAG_UNSORTED | bpt.FLAG_SLOTWISE, bpt.FLAG_QUEUE, 0]
+        variants = [bpt.FLAG_UNSORTED | bpt.FLAG_SLOTWISE, bpt.FLAG_QUEUE | bpt.FLAG_UNSORTED, 0]
     else:
         cfg = graphgen.scaled(graphgen.CONFIGS["C3"], 1 << 12, theta=2048)
         row_ptr, col, thr = graphgen.make_graph(cfg)
