@@ -46,6 +46,7 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
     dist.broadcast_object_list(uid, src=0)
     comm = bpt.Comm(world, rank, rank, uid[0])
     kw = dict(kw or {})
+    colors = kw.pop("colors", 64)
     model = bpt.IC if cfg.model == "IC" else bpt.LT
     if kw.pop("bcast", False):  # collective load: only rank 0's arrays are read
         g = bpt.Graph(row_ptr if rank == 0 else None, col if rank == 0 else None, w_q31=thr if rank == 0 else None,
@@ -56,7 +57,7 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
         ref.close()
     else:
         g = bpt.Graph(row_ptr, col, w_q31=thr, model=model, comm=comm)
-    s = g.sample(theta, colors=64, seed=cfg.seed, **kw)
+    s = g.sample(theta, colors=colors, seed=cfg.seed, **kw)
     sizes = s.sizes(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint32)
     digests = s.digests(s.s0, s.s1 - s.s0) if s.s1 > s.s0 else np.zeros(0, np.uint64)
     seeds, gains, sigma = s.select_seeds(cfg.k)
@@ -68,7 +69,7 @@ def _rank_main(rank, world, port, cfg_name, n_scaled, theta, q, kw=None):
 
 
 MODES = {"ic": ("C2", 1 << 14, {}), "ic_wide": ("C2", 1 << 14, {"wide": True}),
-         "ic_bcast": ("C2", 1 << 14, {"bcast": True}),
+         "ic_bcast": ("C2", 1 << 14, {"bcast": True}), "ic_c8": ("C2", 1 << 14, {"colors": 8}),
          "lt": ("C3", 1 << 13, {}), "lt_sparse": ("C3", 1 << 13, {"sparse": True})}
 
 
