@@ -33,7 +33,7 @@ FLAG_LT_DENSE = 16  # LT walks: dense store
 FLAG_LT_REWALK = 32  # LT sparse store: member lists by a second walk
 FLAG_LT_LEVELS = 64  # LT fused: per-level launches instead of one cooperative launch per batch
 FLAG_QUEUE = 128  # IC 64 colours: first-setter queue instead of the touched bitmap
-FLAG_UNSORTED = 256  # IC 64 colours: sample s in slot s (no start-vertex sort)
+FLAG_UNSORTED = 256  # IC, 1 < C <= 64: sample s in slot s (no start-vertex sort)
 FLAG_PULL = 512  # IC 64 colours: pull expansion of the heavy levels (direction switching)
 FLAG_SLOTWISE = 1024  # IC 64 colours: one frontier per 64-sample block instead of one per batch
 _STATUS = {0: "BPT_OK", -1: "BPT_EINVAL", -2: "BPT_ENOMEM", -3: "BPT_ECUDA", -4: "BPT_ENCCL", -5: "BPT_ESTATE"}
